@@ -1,0 +1,842 @@
+// Session: Algorithm-1 memory planning over one HBM arena, event-based
+// multi-stream dispatch, CUDA-graph capture/replay with a plan cache.
+#include "opflow/engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <numeric>
+
+#include "opflow/json.hpp"
+
+namespace opflow {
+
+namespace {
+
+constexpr int64_t kAlign = 256;
+int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+int64_t tensor_bytes_rows(const TensorMeta& m, int64_t rows) {
+  return rows * m.row_elems() * dtype_bytes(m.dtype);
+}
+
+// Lane-aware block allocator: a freed block is handed out again only to a
+// dispatch that happens-after every previous user (vector clocks over lanes).
+struct Block {
+  int64_t off = 0, bytes = 0;
+  bool live = false;
+  bool pinned = false;  // graph outputs: never recycled
+  std::vector<int32_t> users;
+};
+
+struct Planner {
+  std::vector<Block> blocks;
+  int64_t top = 0, live = 0, peak = 0;
+  const std::vector<std::vector<int32_t>>* vc = nullptr;  // per dispatch
+  const std::vector<int32_t>* lane_of = nullptr;
+  const std::vector<int32_t>* seq_of = nullptr;
+
+  bool hb(int32_t x, int32_t d) const {
+    if (x == d) return true;
+    return (*vc)[d][(*lane_of)[x]] >= (*seq_of)[x];
+  }
+  int32_t alloc(int64_t bytes, int32_t d, bool pinned = false) {
+    bytes = align_up(std::max<int64_t>(bytes, 1));
+    int32_t best = -1;
+    if (!pinned) {
+      for (int32_t i = 0; i < static_cast<int32_t>(blocks.size()); ++i) {
+        const Block& b = blocks[i];
+        if (b.live || b.pinned || b.bytes < bytes) continue;
+        if (best >= 0 && blocks[best].bytes <= b.bytes) continue;
+        bool ok = true;
+        for (int32_t u : b.users) ok = ok && hb(u, d);
+        if (ok) best = i;
+      }
+    }
+    if (best < 0) {
+      Block b;
+      b.off = top;
+      b.bytes = bytes;
+      top += bytes;
+      blocks.push_back(b);
+      best = static_cast<int32_t>(blocks.size()) - 1;
+    }
+    Block& b = blocks[best];
+    b.live = true;
+    b.pinned = pinned;
+    b.users.assign(1, d);
+    live += b.bytes;
+    peak = std::max(peak, live);
+    return best;
+  }
+  void use(int32_t blk, int32_t d) {
+    auto& u = blocks[blk].users;
+    if (std::find(u.begin(), u.end(), d) == u.end()) u.push_back(d);
+  }
+  void release(int32_t blk) {
+    Block& b = blocks[blk];
+    if (!b.live || b.pinned) return;
+    b.live = false;
+    live -= b.bytes;
+  }
+};
+
+struct InstBinding {
+  int32_t block = -1;
+  int64_t row_off = 0;   // rows into the block
+  int32_t producer = -1; // dispatch id
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ Session
+Session::Session(const Graph& g, const PartitionPlan& p, SessionConfig cfg, opf_comm* comm)
+    : g_(g), p_(p), cfg_(cfg), comm_(comm) {
+  lanes_.assign(std::max(1, cfg_.lanes), nullptr);
+  ext_.assign(g_.tensors.size(), opf_view{});
+  prepacked_.assign(g_.tensors.size(), nullptr);
+  if (cfg_.device < 0) return;  // dry session
+  OPF_CUDA(cudaSetDevice(cfg_.device));
+  for (auto& s : lanes_) OPF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+}
+
+std::unique_ptr<Session> Session::dry(const Graph& g, const PartitionPlan& p, SessionConfig cfg,
+                                      int64_t rows) {
+  cfg.device = -1;
+  auto s = std::make_unique<Session>(g, p, cfg, nullptr);
+  s->dry_ = true;
+  s->dry_rows_ = rows;
+  return s;
+}
+
+Session::~Session() {
+  if (dry_) return;
+  for (auto& kv : cache_)
+    if (kv.second->exec) cudaGraphExecDestroy(kv.second->exec);
+  for (auto& s : lanes_) cudaStreamDestroy(s);
+  for (auto& e : events_) cudaEventDestroy(e);
+  for (void* p : prepacked_)
+    if (p) cudaFree(p);
+  for (auto& kv : perms_) cudaFree(kv.second);
+  if (arena_) cudaFree(arena_);
+}
+
+void Session::bind(const std::string& name, const opf_view& v) {
+  const int32_t t = g_.tensor_id(name);
+  const TensorMeta& m = g_.tensors[t];
+  require(m.role != TensorRole::kIntermediate, Errc::ConfigError,
+          "tensor '" + name + "' is an intermediate; only inputs, weights and outputs bind");
+  require(v.dtype == static_cast<int32_t>(m.dtype), Errc::ShapeMismatch,
+          "binding dtype mismatch for '" + name + "'");
+  require(v.rank == static_cast<int32_t>(m.shape.size()), Errc::ShapeMismatch,
+          "binding rank mismatch for '" + name + "'");
+  for (int d = (m.batch == BatchSemantics::kBatched ? 1 : 0); d < v.rank; ++d)
+    require(v.shape[d] == m.shape[d], Errc::ShapeMismatch,
+            "binding extent mismatch for '" + name + "'");
+  require(v.base != nullptr, Errc::MissingBinding, "null binding for '" + name + "'");
+  const bool changed = ext_[t].base != v.base || ext_[t].elem_offset != v.elem_offset ||
+                       ext_[t].shape[0] != v.shape[0];
+  ext_[t] = v;
+  if (changed) {
+    if (m.role == TensorRole::kWeight) {
+      prepack_dirty_ = true;
+      if (prepacked_[t]) {
+        cudaFree(prepacked_[t]);
+        prepacked_[t] = nullptr;
+      }
+    }
+    // captured graphs embed pointers: drop them (plans are rebuilt lazily)
+    for (auto& kv : cache_)
+      if (kv.second->exec) {
+        cudaGraphExecDestroy(kv.second->exec);
+        kv.second->exec = nullptr;
+      }
+  }
+}
+
+int64_t Session::rows() const {
+  if (dry_) return dry_rows_;
+  int64_t rows = 0;
+  for (int32_t t : g_.graph_inputs) {
+    const TensorMeta& m = g_.tensors[t];
+    require(ext_[t].base != nullptr, Errc::MissingBinding,
+            "no binding for tensor '" + m.name + "'");
+    if (m.batch != BatchSemantics::kBatched) continue;
+    if (rows == 0) rows = ext_[t].shape[0];
+    require(ext_[t].shape[0] == rows, Errc::ShapeMismatch, "batched inputs disagree on rows");
+  }
+  for (int32_t t : g_.weights)
+    require(ext_[t].base != nullptr, Errc::MissingBinding,
+            "no binding for tensor '" + g_.tensors[t].name + "'");
+  return rows == 0 ? 1 : rows;
+}
+
+void Session::ensure_prepacked(cudaStream_t s) {
+  if (!prepack_dirty_) return;
+  // MatMul bf16 weights are [K,N] (reference layout); the tcgen05 GEMM wants
+  // K-major B, i.e. [N,K]: transpose once per binding.
+  for (const OperatorNode& op : g_.ops) {
+    if (op.kind != OperatorKind::kMatMul) continue;
+    const int32_t w = op.inputs[1];
+    const TensorMeta& m = g_.tensors[w];
+    if (m.dtype != Dtype::kBF16 || m.role != TensorRole::kWeight || prepacked_[w]) continue;
+    OPF_CUDA(cudaMalloc(&prepacked_[w], m.numel() * 2));
+    k_transpose_bf16(view_ptr(ext_[w]), prepacked_[w], m.shape[0], m.shape[1], s);
+  }
+  OPF_CUDA(cudaGetLastError());
+  prepack_dirty_ = false;
+}
+
+void Session::warm_aux(const CompiledPlan& cp) {
+  for (const PlannedDispatch& pd : cp.dispatches)
+    for (const PlannedLaunch& l : pd.launches)
+      if (!l.is_copy && l.fn.empty() && l.kind == OperatorKind::kAllToAll)
+        alltoall_perm_device(l.attrs.seed, l.in[0].shape.size() > 1 ? l.in[0].shape[1] : 1);
+}
+
+void Session::ensure_arena(int64_t bytes) {
+  if (bytes <= arena_bytes_) return;
+  if (arena_) {
+    OPF_CUDA(cudaDeviceSynchronize());
+    OPF_CUDA(cudaFree(arena_));
+  }
+  OPF_CUDA(cudaMalloc(&arena_, bytes));
+  arena_bytes_ = bytes;
+}
+
+std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const std::string& key) {
+  auto cp = std::make_unique<CompiledPlan>();
+  cp->key = key;
+  const auto& ds = ctx.dispatches();
+  const int32_t nd = static_cast<int32_t>(ds.size());
+  SchedContext& mctx = const_cast<SchedContext&>(ctx);
+  const std::vector<int64_t> sizes = mctx.sizes();
+  const int32_t U = static_cast<int32_t>(sizes.size());
+  std::vector<int64_t> offs(U + 1, 0);
+  for (int32_t u = 0; u < U; ++u) offs[u + 1] = offs[u] + sizes[u];
+  const int64_t total_rows = offs[U];
+
+  SplitSignature sig;
+  sig.sizes = sizes;
+  for (const Dispatch& d : ds)
+    if (d.kind == Dispatch::Kind::kMerged) sig.merge_set.insert(d.subgraphs[0]);
+  std::vector<MicroBatchContext> mb = static_analysis(g_, p_, sig);
+  cp->analysis_ops += static_cast<int64_t>(g_.tensors.size()) * U + p_.size();
+  if (!cfg_.prealloc)
+    for (auto& c : mb)
+      for (auto& st : c.states) st.prealloc = false;
+
+  const int L = static_cast<int>(lanes_.size());
+  std::vector<std::vector<int32_t>> vc(nd, std::vector<int32_t>(L, 0));
+  std::vector<int32_t> lane_of(nd), seq_of(nd), lane_last(L, -1), lane_seq(L, 0);
+  Planner pl;
+  pl.vc = &vc;
+  pl.lane_of = &lane_of;
+  pl.seq_of = &seq_of;
+
+  const int32_t NT = static_cast<int32_t>(g_.tensors.size());
+  std::vector<std::vector<InstBinding>> inst(NT, std::vector<InstBinding>(U));
+  std::vector<int32_t> merge_buf(NT, -1);  // full-batch block of prealloc / output tensors
+  std::vector<int32_t> block_pending;      // live (t,u) slices per block
+  auto pending = [&](int32_t b) -> int32_t& {
+    if (static_cast<int32_t>(block_pending.size()) <= b) block_pending.resize(b + 1, 0);
+    return block_pending[b];
+  };
+
+  // Graph outputs not bound by the caller live in pinned arena blocks.
+  for (int32_t t : g_.graph_outputs)
+    if (!ext_[t].base) {
+      merge_buf[t] = pl.alloc(tensor_bytes_rows(g_.tensors[t], total_rows), -1, true);
+      pl.blocks[merge_buf[t]].users.clear();
+    }
+
+  auto ext_view = [&](int32_t t, int64_t r0, int64_t nrows) {
+    const TensorMeta& m = g_.tensors[t];
+    PlannedView v;
+    v.src = PlannedView::Src::kExternal;
+    v.tensor = t;
+    v.dtype = m.dtype;
+    v.batched = m.batch == BatchSemantics::kBatched;
+    v.shape = m.shape;
+    if (v.batched) {
+      v.shape[0] = nrows;
+      v.elem_offset = r0 * m.row_elems();
+    }
+    return v;
+  };
+  auto arena_view = [&](int32_t blk, int32_t t, int64_t row_off, int64_t nrows) {
+    const TensorMeta& m = g_.tensors[t];
+    PlannedView v;
+    v.src = PlannedView::Src::kArena;
+    v.block_off = pl.blocks[blk].off;
+    v.tensor = blk;
+    v.dtype = m.dtype;
+    v.shape = m.shape;
+    v.shape[0] = nrows;
+    v.elem_offset = row_off * m.row_elems();
+    v.batched = true;
+    return v;
+  };
+
+  for (int32_t di = 0; di < nd; ++di) {
+    const Dispatch& d = ds[di];
+    PlannedDispatch pd;
+    pd.d = d;
+    const int64_t r0 = offs[d.u0], nrows = offs[d.u1] - offs[d.u0];
+    pd.rows = nrows;
+    lane_of[di] = d.lane;
+
+    // ---- member ops, produced set, boundary inputs/outputs of the dispatch
+    std::vector<int32_t> ops;
+    std::set<int32_t> produced, member_set(d.subgraphs.begin(), d.subgraphs.end());
+    for (int32_t s : d.subgraphs)
+      for (int32_t op : p_.subgraphs[s].ops) ops.push_back(op);
+    for (int32_t op : ops)
+      for (int32_t t : g_.ops[op].outputs) produced.insert(t);
+    std::vector<int32_t> b_in, b_out;  // ordered (first use / production order)
+    for (int32_t op : ops)
+      for (int32_t t : g_.ops[op].inputs)
+        if (!produced.count(t) && std::find(b_in.begin(), b_in.end(), t) == b_in.end())
+          b_in.push_back(t);
+    for (int32_t op : ops)
+      for (int32_t t : g_.ops[op].outputs) {
+        bool leaves = g_.is_output(t);
+        for (int32_t c : g_.tensors[t].consumers)
+          leaves = leaves || !member_set.count(p_.op_to_subgraph[c]);
+        if (leaves) b_out.push_back(t);
+      }
+    // boundary inputs as Algorithm 1 sees them: per member subgraph
+    std::vector<std::pair<int32_t, int32_t>> consumed;  // (tensor, member subgraph)
+    for (int32_t s : d.subgraphs)
+      for (int32_t t : p_.subgraphs[s].boundary_inputs) consumed.push_back({t, s});
+
+    // ---- dependencies from input producers
+    std::set<int32_t> deps;
+    for (int32_t t : b_in) {
+      const TensorMeta& m = g_.tensors[t];
+      if (m.producer < 0) {
+        require(dry_ || ext_[t].base != nullptr, Errc::MissingBinding,
+                "no binding for '" + m.name + "'");
+        continue;
+      }
+      for (int32_t u = d.u0; u < d.u1; ++u) {
+        const TensorState& st = mb[u].states[t];
+        require(st.binding != BindingKind::kUnmaterialized, Errc::Unmaterialized,
+                "tensor '" + m.name + "' ubatch " + std::to_string(u) + " not materialized");
+        require(st.ref_count > 0, Errc::UseAfterFree,
+                "tensor '" + m.name + "' ubatch " + std::to_string(u) + " already reclaimed");
+        deps.insert(inst[t][u].producer);
+      }
+    }
+    // vector clock of this dispatch
+    std::vector<int32_t>& my = vc[di];
+    if (lane_last[d.lane] >= 0) my = vc[lane_last[d.lane]];
+    for (int32_t x : deps)
+      for (int l = 0; l < L; ++l) my[l] = std::max(my[l], vc[x][l]);
+    const std::vector<int32_t> before = lane_last[d.lane] >= 0 ? vc[lane_last[d.lane]]
+                                                              : std::vector<int32_t>(L, 0);
+    seq_of[di] = ++lane_seq[d.lane];
+    my[d.lane] = seq_of[di];
+    for (int32_t x : deps)
+      if (lane_of[x] != d.lane && before[lane_of[x]] < seq_of[x]) {
+        // not yet ordered by an earlier wait on this lane
+        bool covered = false;
+        for (int32_t y : pd.wait_on) covered = covered || (vc[y][lane_of[x]] >= seq_of[x]);
+        if (!covered) pd.wait_on.push_back(x);
+      }
+    std::sort(pd.wait_on.begin(), pd.wait_on.end());
+
+    // ---- input views (zero-copy slices, or counted concat copies in fallback mode)
+    std::map<int32_t, PlannedView> view_of;
+    std::vector<int32_t> scratch;  // blocks freed after this dispatch
+    for (int32_t t : b_in) {
+      const TensorMeta& m = g_.tensors[t];
+      if (m.producer < 0) {
+        view_of[t] = ext_view(t, r0, nrows);
+        continue;
+      }
+      const InstBinding& first = inst[t][d.u0];
+      bool contiguous = true;
+      for (int32_t u = d.u0 + 1; u < d.u1; ++u)
+        contiguous = contiguous && inst[t][u].block == first.block &&
+                     inst[t][u].row_off == first.row_off + (offs[u] - offs[d.u0]);
+      if (contiguous) {
+        view_of[t] = first.block == -2 ? ext_view(t, r0, nrows)
+                                       : arena_view(first.block, t, first.row_off, nrows);
+        if (first.block >= 0)
+          for (int32_t u = d.u0; u < d.u1; ++u) pl.use(inst[t][u].block, di);
+        continue;
+      }
+      // copying fallback: concat_rows into a fresh block (copies counted)
+      const int32_t blk = pl.alloc(tensor_bytes_rows(m, nrows), di);
+      scratch.push_back(blk);
+      for (int32_t u = d.u0; u < d.u1; ++u) {
+        const InstBinding& ib = inst[t][u];
+        PlannedLaunch cpy;
+        cpy.is_copy = true;
+        cpy.name = "concat_rows:" + m.name;
+        cpy.rows = sizes[u];
+        cpy.in.push_back(ib.block == -2 ? ext_view(t, offs[u], sizes[u])
+                                        : arena_view(ib.block, t, ib.row_off, sizes[u]));
+        cpy.out.push_back(arena_view(blk, t, offs[u] - offs[d.u0], sizes[u]));
+        if (ib.block >= 0) pl.use(ib.block, di);
+        pd.launches.push_back(std::move(cpy));
+        cp->copied_elements += sizes[u] * m.row_elems();
+      }
+      view_of[t] = arena_view(blk, t, 0, nrows);
+    }
+
+    // ---- output bindings (on_outputs)
+    for (int32_t t : b_out) {
+      const TensorMeta& m = g_.tensors[t];
+      for (int32_t u = d.u0; u < d.u1; ++u)
+        require(mb[u].states[t].binding == BindingKind::kUnmaterialized, Errc::DoubleProduce,
+                "tensor '" + m.name + "' produced twice in ubatch " + std::to_string(u));
+      if (g_.is_output(t) && ext_[t].base) {
+        for (int32_t u = d.u0; u < d.u1; ++u) {
+          inst[t][u] = {-2, offs[u], di};
+          mb[u].states[t].binding = BindingKind::kSlice;
+        }
+        view_of[t] = ext_view(t, r0, nrows);
+        continue;
+      }
+      const bool full = g_.is_output(t) || mb[d.u0].states[t].prealloc;
+      int32_t blk;
+      int64_t base_row;
+      if (full) {
+        if (merge_buf[t] < 0) merge_buf[t] = pl.alloc(tensor_bytes_rows(m, total_rows), di);
+        blk = merge_buf[t];
+        pl.use(blk, di);
+        base_row = r0;
+      } else {
+        blk = pl.alloc(tensor_bytes_rows(m, nrows), di);
+        base_row = 0;
+      }
+      for (int32_t u = d.u0; u < d.u1; ++u) {
+        inst[t][u] = {blk, base_row + (offs[u] - offs[d.u0]), di};
+        mb[u].states[t].binding = full ? BindingKind::kSlice : BindingKind::kOwned;
+        mb[u].states[t].buffer = blk;
+        mb[u].states[t].row_offset = inst[t][u].row_off;
+        mb[u].states[t].row_extent = sizes[u];
+        ++pending(blk);
+      }
+      view_of[t] = arena_view(blk, t, base_row, nrows);
+    }
+
+    // ---- launches
+    auto weight_view = [&](int32_t t, const OperatorNode&) { return ext_view(t, 0, 0); };
+    const bool fused = d.kind == Dispatch::Kind::kFused;
+    if (fused) {
+      PlannedLaunch l;
+      l.fn = d.replace_fn;
+      l.name = d.replace_fn;
+      l.rows = nrows;
+      for (int32_t op : ops) {  // merged attrs: max world_size, union of params
+        const OpAttrs& a = g_.ops[op].attrs;
+        l.attrs.world_size = std::max(l.attrs.world_size, a.world_size);
+        if (!l.attrs.seed) l.attrs.seed = a.seed;
+        for (const auto& kv : a.params) l.attrs.params.insert(kv);
+        l.name += ":" + g_.ops[op].name;
+      }
+      l.attrs.custom_name = d.replace_fn;
+      for (int32_t t : b_in)
+        l.in.push_back(g_.tensors[t].role == TensorRole::kWeight ? ext_view(t, 0, 0) : view_of.at(t));
+      for (int32_t t : b_out) l.out.push_back(view_of.at(t));
+      const OpEntry* e = OpRegistry::global().find(d.replace_fn);
+      require(e != nullptr, Errc::SignatureMismatch, "no replacement op '" + d.replace_fn + "'");
+      require((e->n_in < 0 || e->n_in == static_cast<int>(l.in.size())) &&
+                  (e->n_out < 0 || e->n_out == static_cast<int>(l.out.size())),
+              Errc::SignatureMismatch,
+              "replacement '" + d.replace_fn + "' takes " + std::to_string(e->n_in) + "->" +
+                  std::to_string(e->n_out) + " tensors, fused subgraphs expose " +
+                  std::to_string(l.in.size()) + "->" + std::to_string(l.out.size()));
+      pd.launches.push_back(std::move(l));
+    } else {
+      // internal tensors of the subgraph get scratch blocks for this dispatch
+      for (int32_t op : ops) {
+        const OperatorNode& node = g_.ops[op];
+        for (int32_t t : node.outputs)
+          if (!view_of.count(t)) {
+            const int32_t blk = pl.alloc(tensor_bytes_rows(g_.tensors[t], nrows), di);
+            scratch.push_back(blk);
+            view_of[t] = arena_view(blk, t, 0, nrows);
+          }
+        PlannedLaunch l;
+        l.op = op;
+        l.kind = node.kind;
+        l.fn = node.kind == OperatorKind::kCustom ? node.attrs.custom_name : "";
+        l.attrs = node.attrs;
+        l.name = node.name;
+        l.rows = nrows;
+        for (int32_t t : node.inputs)
+          l.in.push_back(g_.tensors[t].role == TensorRole::kWeight ? weight_view(t, node)
+                                                                     : view_of.at(t));
+        for (int32_t t : node.outputs) l.out.push_back(view_of.at(t));
+        if (node.kind == OperatorKind::kMatMul && g_.tensors[node.inputs[1]].dtype == Dtype::kBF16 &&
+            g_.tensors[node.inputs[1]].role == TensorRole::kWeight)
+          l.prepacked = node.inputs[1];  // aux = [N,K] copy, resolved at launch
+        if (node.kind == OperatorKind::kCustom)
+          require(OpRegistry::global().find(node.attrs.custom_name) != nullptr, Errc::ConfigError,
+                  "no device op registered for '" + node.attrs.custom_name + "'");
+        pd.launches.push_back(std::move(l));
+      }
+    }
+    // workspace + SM budget
+    for (PlannedLaunch& l : pd.launches) {
+      if (l.is_copy) continue;
+      if (cfg_.gemm_sm_budget > 0 && d.lane == 0) l.max_ctas = cfg_.gemm_sm_budget;
+      opf_op_ctx c{};
+      c.kind = static_cast<int32_t>(l.kind);
+      c.world_size = l.attrs.world_size;
+      c.comm = comm_;
+      std::vector<opf_view> iv, ov;
+      for (const auto& v : l.in) iv.push_back(make_view(nullptr, v.elem_offset, v.dtype, v.shape, v.batched));
+      for (const auto& v : l.out) ov.push_back(make_view(nullptr, v.elem_offset, v.dtype, v.shape, v.batched));
+      std::vector<const char*> pn;
+      std::vector<double> pv;
+      for (const auto& kv : l.attrs.params) {
+        pn.push_back(kv.first.c_str());
+        pv.push_back(kv.second);
+      }
+      c.n_params = static_cast<int32_t>(pn.size());
+      c.param_names = pn.data();
+      c.param_values = pv.data();
+      size_t ws = 0;
+      if (l.fn.empty()) {
+        ws = kind_workspace(c, iv.data(), static_cast<int>(iv.size()), ov.data(),
+                            static_cast<int>(ov.size()), l.rows);
+      } else if (const OpEntry* e = OpRegistry::global().find(l.fn); e && e->workspace) {
+        ws = e->workspace(c, iv.data(), static_cast<int>(iv.size()), ov.data(),
+                          static_cast<int>(ov.size()), l.rows);
+      }
+      if (ws > 0) {
+        const int32_t blk = pl.alloc(static_cast<int64_t>(ws), di);
+        scratch.push_back(blk);
+        l.ws_off = pl.blocks[blk].off;
+        l.ws_bytes = static_cast<int64_t>(ws);
+      }
+    }
+
+    // ---- on_inputs: decrement ref counts, reclaim dead slices after the dispatch
+    for (const auto& [t, s] : consumed) {
+      (void)s;
+      if (g_.tensors[t].producer < 0) continue;
+      const bool internal = produced.count(t) > 0;
+      if (internal && std::find(b_out.begin(), b_out.end(), t) == b_out.end()) continue;
+      for (int32_t u = d.u0; u < d.u1; ++u) {
+        TensorState& st = mb[u].states[t];
+        require(st.ref_count > 0, Errc::UseAfterFree,
+                "tensor '" + g_.tensors[t].name + "' over-consumed");
+        if (--st.ref_count == 0 && !g_.is_output(t)) {
+          const int32_t blk = inst[t][u].block;
+          if (blk >= 0 && --pending(blk) == 0) pl.release(blk);
+        }
+      }
+    }
+    // fused-internal tensors never materialize: retire their Algorithm-1 state
+    if (fused)
+      for (int32_t t : produced)
+        if (std::find(b_out.begin(), b_out.end(), t) == b_out.end())
+          for (int32_t u = d.u0; u < d.u1; ++u) mb[u].states[t].ref_count = 0;
+    for (int32_t blk : scratch) pl.release(blk);
+    lane_last[d.lane] = di;
+    cp->n_launches += static_cast<int64_t>(pd.launches.size());
+    cp->dispatches.push_back(std::move(pd));
+  }
+  // events are recorded only where another lane waits
+  for (const PlannedDispatch& pd : cp->dispatches)
+    for (int32_t x : pd.wait_on) cp->dispatches[x].record_event = true;
+  std::set<int32_t> used;
+  for (const Dispatch& d : ds) used.insert(d.lane);
+  cp->lanes_used = static_cast<int>(used.size());
+  for (int32_t t : g_.graph_outputs)
+    if (merge_buf[t] >= 0) cp->outputs.push_back({t, pl.blocks[merge_buf[t]].off});
+  cp->end_live_tensors = 0;
+  for (int32_t t = 0; t < NT; ++t)
+    for (int32_t u = 0; u < U; ++u)
+      if (g_.tensors[t].producer >= 0 && mb[u].states[t].ref_count > 0) {
+        ++cp->end_live_tensors;
+        break;
+      }
+  cp->arena_bytes = pl.top;
+  cp->peak_live_bytes = pl.peak;
+  return cp;
+}
+
+opf_view Session::resolve(const PlannedView& v) const {
+  switch (v.src) {
+    case PlannedView::Src::kArena:
+      return make_view(static_cast<char*>(arena_) + v.block_off, v.elem_offset, v.dtype, v.shape,
+                       v.batched);
+    case PlannedView::Src::kExternal: {
+      const opf_view& e = ext_[v.tensor];
+      return make_view(e.base, e.elem_offset + v.elem_offset, v.dtype, v.shape, v.batched);
+    }
+    case PlannedView::Src::kPrepacked:
+      return make_view(prepacked_[v.tensor], 0, v.dtype, v.shape, false);
+    default:
+      fail(Errc::Unmaterialized, "unresolved planned view");
+  }
+}
+
+void Session::launch_one(const PlannedLaunch& l, cudaStream_t s) {
+  if (l.is_copy) {
+    const opf_view src = resolve(l.in[0]), dst = resolve(l.out[0]);
+    k_copy_rows(view_ptr(src), view_ptr(dst), view_numel(src) * dtype_bytes(Dtype(src.dtype)), s);
+    return;
+  }
+  std::vector<opf_view> iv, ov;
+  for (const auto& v : l.in) iv.push_back(resolve(v));
+  for (const auto& v : l.out) ov.push_back(resolve(v));
+  std::vector<const char*> pn;
+  std::vector<double> pv;
+  for (const auto& kv : l.attrs.params) {
+    pn.push_back(kv.first.c_str());
+    pv.push_back(kv.second);
+  }
+  opf_op_ctx c{};
+  c.op_name = l.name.c_str();
+  c.kind = static_cast<int32_t>(l.kind);
+  c.custom_name = l.attrs.custom_name.c_str();
+  c.world_size = l.attrs.world_size;
+  c.seed = l.attrs.seed;
+  c.n_params = static_cast<int32_t>(pn.size());
+  c.param_names = pn.data();
+  c.param_values = pv.data();
+  c.max_ctas = l.max_ctas;
+  c.comm = comm_;
+  c.aux = l.prepacked >= 0 ? prepacked_[l.prepacked] : l.aux;
+  if (l.kind == OperatorKind::kAllToAll && l.fn.empty())
+    c.aux = alltoall_perm_device(l.attrs.seed, view_row_elems(iv[0]));
+  c.workspace = l.ws_off >= 0 ? static_cast<char*>(arena_) + l.ws_off : nullptr;
+  c.workspace_bytes = static_cast<size_t>(l.ws_bytes);
+  opf_status st;
+  if (l.fn.empty()) {
+    st = launch_kind(c, iv.data(), static_cast<int>(iv.size()), ov.data(),
+                     static_cast<int>(ov.size()), l.rows, s);
+  } else {
+    const OpEntry* e = OpRegistry::global().find(l.fn);
+    require(e != nullptr, Errc::ConfigError, "no device op '" + l.fn + "'");
+    st = e->fn(&c, iv.data(), static_cast<int>(iv.size()), ov.data(), static_cast<int>(ov.size()),
+               l.rows, s);
+  }
+  if (st != 0)
+    fail(static_cast<Errc>(st - 1), "op '" + l.name + "': " + std::string(opf_last_error()));
+}
+
+void Session::launch_plan(CompiledPlan& cp, cudaStream_t origin, bool capturing) {
+  const int L = static_cast<int>(lanes_.size());
+  const std::size_t need = cp.dispatches.size() + L + 1;
+  while (events_.size() < need) {
+    cudaEvent_t e;
+    OPF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    events_.push_back(e);
+  }
+  cudaEvent_t fork = events_[cp.dispatches.size()];
+  OPF_CUDA(cudaEventRecord(fork, origin));
+  std::vector<bool> used(L, false);
+  for (const PlannedDispatch& pd : cp.dispatches) used[pd.d.lane] = true;
+  for (int l = 0; l < L; ++l)
+    if (used[l]) OPF_CUDA(cudaStreamWaitEvent(lanes_[l], fork, 0));
+  for (const PlannedDispatch& pd : cp.dispatches) {
+    cudaStream_t s = lanes_[pd.d.lane];
+    for (int32_t w : pd.wait_on) OPF_CUDA(cudaStreamWaitEvent(s, events_[w], 0));
+    for (const PlannedLaunch& l : pd.launches) launch_one(l, s);
+    if (pd.record_event) OPF_CUDA(cudaEventRecord(events_[pd.d.id], s));
+  }
+  for (int l = 0; l < L; ++l)
+    if (used[l]) {
+      cudaEvent_t j = events_[cp.dispatches.size() + 1 + l];
+      OPF_CUDA(cudaEventRecord(j, lanes_[l]));
+      OPF_CUDA(cudaStreamWaitEvent(origin, j, 0));
+    }
+  (void)capturing;
+}
+
+CompiledPlan* Session::lookup_or_build(Scheduler& strat, const std::string& key_in) {
+  const int64_t r = rows();
+  const std::string key = key_in + "|rows=" + std::to_string(r);
+  ++runs_;
+  auto it = cache_.find(key);
+  if (it != cache_.end()) {
+    ++hits_;
+    return it->second.get();
+  }
+  ++misses_;
+  SchedContext ctx(g_, p_, r, static_cast<int>(lanes_.size()));
+  strat.schedule(ctx);
+  ctx.finish();
+  auto built = compile(ctx, key);
+  CompiledPlan* cp = built.get();
+  cache_[key] = std::move(built);
+  return cp;
+}
+
+void Session::plan_only(Scheduler& strat, const std::string& key) {
+  last_ = lookup_or_build(strat, key);
+}
+
+void Session::run(Scheduler& strat, const std::string& key_in, cudaStream_t stream) {
+  require(!dry_, Errc::EngineStopped, "dry session cannot execute");
+  CompiledPlan* cp = lookup_or_build(strat, key_in);
+  last_ = cp;
+  ensure_prepacked(stream);
+  ensure_arena(cp->arena_bytes);
+  warm_aux(*cp);
+  if (!cfg_.cuda_graph) {
+    launch_plan(*cp, stream, false);
+    OPF_CUDA(cudaGetLastError());
+    return;
+  }
+  if (!cp->exec || cp->arena_base_at_capture != arena_) {
+    if (cp->exec) {
+      OPF_CUDA(cudaGraphExecDestroy(cp->exec));
+      cp->exec = nullptr;
+    }
+    cudaStream_t cap;
+    OPF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    // prior work on `stream` (prepack, input uploads) must precede capture-free replay
+    OPF_CUDA(cudaStreamSynchronize(stream));
+    OPF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    try {
+      launch_plan(*cp, cap, true);
+    } catch (...) {
+      cudaGraph_t g;
+      cudaStreamEndCapture(cap, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaStreamDestroy(cap);
+      throw;
+    }
+    cudaGraph_t graph;
+    OPF_CUDA(cudaStreamEndCapture(cap, &graph));
+    OPF_CUDA(cudaGraphInstantiate(&cp->exec, graph, 0));
+    OPF_CUDA(cudaGraphDestroy(graph));
+    OPF_CUDA(cudaStreamDestroy(cap));
+    cp->arena_base_at_capture = arena_;
+  }
+  OPF_CUDA(cudaGraphLaunch(cp->exec, stream));
+}
+
+opf_view Session::output(const std::string& name) {
+  const int32_t t = g_.tensor_id(name);
+  require(g_.is_output(t), Errc::ConfigError, "'" + name + "' is not a graph output");
+  if (ext_[t].base) return ext_[t];
+  require(last_ != nullptr, Errc::Unmaterialized, "no run yet");
+  for (const auto& [tt, off] : last_->outputs)
+    if (tt == t) {
+      const TensorMeta& m = g_.tensors[t];
+      std::vector<int64_t> shape = m.shape;
+      shape[0] = rows();
+      return make_view(static_cast<char*>(arena_) + off, 0, m.dtype, shape, true);
+    }
+  fail(Errc::Unmaterialized, "output '" + name + "' not found in last plan");
+}
+
+std::string Session::stats_json() const {
+  std::string s = "{\"runs\":" + std::to_string(runs_) +
+                  ",\"plan_cache_hits\":" + std::to_string(hits_) +
+                  ",\"plan_cache_misses\":" + std::to_string(misses_) +
+                  ",\"arena_bytes\":" + std::to_string(arena_bytes_) +
+                  ",\"cached_plans\":" + std::to_string(cache_.size());
+  if (last_) {
+    s += ",\"last\":{\"key\":" + json::quote(last_->key) +
+         ",\"dispatches\":" + std::to_string(last_->dispatches.size()) +
+         ",\"launches\":" + std::to_string(last_->n_launches) +
+         ",\"copied_elements\":" + std::to_string(last_->copied_elements) +
+         ",\"plan_arena_bytes\":" + std::to_string(last_->arena_bytes) +
+         ",\"peak_live_bytes\":" + std::to_string(last_->peak_live_bytes) +
+         ",\"analysis_ops\":" + std::to_string(last_->analysis_ops) +
+         ",\"lanes_used\":" + std::to_string(last_->lanes_used) +
+         ",\"end_live_tensors\":" + std::to_string(last_->end_live_tensors) +
+         ",\"captured\":" + (last_->exec ? "true" : "false") + "}";
+  }
+  return s + "}";
+}
+
+std::string Session::schedule_json() const {
+  require(last_ != nullptr, Errc::Unmaterialized, "no run yet");
+  static const char* kinds[] = {"single", "merged", "fused"};
+  std::string s = "{\"key\":" + json::quote(last_->key) + ",\"dispatches\":[";
+  for (std::size_t i = 0; i < last_->dispatches.size(); ++i) {
+    const PlannedDispatch& pd = last_->dispatches[i];
+    if (i) s += ',';
+    std::vector<std::string> labels;
+    for (int32_t sg : pd.d.subgraphs) labels.push_back(p_.subgraphs[sg].label);
+    s += "{\"id\":" + std::to_string(pd.d.id) + ",\"lane\":" + std::to_string(pd.d.lane) +
+         ",\"kind\":\"" + kinds[static_cast<int>(pd.d.kind)] +
+         "\",\"subgraphs\":" + json::int_list(pd.d.subgraphs) +
+         ",\"labels\":" + json::str_list(labels) + ",\"u0\":" + std::to_string(pd.d.u0) +
+         ",\"u1\":" + std::to_string(pd.d.u1) + ",\"rows\":" + std::to_string(pd.rows) +
+         ",\"wait_on\":" + json::int_list(pd.wait_on) + ",\"replace_fn\":" +
+         json::quote(pd.d.replace_fn) + ",\"launches\":[";
+    for (std::size_t j = 0; j < pd.launches.size(); ++j) {
+      const PlannedLaunch& l = pd.launches[j];
+      if (j) s += ',';
+      auto views = [&](const std::vector<PlannedView>& vs) {
+        std::string o = "[";
+        for (std::size_t k = 0; k < vs.size(); ++k) {
+          static const char* src[] = {"arena", "external", "prepacked", "none"};
+          if (k) o += ',';
+          o += "{\"src\":\"" + std::string(src[static_cast<int>(vs[k].src)]) +
+               "\",\"block_off\":" + std::to_string(vs[k].block_off) +
+               ",\"tensor\":" + std::to_string(vs[k].tensor) +
+               ",\"elem_offset\":" + std::to_string(vs[k].elem_offset) +
+               ",\"shape\":" + json::int_list(vs[k].shape) + "}";
+        }
+        return o + "]";
+      };
+      s += "{\"name\":" + json::quote(l.name) + ",\"op\":" + std::to_string(l.op) +
+           ",\"copy\":" + (l.is_copy ? "true" : "false") + ",\"rows\":" + std::to_string(l.rows) +
+           ",\"in\":" + views(l.in) + ",\"out\":" + views(l.out) + "}";
+    }
+    s += "]}";
+  }
+  return s + "]}";
+}
+
+std::string Session::trace_json() {
+  require(last_ != nullptr, Errc::Unmaterialized, "no run yet");
+  // Profiled eager replay: timing events around every dispatch on its lane.
+  CompiledPlan& cp = *last_;
+  const std::size_t n = cp.dispatches.size();
+  std::vector<cudaEvent_t> b(n), e(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    OPF_CUDA(cudaEventCreate(&b[i]));
+    OPF_CUDA(cudaEventCreate(&e[i]));
+  }
+  cudaEvent_t t0;
+  OPF_CUDA(cudaEventCreate(&t0));
+  OPF_CUDA(cudaDeviceSynchronize());
+  OPF_CUDA(cudaEventRecord(t0, lanes_[0]));
+  for (auto& l : lanes_) OPF_CUDA(cudaStreamWaitEvent(l, t0, 0));
+  for (std::size_t i = 0; i < n; ++i) {
+    const PlannedDispatch& pd = cp.dispatches[i];
+    cudaStream_t s = lanes_[pd.d.lane];
+    for (int32_t w : pd.wait_on) OPF_CUDA(cudaStreamWaitEvent(s, e[w], 0));
+    OPF_CUDA(cudaEventRecord(b[i], s));
+    for (const PlannedLaunch& l : pd.launches) launch_one(l, s);
+    OPF_CUDA(cudaEventRecord(e[i], s));
+  }
+  OPF_CUDA(cudaDeviceSynchronize());
+  std::string out = "[";
+  for (std::size_t i = 0; i < n; ++i) {
+    float ts = 0, te = 0;
+    OPF_CUDA(cudaEventElapsedTime(&ts, t0, b[i]));
+    OPF_CUDA(cudaEventElapsedTime(&te, t0, e[i]));
+    const PlannedDispatch& pd = cp.dispatches[i];
+    std::string name;
+    for (int32_t sg : pd.d.subgraphs) name += (name.empty() ? "" : "+") + p_.subgraphs[sg].label;
+    name += " u" + std::to_string(pd.d.u0) + (pd.d.u1 - pd.d.u0 > 1 ? "-" + std::to_string(pd.d.u1 - 1) : "");
+    char buf[128];
+    std::snprintf(buf, sizeof buf, ",\"ts\":%.3f,\"dur\":%.3f,\"pid\":0,\"tid\":%d}", ts * 1e3,
+                  (te - ts) * 1e3, pd.d.lane);
+    out += std::string(i ? "," : "") + "{\"name\":" + json::quote(name) +
+           ",\"cat\":\"dispatch\",\"ph\":\"X\"" + buf;
+    cudaEventDestroy(b[i]);
+    cudaEventDestroy(e[i]);
+  }
+  cudaEventDestroy(t0);
+  return out + "]";
+}
+
+}  // namespace opflow

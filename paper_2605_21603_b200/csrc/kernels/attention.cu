@@ -1,0 +1,373 @@
+// Attention ops for the Llama-shaped graphs.
+//
+//  attn_decode  (memory-bound, the north star's paged decode attention)
+//    qkv_rot [B, (nq+2nkv)*hd], k_cache / v_cache [pages, page, nkv, hd],
+//    block_table [B, max_pages] (i64), ctx_len [B] (i64) -> out [B, nq*hd].
+//    One CTA per (sequence, kv head) serves the whole GQA group, so every
+//    cached K/V byte is read from HBM exactly once: algorithmic bytes per
+//    (sequence, kv head) = 2 * ctx * hd * 2 B.  Each token's K (or V) row is
+//    256 contiguous bytes read by 16 lanes with 16-byte loads; a warp covers
+//    two tokens per step and four steps are kept in flight (8 x 16 B per lane).
+//    Online softmax in fp32; the 4 warps' partial states merge in smem.
+//
+//  attn_prefill (causal GQA within fixed-length sequences; SIMT reference
+//    path here, tensor-core path in attention_tc.cu).
+#include <cuda_bf16.h>
+
+#include <cfloat>
+
+#include "opflow/device.hpp"
+
+namespace opflow {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16(v); }
+
+// ---------------------------------------------------------------- prefill (SIMT)
+// One warp per (row, q head); lanes split head_dim.  Correctness path for fp32
+// graphs and the numerics reference of the tensor-core kernel.
+template <typename T>
+__global__ void prefill_simt_kernel(const T* __restrict__ qkv, T* __restrict__ out, int64_t rows,
+                                    int nq, int nkv, int hd, int S, float scale) {
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (gw >= rows * nq) return;
+  const int64_t r = gw / nq;
+  const int h = static_cast<int>(gw % nq), kh = h / (nq / nkv);
+  const int64_t W = static_cast<int64_t>(nq + 2 * nkv) * hd;
+  const int64_t s0 = r - r % S;
+  constexpr int MAXD = 8;  // hd <= 256
+  float q[MAXD], acc[MAXD];
+#pragma unroll
+  for (int i = 0; i < MAXD; ++i) {
+    const int d = lane + 32 * i;
+    q[i] = d < hd ? to_f(qkv[r * W + h * hd + d]) * scale : 0.0f;
+    acc[i] = 0.0f;
+  }
+  float m = -FLT_MAX, l = 0.0f;
+  for (int64_t j = s0; j <= r; ++j) {
+    const T* k = qkv + j * W + static_cast<int64_t>(nq + kh) * hd;
+    float dot = 0.0f;
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) {
+      const int d = lane + 32 * i;
+      if (d < hd) dot += q[i] * to_f(k[d]);
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, s);
+    const float mn = fmaxf(m, dot);
+    const float corr = expf(m - mn), p = expf(dot - mn);
+    l = l * corr + p;
+    const T* v = qkv + j * W + static_cast<int64_t>(nq + nkv + kh) * hd;
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) {
+      const int d = lane + 32 * i;
+      acc[i] = acc[i] * corr + (d < hd ? p * to_f(v[d]) : 0.0f);
+    }
+    m = mn;
+  }
+#pragma unroll
+  for (int i = 0; i < MAXD; ++i) {
+    const int d = lane + 32 * i;
+    if (d < hd) out[r * nq * hd + h * hd + d] = from_f<T>(acc[i] / l);
+  }
+}
+
+// ---------------------------------------------------------------- decode (paged)
+constexpr int kDecWarps = 4;
+constexpr int kMaxGroup = 8;   // q heads per kv head
+constexpr int kUnroll = 4;     // token pairs in flight per warp
+
+template <int GRP>
+__global__ void __launch_bounds__(kDecWarps * 32) decode_bf16_kernel(
+    const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ kc,
+    const __nv_bfloat16* __restrict__ vc, const int64_t* __restrict__ table,
+    const int64_t* __restrict__ ctx_len, __nv_bfloat16* __restrict__ out, int nq, int nkv,
+    int64_t max_pages, int page, float scale) {
+  constexpr int HD = 128;  // 16 lanes x 8 bf16
+  const int64_t b = blockIdx.x / nkv;
+  const int kh = blockIdx.x % nkv;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int half = lane / 16, sub = lane % 16;  // token parity, 16-byte chunk index
+  const int64_t W = static_cast<int64_t>(nq + 2 * nkv) * HD;
+  const int64_t ctx = ctx_len[b];
+  const int64_t total = ctx + 1;  // cached tokens + the current one
+  const __nv_bfloat16* row = qkv + b * W;
+
+  float q[GRP][8];
+#pragma unroll
+  for (int g = 0; g < GRP; ++g) {
+    const uint4 u = *reinterpret_cast<const uint4*>(row + (kh * GRP + g) * HD + sub * 8);
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h2[i]);
+      q[g][2 * i] = f.x * scale;
+      q[g][2 * i + 1] = f.y * scale;
+    }
+  }
+  float m[GRP], l[GRP], acc[GRP][8];
+#pragma unroll
+  for (int g = 0; g < GRP; ++g) {
+    m[g] = -FLT_MAX;
+    l[g] = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[g][i] = 0.0f;
+  }
+  const int64_t kv_stride = static_cast<int64_t>(nkv) * HD;
+  auto kv_ptr = [&](const __nv_bfloat16* cache, const __nv_bfloat16* cur, int64_t j) {
+    if (j == ctx) return cur;
+    const int64_t pg = table[b * max_pages + j / page];
+    return cache + (pg * page + j % page) * kv_stride + static_cast<int64_t>(kh) * HD;
+  };
+  const __nv_bfloat16* kcur = row + static_cast<int64_t>(nq + kh) * HD;
+  const __nv_bfloat16* vcur = row + static_cast<int64_t>(nq + nkv + kh) * HD;
+
+  // token j handled by (warp, half) = ((j/2) % kDecWarps, j % 2)
+  for (int64_t base = 2 * warp; base < total; base += 2 * kDecWarps * kUnroll) {
+    uint4 kr[kUnroll], vr[kUnroll];
+    bool ok[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t j = base + static_cast<int64_t>(u) * 2 * kDecWarps + half;
+      ok[u] = j < total;
+      if (ok[u]) {
+        kr[u] = __ldg(reinterpret_cast<const uint4*>(kv_ptr(kc, kcur, j) + sub * 8));
+        vr[u] = __ldg(reinterpret_cast<const uint4*>(kv_ptr(vc, vcur, j) + sub * 8));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      float kf[8], vf[8];
+      const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kr[u]);
+      const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vr[u]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 a = __bfloat1622float2(k2[i]), c = __bfloat1622float2(v2[i]);
+        kf[2 * i] = a.x;
+        kf[2 * i + 1] = a.y;
+        vf[2 * i] = c.x;
+        vf[2 * i + 1] = c.y;
+      }
+#pragma unroll
+      for (int g = 0; g < GRP; ++g) {
+        float s = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += q[g][i] * kf[i];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);  // within 16 lanes
+        if (ok[u]) {
+          const float mn = fmaxf(m[g], s);
+          const float corr = __expf(m[g] - mn), p = __expf(s - mn);
+          l[g] = l[g] * corr + p;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[g][i] = acc[g][i] * corr + p * vf[i];
+          m[g] = mn;
+        }
+      }
+    }
+  }
+  // merge the two half-warps, then the warps, through shared memory
+  __shared__ float sm_m[kDecWarps * 2][GRP], sm_l[kDecWarps * 2][GRP];
+  __shared__ float sm_acc[kDecWarps * 2][GRP][HD];
+  const int slot = warp * 2 + half;
+#pragma unroll
+  for (int g = 0; g < GRP; ++g) {
+    if (sub == 0) {
+      sm_m[slot][g] = m[g];
+      sm_l[slot][g] = l[g];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sm_acc[slot][g][sub * 8 + i] = acc[g][i];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < GRP * HD; idx += blockDim.x) {
+    const int g = idx / HD, d = idx % HD;
+    float M = -FLT_MAX;
+    for (int sl = 0; sl < kDecWarps * 2; ++sl) M = fmaxf(M, sm_m[sl][g]);
+    float L = 0.0f, A = 0.0f;
+    for (int sl = 0; sl < kDecWarps * 2; ++sl) {
+      if (sm_l[sl][g] == 0.0f) continue;
+      const float c = __expf(sm_m[sl][g] - M);
+      L += sm_l[sl][g] * c;
+      A += sm_acc[sl][g][d] * c;
+    }
+    out[b * static_cast<int64_t>(nq) * HD + (kh * GRP + g) * HD + d] = __float2bfloat16(A / L);
+  }
+}
+
+// Generic (any dtype / head_dim) decode: one warp per (sequence, q head).
+template <typename T>
+__global__ void decode_simt_kernel(const T* __restrict__ qkv, const T* __restrict__ kc,
+                                   const T* __restrict__ vc, const int64_t* __restrict__ table,
+                                   const int64_t* __restrict__ ctx_len, T* __restrict__ out,
+                                   int64_t B, int nq, int nkv, int hd, int64_t max_pages, int page,
+                                   float scale) {
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (gw >= B * nq) return;
+  const int64_t b = gw / nq;
+  const int h = static_cast<int>(gw % nq), kh = h / (nq / nkv);
+  const int64_t W = static_cast<int64_t>(nq + 2 * nkv) * hd, ctx = ctx_len[b];
+  constexpr int MAXD = 8;
+  float q[MAXD], acc[MAXD];
+#pragma unroll
+  for (int i = 0; i < MAXD; ++i) {
+    const int d = lane + 32 * i;
+    q[i] = d < hd ? to_f(qkv[b * W + h * hd + d]) * scale : 0.0f;
+    acc[i] = 0.0f;
+  }
+  float m = -FLT_MAX, l = 0.0f;
+  for (int64_t j = 0; j <= ctx; ++j) {
+    const T *k, *v;
+    if (j == ctx) {
+      k = qkv + b * W + static_cast<int64_t>(nq + kh) * hd;
+      v = qkv + b * W + static_cast<int64_t>(nq + nkv + kh) * hd;
+    } else {
+      const int64_t pg = table[b * max_pages + j / page];
+      const int64_t off = ((pg * page + j % page) * nkv + kh) * static_cast<int64_t>(hd);
+      k = kc + off;
+      v = vc + off;
+    }
+    float dot = 0.0f;
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) {
+      const int d = lane + 32 * i;
+      if (d < hd) dot += q[i] * to_f(k[d]);
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, s);
+    const float mn = fmaxf(m, dot), corr = expf(m - mn), p = expf(dot - mn);
+    l = l * corr + p;
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) {
+      const int d = lane + 32 * i;
+      acc[i] = acc[i] * corr + (d < hd ? p * to_f(v[d]) : 0.0f);
+    }
+    m = mn;
+  }
+#pragma unroll
+  for (int i = 0; i < MAXD; ++i) {
+    const int d = lane + 32 * i;
+    if (d < hd) out[b * nq * hd + h * hd + d] = from_f<T>(acc[i] / l);
+  }
+}
+
+}  // namespace
+
+// implemented in attention_tc.cu (tensor-core prefill); returns false when the
+// shape is not supported there.
+bool prefill_bf16_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t rows, int nq, int nkv,
+                     int hd, int S, float scale, cudaStream_t s);
+
+opf_status attn_prefill_simt(const opf_view& in, opf_view& out, int64_t rows, int nq, int nkv,
+                             int hd, int S, cudaStream_t s) {
+  const float scale = 1.0f / sqrtf(static_cast<float>(hd));
+  const int64_t warps = rows * nq;
+  const int threads = 128;
+  const unsigned grid = static_cast<unsigned>((warps * 32 + threads - 1) / threads);
+  if (in.dtype == OPF_BF16)
+    prefill_simt_kernel<__nv_bfloat16><<<grid, threads, 0, s>>>(
+        vptr<__nv_bfloat16>(in), vptr<__nv_bfloat16>(out), rows, nq, nkv, hd, S, scale);
+  else
+    prefill_simt_kernel<float><<<grid, threads, 0, s>>>(vptr<float>(in), vptr<float>(out), rows, nq,
+                                                        nkv, hd, S, scale);
+  return launch_status("attn_prefill_simt");
+}
+
+namespace {
+
+opf_status op_attn_prefill(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out,
+                           int32_t n_out, int64_t rows, void* stream) {
+  if (n_in != 1 || n_out != 1) return op_error(Errc::ShapeMismatch, "attn_prefill takes (qkv) -> o");
+  const int nq = static_cast<int>(ctx_param(*c, "heads", 1));
+  const int nkv = static_cast<int>(ctx_param(*c, "kv_heads", 1));
+  const int hd = static_cast<int>(ctx_param(*c, "head_dim", 128));
+  const int S = static_cast<int>(ctx_param(*c, "seq_len", 1));
+  if (nq % nkv || hd > 256) return op_error(Errc::ShapeMismatch, "attn_prefill: heads");
+  if (view_row_elems(in[0]) != static_cast<int64_t>(nq + 2 * nkv) * hd ||
+      view_row_elems(out[0]) != static_cast<int64_t>(nq) * hd)
+    return op_error(Errc::ShapeMismatch, "attn_prefill: widths");
+  if (rows % S)
+    return op_error(Errc::ShapeMismatch, "attn_prefill: rows " + std::to_string(rows) +
+                                             " not a multiple of seq_len " + std::to_string(S));
+  if (rows == 0) return 0;
+  auto s = static_cast<cudaStream_t>(stream);
+  const bool force_simt = ctx_param(*c, "simt", 0.0) != 0.0;
+  if (in[0].dtype == OPF_BF16 && !force_simt &&
+      prefill_bf16_tc(vptr<__nv_bfloat16>(in[0]), vptr<__nv_bfloat16>(out[0]), rows, nq, nkv, hd, S,
+                      1.0f / sqrtf(static_cast<float>(hd)), s))
+    return launch_status("attn_prefill_tc");
+  return attn_prefill_simt(in[0], out[0], rows, nq, nkv, hd, S, s);
+}
+
+opf_status op_attn_decode(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out,
+                          int32_t n_out, int64_t rows, void* stream) {
+  if (n_in != 5 || n_out != 1)
+    return op_error(Errc::ShapeMismatch, "attn_decode takes (qkv, k_cache, v_cache, table, ctx)");
+  const int nq = static_cast<int>(ctx_param(*c, "heads", 1));
+  const int nkv = static_cast<int>(ctx_param(*c, "kv_heads", 1));
+  const int hd = static_cast<int>(ctx_param(*c, "head_dim", 128));
+  const int page = static_cast<int>(ctx_param(*c, "page_size", 16));
+  if (nq % nkv || hd > 256) return op_error(Errc::ShapeMismatch, "attn_decode: heads");
+  if (in[1].rank != 4 || in[1].shape[1] != page || in[1].shape[2] != nkv || in[1].shape[3] != hd)
+    return op_error(Errc::ShapeMismatch, "attn_decode: cache must be [pages, page, kv_heads, hd]");
+  if (rows == 0) return 0;
+  const int64_t max_pages = view_row_elems(in[3]);
+  const float scale = 1.0f / sqrtf(static_cast<float>(hd));
+  auto s = static_cast<cudaStream_t>(stream);
+  const int grp = nq / nkv;
+  if (in[0].dtype == OPF_BF16 && hd == 128 && grp <= kMaxGroup && ctx_param(*c, "simt", 0.0) == 0.0) {
+    const unsigned grid = static_cast<unsigned>(rows * nkv);
+    auto args = [&](auto kern) {
+      kern<<<grid, kDecWarps * 32, 0, s>>>(vptr<__nv_bfloat16>(in[0]), vptr<__nv_bfloat16>(in[1]),
+                                           vptr<__nv_bfloat16>(in[2]), vptr<int64_t>(in[3]),
+                                           vptr<int64_t>(in[4]), vptr<__nv_bfloat16>(out[0]), nq,
+                                           nkv, max_pages, page, scale);
+    };
+    switch (grp) {
+      case 1: args(decode_bf16_kernel<1>); break;
+      case 2: args(decode_bf16_kernel<2>); break;
+      case 4: args(decode_bf16_kernel<4>); break;
+      case 8: args(decode_bf16_kernel<8>); break;
+      default: goto generic;
+    }
+    return launch_status("attn_decode");
+  }
+generic:
+  {
+    const int threads = 128;
+    const unsigned grid = static_cast<unsigned>((rows * nq * 32 + threads - 1) / threads);
+    if (in[0].dtype == OPF_BF16)
+      decode_simt_kernel<__nv_bfloat16><<<grid, threads, 0, s>>>(
+          vptr<__nv_bfloat16>(in[0]), vptr<__nv_bfloat16>(in[1]), vptr<__nv_bfloat16>(in[2]),
+          vptr<int64_t>(in[3]), vptr<int64_t>(in[4]), vptr<__nv_bfloat16>(out[0]), rows, nq, nkv, hd,
+          max_pages, page, scale);
+    else
+      decode_simt_kernel<float><<<grid, threads, 0, s>>>(
+          vptr<float>(in[0]), vptr<float>(in[1]), vptr<float>(in[2]), vptr<int64_t>(in[3]),
+          vptr<int64_t>(in[4]), vptr<float>(out[0]), rows, nq, nkv, hd, max_pages, page, scale);
+  }
+  return launch_status("attn_decode_simt");
+}
+
+}  // namespace
+
+void register_attention_ops(OpRegistry& r) {
+  r.add({"attn_prefill", op_attn_prefill, ResourceClass::kCompute, 1, 1, {}});
+  r.add({"attn_decode", op_attn_decode, ResourceClass::kMemory, 5, 1, {}});
+}
+
+}  // namespace opflow

@@ -1,0 +1,414 @@
+// bf16 GEMM for the QKV / O / gate_up / down projections (the only dense
+// contractions of the Llama layer):  C[M,N] = A[M,K] * Bt[N,K]^T, fp32
+// accumulation, bf16 out.  A = activations (row-major), Bt = the weight
+// pre-packed K-major at bind time (the reference MatMul weight is [K,N],
+// /root/reference/proj/src/kernels_scalar.cpp:40-66).
+//
+// tcgen05 path (sm_100a), one CTA per SM, persistent over output tiles:
+//   warp 0      TMA producer: A 128x64 and B 256x64 bf16 tiles (128B swizzle)
+//               into a 4-stage shared-memory ring (48 KB / stage)
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma
+//               (M=128, N=256, K=16, kind::f16) into a double-buffered TMEM
+//               accumulator (2 x 256 fp32 columns = all 512 TMEM columns)
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> bf16 -> swizzled smem -> TMA
+//               store; each warp owns 32 accumulator lanes (rows)
+// Tiles are rasterised in groups of 16 M-blocks so concurrently resident CTAs
+// share A and B tiles through L2.  `max_ctas` caps the grid (SM partitioning
+// when the GEMM overlaps another stream).
+//
+// gemm_bf16_simt is a plain CUDA-core kernel kept as the numerics cross-check
+// and for direct opf_launch calls on un-packed [K,N] weights.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+
+#include "opflow/device.hpp"
+
+namespace opflow {
+
+namespace {
+
+// ------------------------------------------------------------------ SIMT reference
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const __nv_bfloat16* __restrict__ A,
+                                                        const __nv_bfloat16* __restrict__ B,
+                                                        __nv_bfloat16* __restrict__ C, int64_t M,
+                                                        int64_t N, int64_t K, int64_t lda,
+                                                        int64_t ldc, bool b_kn) {
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ float As[BK][BM + 1];
+  __shared__ float Bs[BK][BN + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM, n0 = static_cast<int64_t>(blockIdx.x) * BN;
+  float acc[4][4] = {};
+  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+    for (int i = threadIdx.x; i < BM * BK; i += 256) {
+      const int r = i / BK, c = i % BK;
+      As[c][r] = (m0 + r < M && k0 + c < K) ? __bfloat162float(A[(m0 + r) * lda + k0 + c]) : 0.0f;
+    }
+    for (int i = threadIdx.x; i < BN * BK; i += 256) {
+      const int n = i / BK, c = i % BK;
+      float v = 0.0f;
+      if (n0 + n < N && k0 + c < K)
+        v = __bfloat162float(b_kn ? B[(k0 + c) * N + n0 + n] : B[(n0 + n) * K + k0 + c]);
+      Bs[c][n] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += As[kk][ty * 4 + i] * Bs[kk][tx * 4 + j];
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t r = m0 + ty * 4 + i, c = n0 + tx * 4 + j;
+      if (r < M && c < N) C[r * ldc + c] = __float2bfloat16(acc[i][j]);
+    }
+}
+
+// ------------------------------------------------------------------ tcgen05 path
+constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int kStages = 4;
+constexpr int kAccStages = 2;
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 64 + kEpiWarps * 32;  // TMA warp, MMA warp, 4 epilogue warps
+constexpr uint32_t kABytes = BM * BK * 2;      // 16 KB
+constexpr uint32_t kBBytes = BN * BK * 2;      // 32 KB
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr uint32_t kEpiBytes = 32 * 128;       // one warp's 32 rows x 64 cols bf16 (swizzled)
+constexpr uint32_t kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes +
+                                kEpiWarps * 2 * kEpiBytes + 256 /*barriers*/;
+constexpr int kGroupM = 16;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0,
+                                             int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+
+// K-major, 128-byte swizzle UMMA shared-memory descriptor (sm_100 format:
+// start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version=1 [46,48),
+// layout SWIZZLE_128B=2 [61,64)).  Rows are 128 B, 8-row atoms are 1024 B apart.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;             // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;     // SBO
+  d |= static_cast<uint64_t>(1) << 46;             // descriptor version
+  d |= static_cast<uint64_t>(2) << 61;             // SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: D=f32, A=B=bf16, K-major both, M=128, N=256.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                            (static_cast<uint32_t>(BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t m_blocks, int64_t n_blocks,
+                                            int64_t& mb, int64_t& nb) {
+  const int64_t per_group = static_cast<int64_t>(kGroupM) * n_blocks;
+  const int64_t g = t / per_group;
+  const int64_t first_m = g * kGroupM;
+  const int64_t gm = min(static_cast<int64_t>(kGroupM), m_blocks - first_m);
+  const int64_t r = t % per_group;
+  mb = first_m + r % gm;
+  nb = r / gm;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_base = smem;
+  uint8_t* epi_base = smem + kStages * kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + kEpiWarps * 2 * kEpiBytes);
+  uint64_t* full = bars;                      // [kStages]
+  uint64_t* empty = bars + kStages;           // [kStages]
+  uint64_t* tfull = bars + 2 * kStages;       // [kAccStages]
+  uint64_t* tempty = bars + 2 * kStages + kAccStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAccStages);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t m_blocks = (M + BM - 1) / BM, n_blocks = (N + BN - 1) / BN;
+  const int64_t tiles = m_blocks * n_blocks;
+  const int k_blocks = static_cast<int>((K + BK - 1) / BK);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_c)) : "memory");
+    }
+    // whole warp: allocate all 512 TMEM columns (2 accumulators x 256 fp32)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  } else if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < kAccStages; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int64_t mb, nb;
+        tile_coords(t, m_blocks, n_blocks, mb, nb);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = stage_base + stage * kStageBytes;
+          mbar_expect_tx(&full[stage], kStageBytes);
+          tma_load_2d(sa, &map_a, &full[stage], kb * BK, static_cast<int32_t>(mb * BM));
+          tma_load_2d(sa + kABytes, &map_b, &full[stage], kb * BK, static_cast<int32_t>(nb * BN));
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(stage_base + stage * kStageBytes);
+          const uint32_t sb = sa + kABytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_f16(d_tmem, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32),
+                     (kb | k) != 0);
+          umma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (++acc == kAccStages) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {  // ---------------- epilogue warps
+    const int ew = warp - 2;         // 0..3
+    const int quarter = warp % 4;    // TMEM lane quarter this warp may access
+    uint8_t* stg[2] = {epi_base + (ew * 2) * kEpiBytes, epi_base + (ew * 2 + 1) * kEpiBytes};
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int buf = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      int64_t mb, nb;
+      tile_coords(t, m_blocks, n_blocks, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t row0 = mb * BM + quarter * 32;
+#pragma unroll 1
+      for (int chunk = 0; chunk < BN / 64; ++chunk) {
+        uint32_t v0[32], v1[32];
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                               static_cast<uint32_t>(acc * BN + chunk * 64);
+        tmem_ld32(taddr, v0);
+        tmem_ld32(taddr + 32, v1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        // staging buffer reuse: the TMA store issued two chunks ago must have read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint8_t* sbuf = stg[buf];
+        const int r = lane;  // accumulator row within this warp's 32
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {  // 16-byte chunk j = columns 8j..8j+7
+          const uint32_t* src = j < 4 ? &v0[8 * j] : &v1[8 * (j - 4)];
+          uint4 q;
+          q.x = pack_bf16(src[0], src[1]);
+          q.y = pack_bf16(src[2], src[3]);
+          q.z = pack_bf16(src[4], src[5]);
+          q.w = pack_bf16(src[6], src[7]);
+          *reinterpret_cast<uint4*>(sbuf + r * 128 + ((j ^ (r & 7)) * 16)) = q;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && row0 < M) {
+          tma_store_2d(&map_c, sbuf, static_cast<int32_t>(nb * BN + chunk * 64),
+                       static_cast<int32_t>(row0));
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        buf ^= 1;
+      }
+      // accumulator fully read: hand it back to the MMA warp
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == kAccStages) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fail(Errc::SchedulerError, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld_elems,
+                     uint32_t box_inner, uint32_t box_outer) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems) * 2};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                                 dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  require(r == CUDA_SUCCESS, Errc::SchedulerError,
+          "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
+}  // namespace
+
+void gemm_bf16_simt(const GemmArgs& g, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((g.n + 63) / 64), static_cast<unsigned>((g.m + 63) / 64));
+  gemm_simt_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(g.a),
+                                        static_cast<const __nv_bfloat16*>(g.bt),
+                                        static_cast<__nv_bfloat16*>(g.c), g.m, g.n, g.k, g.lda,
+                                        g.ldc, g.b_kn);
+}
+
+void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
+  require(g.k % 8 == 0 && g.lda % 8 == 0 && g.ldc % 8 == 0, Errc::ShapeMismatch,
+          "tcgen05 GEMM needs 16-byte aligned rows (K, lda, ldc multiples of 8)");
+  require((reinterpret_cast<uintptr_t>(g.a) | reinterpret_cast<uintptr_t>(g.bt) |
+           reinterpret_cast<uintptr_t>(g.c)) % 16 == 0,
+          Errc::ShapeMismatch, "tcgen05 GEMM needs 16-byte aligned base pointers");
+  static std::once_flag once;
+  std::call_once(once, [] {
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBytes)));
+  });
+  const CUtensorMap ma = make_map(g.a, g.k, g.m, g.lda, BK, BM);
+  const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN);
+  const CUtensorMap mc = make_map(g.c, g.n, g.m, g.ldc, 64, 32);
+  const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN);
+  int grid = num_sms();
+  if (g.max_ctas > 0 && g.max_ctas < grid) grid = g.max_ctas;
+  if (tiles < grid) grid = static_cast<int>(tiles);
+  gemm_tc_kernel<<<grid, kThreads, kSmemBytes, s>>>(ma, mb, mc, g.m, g.n, g.k);
+}
+
+}  // namespace opflow
