@@ -1,0 +1,388 @@
+#!/usr/bin/env python3
+"""Headline benchmark (BASELINE.json): tokens/s of the overlapped schedule vs the
+same engine's sequential schedule, Llama-3-8B-shaped layers, TP = --gpus.
+
+Workload (default): Llama-3-8B-shaped 32-layer prefill, 8192 tokens per GPU
+(8 sequences x 1024), bf16, synthetic seeded inputs and random-init weights,
+TP = N (one process per GPU, NCCL over NVLink for the all-reduces).
+A "step" = one forward of the whole schedule (a CUDA-graph replay).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`value` = whole-job tokens/s with inputs resident in HBM (CUDA events, max over
+ranks).  `e2e` = the same metric through the C-ABI with pinned host input /
+output copies inside the timed region.  `roofline` = the dominant kernel (the
+tcgen05 GEMM) timed alone with CUDA events on its stream.  `cpu_baseline` /
+`--impl reference` = the reference's own eval_reference (compiled from its
+sources into oracle/_ref) on the box's host cores, bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS = {"hbm_gbs": 6513.8, "bf16_tflops": 1646.1, "bf16_tflops_sustained": 1381.1}
+try:
+    PEAKS.update(json.loads((ROOT / "MEASURED_PEAKS.json").read_text()))
+    PEAK_SRC = "measured"
+except Exception:  # noqa: BLE001
+    PEAK_SRC = "fallback"
+
+LLAMA = dict(hidden=4096, heads=32, kv_heads=8, head_dim=128, inter=14336)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--layers", type=int, default=32)
+    p.add_argument("--tokens", type=int, default=8192)
+    p.add_argument("--seq-len", type=int, default=1024)
+    p.add_argument("--workload", default="prefill", choices=["prefill", "decode"])
+    p.add_argument("--strategies", default="auto")
+    p.add_argument("--cpu-seconds", type=float, default=20.0)
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    def __init__(self, dev: int):
+        self.dev, self.samples, self.stop = dev, [], threading.Event()
+        self.t = threading.Thread(target=self.loop, daemon=True)
+
+    def loop(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,"
+                     "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                f = [x.strip() for x in out.strip().split(",")]
+                self.samples.append(f)
+            except Exception:  # noqa: BLE001
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=6)
+
+    def summary(self):
+        import statistics
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons}
+
+
+# ------------------------------------------------------------------ distributed
+def dist_init(n):
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    return rank, world, local
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ our engine
+def build_session(of, desc, rules, dev, comm, seed):
+    import torch
+    g = of.build_graph(desc)
+    plan = of.partition(g, rules)
+    sess = of.Session(g, plan, {"lanes": 3, "device": dev.index}, comm)
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    bufs = {}
+    seq = int(json.loads(desc)["operators"][3]["attrs"]["params"].get("seq_len", 1)) if False else None
+    for t in g.description["tensors"]:
+        if t["role"] not in ("input", "weight", "output"):
+            continue
+        shape = t["shape"]
+        if t["name"] == "positions":
+            continue
+        dt = torch.bfloat16 if t.get("dtype") == "bf16" else torch.int64
+        if t["role"] == "output":
+            x = torch.empty(shape, dtype=dt, device=dev)
+        elif t["name"].endswith("norm.w"):
+            x = (1.0 + 0.1 * (torch.rand(shape, device=dev, generator=gen) - 0.5)).to(dt)
+        elif t["role"] == "weight":
+            x = ((torch.rand(shape, device=dev, generator=gen) * 2 - 1) / shape[0] ** 0.5).to(dt)
+        else:
+            x = (torch.rand(shape, device=dev, generator=gen) * 2 - 1).to(dt)
+        bufs[t["name"]] = x
+        sess.bind(t["name"], x)
+    return g, plan, sess, bufs
+
+
+def time_steps(torch, fn, steps, warmup, stream, world):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    barrier(world)
+    return allreduce_max(ms, world)
+
+
+def gemm_roofline(of, torch, dev, shapes, reps=20):
+    """Time each projection GEMM alone (tcgen05 kernel, CUDA events on its
+    stream, inputs > L2 rotated); FLOP-weighted achieved TFLOP/s."""
+    tot_flops, tot_ms, rows = 0.0, 0.0, []
+    stream = torch.cuda.current_stream(dev)
+    for name, (m, k, n) in shapes.items():
+        desc = json.dumps({"tensors": [
+            {"name": "a", "shape": [m, k], "dtype": "bf16", "role": "input"},
+            {"name": "w", "shape": [k, n], "batch": "replicated", "dtype": "bf16", "role": "weight"},
+            {"name": "c", "shape": [m, n], "dtype": "bf16", "role": "output"}],
+            "operators": [{"name": "mm", "kind": "MatMul", "inputs": ["a", "w"], "outputs": ["c"]}]})
+        g = of.build_graph(desc)
+        sess = of.Session(g, of.partition(g, []), {"lanes": 1, "device": dev.index})
+        a = torch.randn(m, k, device=dev, dtype=torch.bfloat16)
+        w = (torch.randn(k, n, device=dev, dtype=torch.bfloat16) / k ** 0.5).to(torch.bfloat16)
+        c = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+        sess.bind("a", a), sess.bind("w", w), sess.bind("c", c)
+        for _ in range(3):
+            sess.run(None, stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            sess.run(None, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        fl = 2.0 * m * n * k
+        tot_flops += fl
+        tot_ms += ms
+        rows.append({"gemm": name, "m": m, "n": n, "k": k, "ms": round(ms, 4),
+                     "tflops": round(fl / ms / 1e9, 1)})
+        del sess
+    achieved = tot_flops / tot_ms / 1e9
+    return achieved, rows
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    from paper_2605_21603_b200 import opflow as of
+
+    rank, world, local = dist_init(args.gpus)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        uid = [of.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = of.Comm(world, rank, local, uid[0])
+    tp = world
+    T, S, L = args.tokens, args.seq_len, args.layers
+    desc = of.llama_graph(layers=L, tokens=T, seq_len=S, tp=tp, dtype="bf16", **LLAMA)
+    rules = [of.PartitionRule.by_func("AllReduce"), of.PartitionRule.by_func("add_rmsnorm")] if tp > 1 else []
+    g, plan, sess, bufs = build_session(of, desc, rules, dev, comm, seed=1234 + rank)
+    pos = (torch.arange(T, device=dev) % S).to(torch.int64)
+    bufs["positions"] = pos
+    sess.bind("positions", pos)
+    stream = torch.cuda.current_stream(dev)
+
+    cands = {"sequential": {"name": "sequential"}}
+    if args.strategies == "auto":
+        cands["nanoflow_u2"] = {"name": "split_overlap", "n_microbatches": 2, "align": S, "lane_mode": "ubatch"}
+        cands["nanoflow_class"] = {"name": "split_overlap", "n_microbatches": 2, "align": S}
+        if tp > 1:
+            cands["tokenweave"] = {"name": "fuse_norm_comm", "align": S}
+    else:
+        for s in args.strategies.split(","):
+            cands[s] = json.loads(s) if s.startswith("{") else {"name": s, "align": S}
+    results = {}
+    out_name = [t["name"] for t in g.description["tensors"] if t["role"] == "output"][0]
+    with Clocks(local) as clk:
+        for name, spec in cands.items():
+            ms = time_steps(torch, lambda: sess.run(spec, stream), args.steps, args.warmup, stream, world)
+            results[name] = ms
+    best = min((k for k in results if k != "sequential"), key=lambda k: results[k], default="sequential")
+    seq_ms, best_ms = results["sequential"], results[best]
+    tokens_job = T * 1  # TP: every rank processes the same T tokens of one replica
+    value = tokens_job / (best_ms / 1e3)
+    stats = sess.stats()
+    launches = stats["last"]["launches"]
+
+    # ---- e2e through the C-ABI with host buffers (pinned), copies in the timed region
+    xh = torch.empty(T, LLAMA["hidden"], dtype=torch.bfloat16, pin_memory=True)
+    xh.copy_(bufs["x"].cpu())
+    oh = torch.empty(T, LLAMA["hidden"], dtype=torch.bfloat16, pin_memory=True)
+    spec = cands[best]
+
+    def e2e_step():
+        bufs["x"].copy_(xh, non_blocking=True)
+        sess.run(spec, stream)
+        oh.copy_(bufs[out_name], non_blocking=True)
+
+    e2e_ms = time_steps(torch, e2e_step, args.steps, args.warmup, stream, world)
+    e2e_val = tokens_job / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (tcgen05 GEMM), per-rank shapes
+    H, I = LLAMA["hidden"], LLAMA["inter"] // tp
+    nq, nkv, hd = LLAMA["heads"] // tp, LLAMA["kv_heads"] // tp, LLAMA["head_dim"]
+    shapes = {"qkv": (T, H, (nq + 2 * nkv) * hd), "o": (T, nq * hd, H), "gate_up": (T, H, 2 * I),
+              "down": (T, I, H)}
+    achieved, gemm_rows = gemm_roofline(of, torch, dev, shapes) if rank == 0 else (0.0, [])
+    flops_layer = sum(2.0 * m * k * n for (m, k, n) in shapes.values())
+    line = None
+    if rank == 0:
+        cpu = None if args.no_cpu else cpu_baseline(args, T, S, tp)
+        line = {
+            "metric": "tokens/sec overlapped vs sequential schedule, Llama-3-8B layer TP=1/2/4/8",
+            "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(best_ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded uniform inputs, random-init weights)",
+            "config": {"workload": f"llama3-8b-shaped prefill, {L} layers, {T} tokens "
+                                   f"({T // S} seqs x {S}) per replica, TP={tp}",
+                       "model": "Llama-3-8B-shaped (random init)", "global_batch": T // S,
+                       "seq_len": S, "parallelism": f"tp{tp}", "strategy": best,
+                       "inputs_vs_l2": "activations/weights > 126 MB L2 (no flush needed)"},
+            "sequential": {"ms_per_step": round(seq_ms, 3), "tokens_per_s": round(T / (seq_ms / 1e3), 1)},
+            "strategies_ms": {k: round(v, 3) for k, v in results.items()},
+            "speedup_vs_sequential": round(seq_ms / best_ms, 4),
+            "e2e": {"value": round(e2e_val, 1), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(xh.numel() * 2),
+                    "d2h_bytes_per_step": int(oh.numel() * 2)},
+            "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05, bf16)",
+                         "achieved": round(achieved, 1),
+                         "peak": PEAKS["bf16_tflops"], "unit": "TFLOP/s",
+                         "frac": round(achieved / PEAKS["bf16_tflops"], 4),
+                         "peak_source": PEAK_SRC + " burst (kernel timed alone)",
+                         "traffic": None, "per_gemm": gemm_rows,
+                         "algorithmic_flops_per_layer": flops_layer,
+                         "gemm_share_of_step_at_roofline": round(
+                             flops_layer * L / (PEAKS["bf16_tflops"] * 1e12) * 1e3 / best_ms, 4)},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches) * args.steps,
+            "plan": {"dispatches": stats["last"]["dispatches"], "launches_per_step": launches,
+                     "copied_elements": stats["last"]["copied_elements"],
+                     "arena_bytes": stats["arena_bytes"]},
+        }
+        print(json.dumps(line), flush=True)
+    barrier(world)
+
+
+# ------------------------------------------------------------------ reference (CPU)
+def _ref_worker(args_tuple):
+    desc, rows, seed = args_tuple
+    sys.path.insert(0, str(ROOT))
+    from oracle import ref
+    from paper_2605_21603_b200.workloads import llama_inputs
+    ins = llama_inputs(desc, rows, seed=seed)
+    _, secs = ref.evaluate(desc, rows, ins, timed=True)
+    return secs
+
+
+def cpu_baseline(args, T, S, tp, budget_s=None):
+    """Reference eval_reference (oracle/_ref, compiled from the reference's
+    sources, AVX2 lane, single-threaded by construction) on a bounded sample:
+    1 Llama layer of `rows` tokens per process, one process per host core, each
+    a disjoint sequence; tokens/s is extrapolated to the full workload as
+    (tokens / s per layer) / layers."""
+    import multiprocessing as mp
+    from oracle import ref
+    if not ref.available():
+        return None
+    from paper_2605_21603_b200 import opflow as of
+    cores = os.cpu_count() or 1
+    rows = 128 if S >= 128 else S
+    desc = of.llama_graph(layers=1, tokens=rows, seq_len=rows, tp=tp, dtype="f32", **LLAMA)
+    t0 = time.time()
+    with mp.get_context("fork").Pool(cores) as pool:
+        secs = pool.map(_ref_worker, [(desc, rows, 17 + i) for i in range(cores)])
+    wall = time.time() - t0
+    per_layer_tok_s = cores * rows / max(secs)
+    return {"value": round(per_layer_tok_s / args.layers, 2), "unit": "tokens/s",
+            "cores": cores, "kind": "reference",
+            "sample": f"{cores} procs x 1 Llama-3-8B-shaped layer x {rows} tokens (fp32, eval_reference "
+                      f"AVX2 lane, backend={ref.backend()}), extrapolated to {args.layers} layers; "
+                      f"{max(secs):.1f}s per layer, wall {wall:.1f}s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libopflow_ref.so not built"}))
+        return
+    T, S = args.tokens, args.seq_len
+    tp = max(1, args.gpus)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(args, T, S, tp)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+        if len(vals) >= 1 and i >= args.warmup:
+            break  # each step is a ~20 s bounded sample; one timed sample keeps the run short
+    v = sum(vals) / len(vals)
+    print(json.dumps({
+        "impl": "reference", "metric": "tokens/sec overlapped vs sequential schedule, Llama-3-8B layer TP=1/2/4/8",
+        "value": round(v, 2), "unit": "tokens/s", "n_gpus": args.gpus, "steps": len(vals),
+        "warmup": args.warmup, "higher_is_better": True, "dtype": "f32",
+        "config": {"workload": f"llama3-8b-shaped prefill, {args.layers} layers, {T} tokens, TP={tp}"},
+        "cpu_baseline": cb, "e2e": {"value": round(v, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                                    "d2h_bytes_per_step": 0}}), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -63,7 +63,7 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
     if LIB.exists() and LIB.stat().st_mtime >= newest:
         return LIB
     cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(LIB), *map(str, objs),
-           "-cudart", "static", "-lnccl", "-ldl", "-lpthread",
+           "-cudart", "static", "-ldl", "-lpthread",
            f"-Xlinker=--version-script={CSRC / 'exports.map'}", "-Xlinker=-Bsymbolic"]
     if verbose:
         print(" ".join(cmd), flush=True)

@@ -10,6 +10,7 @@
 
 #include "opflow/builders.hpp"
 #include "opflow/comm.hpp"
+#include "opflow/nccl_api.hpp"
 #include "opflow/engine.hpp"
 #include "opflow/graph.hpp"
 #include "opflow/json.hpp"
@@ -257,8 +258,8 @@ opf_status opf_view_rows(const opf_view* v, int64_t row_off, int64_t nrows, opf_
 opf_status opf_comm_unique_id(uint8_t id_out[128]) {
   return guard([&] {
     ncclUniqueId id;
-    const ncclResult_t r = ncclGetUniqueId(&id);
-    require(r == ncclSuccess, Errc::SchedulerError, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    const ncclResult_t r = nccl().GetUniqueId(&id);
+    require(r == ncclSuccess, Errc::SchedulerError, std::string("ncclGetUniqueId: ") + nccl().GetErrorString(r));
     static_assert(sizeof(id) == 128);
     std::memcpy(id_out, &id, 128);
   });
@@ -275,9 +276,9 @@ opf_status opf_comm_init(const uint8_t id[128], int32_t world, int32_t rank, int
     if (world > 1) {
       ncclUniqueId uid;
       std::memcpy(&uid, id, 128);
-      const ncclResult_t r = ncclCommInitRank(&c->nccl, world, uid, rank);
+      const ncclResult_t r = nccl().CommInitRank(&c->nccl, world, uid, rank);
       require(r == ncclSuccess, Errc::SchedulerError,
-              std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+              std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
     }
     *out = c.release();
   });
@@ -285,7 +286,7 @@ opf_status opf_comm_init(const uint8_t id[128], int32_t world, int32_t rank, int
 
 void opf_comm_free(opf_comm* c) {
   if (!c) return;
-  if (c->nccl) ncclCommDestroy(c->nccl);
+  if (c->nccl) nccl().CommDestroy(c->nccl);
   delete c;
 }
 

@@ -554,7 +554,7 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
   cp->end_live_tensors = 0;
   for (int32_t t = 0; t < NT; ++t)
     for (int32_t u = 0; u < U; ++u)
-      if (g_.tensors[t].producer >= 0 && mb[u].states[t].ref_count > 0) {
+      if (g_.tensors[t].producer >= 0 && !g_.is_output(t) && mb[u].states[t].ref_count > 0) {
         ++cp->end_live_tensors;
         break;
       }

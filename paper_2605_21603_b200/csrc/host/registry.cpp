@@ -4,6 +4,7 @@
 #include <map>
 
 #include "opflow/comm.hpp"
+#include "opflow/nccl_api.hpp"
 #include "opflow/device.hpp"
 
 namespace opflow {
@@ -150,10 +151,10 @@ opf_status launch_kind(const opf_op_ctx& c, const opf_view* in, int n_in, opf_vi
                                                    " != communicator size " +
                                                    std::to_string(comm->world));
           const ncclResult_t r =
-              ncclAllReduce(view_ptr(in[0]), view_ptr(out[0]), static_cast<size_t>(view_numel(in[0])),
+              nccl().AllReduce(view_ptr(in[0]), view_ptr(out[0]), static_cast<size_t>(view_numel(in[0])),
                             nccl_type(in[0].dtype), ncclSum, comm->nccl, s);
           if (r != ncclSuccess)
-            return op_error(Errc::SchedulerError, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+            return op_error(Errc::SchedulerError, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
           return 0;
         }
         // single device: the reference stand-in (sum of world_size identical replicas)

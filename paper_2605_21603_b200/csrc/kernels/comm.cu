@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 
 #include "opflow/comm.hpp"
+#include "opflow/nccl_api.hpp"
 #include "opflow/device.hpp"
 
 namespace opflow {
@@ -147,11 +148,11 @@ opf_status launch_ar_norm(const opf_comm* comm, const opf_view& o, const opf_vie
   if (comm && comm->world > 1) {
     // NCCL all-reduce into the workspace, then one fused add+norm pass.
     T* red = static_cast<T*>(workspace);
-    const ncclResult_t r = ncclAllReduce(src, red, static_cast<size_t>(rows * H),
+    const ncclResult_t r = nccl().AllReduce(src, red, static_cast<size_t>(rows * H),
                                          std::is_same_v<T, float> ? ncclFloat32 : ncclBfloat16,
                                          ncclSum, comm->nccl, s);
     if (r != ncclSuccess)
-      return op_error(Errc::SchedulerError, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+      return op_error(Errc::SchedulerError, std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
     src = red;
     scale = 1.0f;
   }

@@ -1,0 +1,262 @@
+"""GPU parity (run on a B200): every schedule the engine executes must
+reproduce the reference's outputs.
+
+* reference stand-in graphs (i64 / f32): BIT-EXACT vs the compiled reference
+  eval_reference (oracle/_ref) — the device kernels keep the reference's
+  rounding sequence (kernels/standin.cu);
+* Llama-shaped graphs: fp32 toy normwise rel <= 1e-4, bf16 rel <= 2e-2 vs the
+  fp32 oracle (north-star tolerances), and tcgen05 GEMM vs torch.
+"""
+import json
+import random
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2605_21603_b200 import opflow as of
+from paper_2605_21603_b200.workloads import llama_inputs, rel_err, standin_inputs
+from util import random_graph, unit_costs
+
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("built")]
+R = of.PartitionRule
+
+
+def run_graph(desc, rows, host, strategy, rules=(), config=None, dev="cuda:0", repeat=1):
+    import torch
+    g = of.build_graph(desc)
+    plan = of.partition(g, list(rules))
+    sess = of.Session(g, plan, config or {"lanes": 3})
+    keep = {}
+    for name, arr in host.items():
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+        tdesc = g.description["tensors"][g.tensor_id(name)]
+        if tdesc.get("dtype") == "bf16":
+            t = t.to(torch.bfloat16)
+        keep[name] = t.contiguous()
+        sess.bind(name, keep[name])
+    outs = {}
+    for t in g.description["tensors"]:
+        if t["role"] == "output":
+            shape = list(t["shape"])
+            shape[0] = rows
+            dt = {"i64": torch.int64, "f32": torch.float32, "bf16": torch.bfloat16}[t.get("dtype", "i64")]
+            outs[t["name"]] = torch.empty(shape, dtype=dt, device=dev)
+            sess.bind(t["name"], outs[t["name"]])
+    for _ in range(repeat):
+        sess.run(strategy)
+    torch.cuda.synchronize()
+    res = {k: (v.float() if v.dtype == torch.bfloat16 else v).cpu().numpy() for k, v in outs.items()}
+    return res, sess
+
+
+def reference_outputs(ref_mod, desc, rows, host):
+    if ref_mod is not None and ref_mod.available():
+        return ref_mod.evaluate(desc, rows, host)
+    return oracle.evaluate(desc, rows, host)
+
+
+@pytest.fixture(scope="module")
+def refmod():
+    from oracle import ref
+    return ref if ref.available() else None
+
+
+STRATS = [
+    {"name": "sequential"},
+    {"name": "split_overlap", "n_microbatches": 2},
+    {"name": "split_overlap", "n_microbatches": 3, "lane_mode": "ubatch"},
+    {"name": "split_overlap", "sizes": [1, 6, 3]},
+]
+
+
+@pytest.mark.parametrize("builder", ["dense_tp", "moe_ep", "fuse_chain"])
+@pytest.mark.parametrize("dtype", ["i64", "f32"])
+def test_standin_graphs_bit_exact(cuda, refmod, builder, dtype):
+    desc = of.builder_json(builder, layers=2, batch=10, hidden=48, dtype=dtype, costs=unit_costs())
+    host = standin_inputs(desc, 10, seed=11)
+    want = reference_outputs(refmod, desc, 10, host)
+    for strat in STRATS:
+        got, sess = run_graph(desc, 10, host, strat)
+        for k in want:
+            assert np.array_equal(got[k].view(np.uint8), want[k].view(np.uint8)), (builder, strat)
+        assert sess.stats()["last"]["copied_elements"] == 0
+
+
+def test_dbo_and_fuse_norm_comm_bit_exact(cuda, refmod):
+    desc = of.moe_ep_graph(2, 16, 64, dtype="i64", costs=unit_costs())
+    host = standin_inputs(desc, 16, seed=5)
+    want = reference_outputs(refmod, desc, 16, host)
+    dbo_rules = [R.by_module("layer*.attn"), R.by_module("layer*.moe.dispatch"),
+                 R.by_module("layer*.moe.experts"), R.by_module("layer*.moe.combine")]
+    got, sess = run_graph(desc, 16, host, {"name": "dbo"}, dbo_rules)
+    for k in want:
+        assert np.array_equal(got[k], want[k])
+    sched = sess.schedule()
+    merged = [d for d in sched["dispatches"] if d["kind"] == "merged"]
+    assert {d["labels"][0] for d in merged} == {"layer0.attn", "layer1.attn"}
+    assert sess.stats()["last"]["copied_elements"] == 0
+    for dtype in ("i64", "f32"):
+        desc = of.fuse_chain_graph(2, 12, 64, dtype=dtype, costs=unit_costs())
+        host = standin_inputs(desc, 12, seed=6)
+        want = reference_outputs(refmod, desc, 12, host)
+        got, sess = run_graph(desc, 12, host, {"name": "fuse_norm_comm"},
+                              [R.by_func("AllReduce"), R.by_func("RowScale")])
+        assert any(d["kind"] == "fused" for d in sess.schedule()["dispatches"])
+        for k in want:
+            assert np.array_equal(got[k].view(np.uint8), want[k].view(np.uint8))
+
+
+class RandomStrategy(of.Scheduler):
+    """Random legal schedules: random split, random merges, random lanes."""
+
+    def __init__(self, seed):
+        self.rng = random.Random(seed)
+        self.cache_key = f"random{seed}"
+
+    def schedule(self, ctx):
+        rows = ctx.rows
+        n = self.rng.randint(1, min(4, rows))
+        cuts = sorted(self.rng.sample(range(1, rows), n - 1)) if n > 1 else []
+        sizes = [b - a for a, b in zip([0] + cuts, cuts + [rows])]
+        ctx.split(sizes)
+        U = len(sizes)
+        while ctx.unfinished():
+            ready = {u: ctx.get_ready_ops(u) for u in range(U)}
+            # merge a subgraph across a contiguous ready range sometimes
+            for u in range(U):
+                if not ready[u]:
+                    continue
+                h = self.rng.choice(ready[u])
+                group = [h]
+                v = u + 1
+                while v < U and self.rng.random() < 0.5 and any(x.subgraph == h.subgraph for x in ready[v]):
+                    group.append(ctx.handle(h.subgraph, v))
+                    v += 1
+                ctx.execute(group, lane=self.rng.randrange(3))
+                break
+
+
+def test_random_graphs_random_schedules_bit_exact(cuda, refmod):
+    """SPEC acceptance 1-3: schedule independence, Algorithm-1 conservation,
+    zero-copy vs the copying fallback (prealloc off)."""
+    rng = random.Random(2024)
+    for trial in range(40):
+        desc = random_graph(rng, batch=12, hidden=16)
+        host = standin_inputs(desc, 12, seed=trial)
+        want = reference_outputs(refmod, desc, 12, host)
+        rules = [R.by_func("All*")] if trial % 2 else [R.by_module("m0")]
+        got, sess = run_graph(desc, 12, host, RandomStrategy(trial), rules)
+        st = sess.stats()["last"]
+        assert st["copied_elements"] == 0 and st["end_live_tensors"] == 0
+        for k in want:
+            assert np.array_equal(got[k], want[k]), trial
+        got2, sess2 = run_graph(desc, 12, host, RandomStrategy(trial), rules,
+                                config={"lanes": 3, "prealloc": False})
+        for k in want:
+            assert np.array_equal(got2[k], want[k]), trial
+
+
+def test_plan_cache_and_graph_replay(cuda, refmod):
+    desc = of.dense_tp_graph(2, 32, 64, dtype="f32", costs=unit_costs())
+    host = standin_inputs(desc, 32, seed=1)
+    want = reference_outputs(refmod, desc, 32, host)
+    got, sess = run_graph(desc, 32, host, {"name": "split_overlap"}, repeat=3)
+    st = sess.stats()
+    assert st["plan_cache_misses"] == 1 and st["plan_cache_hits"] == 2 and st["last"]["captured"]
+    for k in want:
+        assert np.array_equal(got[k], want[k])
+
+
+def test_toy_decoder_fp32(cuda):
+    """BASELINE configs[0]: 2-layer toy decoder d=512, 8 heads, seq 128, batch 8, fp32."""
+    desc = of.toy_decoder_graph()
+    host = llama_inputs(desc, 1024, seed=2026)
+    want = oracle.evaluate(desc, 1024, host, exact=False)
+    for strat in [{"name": "sequential"}, {"name": "split_overlap", "align": 128},
+                  {"name": "split_overlap", "n_microbatches": 4, "align": 128, "lane_mode": "ubatch"}]:
+        got, _ = run_graph(desc, 1024, host, strat)
+        for k in want:
+            assert rel_err(got[k], want[k]) < 1e-4, strat
+
+
+@pytest.mark.parametrize("tp", [1, 2])
+def test_llama_bf16_layers(cuda, tp):
+    desc = of.llama_graph(layers=2, tokens=512, seq_len=128, hidden=1024, heads=16, kv_heads=4,
+                          head_dim=64, inter=2048, tp=tp, dtype="bf16")
+    host = llama_inputs(desc, 512, seed=tp)
+    want = oracle.evaluate(desc, 512, host, exact=False)
+    strats = [({"name": "sequential"}, []),
+              ({"name": "split_overlap", "align": 128}, []),
+              ({"name": "split_overlap", "align": 128, "lane_mode": "ubatch"}, [])]
+    if tp > 1:
+        strats.append(({"name": "fuse_norm_comm", "align": 128},
+                       [R.by_func("AllReduce"), R.by_func("add_rmsnorm")]))
+    for strat, rules in strats:
+        got, _ = run_graph(desc, 512, host, strat, rules)
+        for k in want:
+            assert rel_err(got[k], want[k]) < 2e-2, (strat, k, rel_err(got[k], want[k]))
+
+
+def test_llama_decode_bf16(cuda):
+    desc = of.llama_decode_graph(layers=1, tokens=16, hidden=512, heads=8, kv_heads=2, head_dim=128,
+                                 inter=1024, ctx_len=300, page_size=16, dtype="bf16")
+    host = llama_inputs(desc, 16, seed=4, ctx_len=257)
+    want = oracle.evaluate(desc, 16, host, exact=False)
+    for strat in [{"name": "sequential"}, {"name": "split_overlap", "lane_mode": "ubatch"}]:
+        got, _ = run_graph(desc, 16, host, strat)
+        for k in want:
+            assert rel_err(got[k], want[k]) < 2e-2
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 512, 1024), (300, 520, 200), (1, 256, 64),
+                                   (2048, 6144, 4096), (8192, 4096, 512), (77, 3000, 1032)])
+def test_gemm_tcgen05_vs_torch(cuda, m, n, k):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n)
+    a = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w = ((torch.rand(k, n, device="cuda", generator=g) * 2 - 1) / k ** 0.5).to(torch.bfloat16)
+    desc = json.dumps({"tensors": [{"name": "a", "shape": [m, k], "dtype": "bf16", "role": "input"},
+                                   {"name": "w", "shape": [k, n], "batch": "replicated", "dtype": "bf16", "role": "weight"},
+                                   {"name": "c", "shape": [m, n], "dtype": "bf16", "role": "output"}],
+                       "operators": [{"name": "mm", "kind": "MatMul", "inputs": ["a", "w"], "outputs": ["c"]}]})
+    gr = of.build_graph(desc)
+    sess = of.Session(gr, of.partition(gr, []), {"lanes": 1})
+    c = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    sess.bind("a", a)
+    sess.bind("w", w)
+    sess.bind("c", c)
+    sess.run()
+    torch.cuda.synchronize()
+    want = a.float() @ w.float()
+    err = ((c.float() - want).norm() / want.norm()).item()
+    assert err < 1e-2, err
+    # the CUDA-core reference path (direct opf_launch on the [K,N] weight) agrees
+    c2 = torch.empty_like(c)
+    of.launch({"name": "mm", "kind": "MatMul", "inputs": [], "outputs": []}, [a, w], [c2], m)
+    torch.cuda.synchronize()
+    assert ((c2.float() - want).norm() / want.norm()).item() < 1e-2
+
+
+def test_memory_kernels_vs_oracle(cuda):
+    import torch
+    rng = np.random.default_rng(0)
+    rows, H = 333, 4096
+    x = rng.standard_normal((rows, H)).astype(np.float32)
+    r = rng.standard_normal((rows, H)).astype(np.float32)
+    g = (1 + 0.1 * rng.standard_normal(H)).astype(np.float32)
+    tb = lambda a: torch.from_numpy(a).cuda().to(torch.bfloat16)
+    y = torch.empty(rows, H, dtype=torch.bfloat16, device="cuda")
+    s = torch.empty_like(y)
+    op = {"name": "n", "kind": "Custom", "inputs": [], "outputs": [], "attrs": {"custom_name": "add_rmsnorm", "params": {"eps": 1e-5}}}
+    of.launch(op, [tb(x), tb(r), tb(g)], [s, y], rows)
+    torch.cuda.synchronize()
+    xs = torch.from_numpy(x).to(torch.bfloat16).float().numpy() + torch.from_numpy(r).to(torch.bfloat16).float().numpy()
+    want = oracle.rmsnorm(xs, torch.from_numpy(g).to(torch.bfloat16).float().numpy(), 1e-5)
+    assert rel_err(y.float().cpu().numpy(), want) < 1e-2
+    gu = rng.standard_normal((rows, 2 * 1536)).astype(np.float32)
+    a = torch.empty(rows, 1536, dtype=torch.bfloat16, device="cuda")
+    of.launch({"name": "a", "kind": "Custom", "inputs": [], "outputs": [], "attrs": {"custom_name": "silu_mul"}},
+              [tb(gu)], [a], rows)
+    torch.cuda.synchronize()
+    assert rel_err(a.float().cpu().numpy(), oracle.silu_mul(torch.from_numpy(gu).to(torch.bfloat16).float().numpy())) < 1e-2
