@@ -40,10 +40,12 @@ struct Planner {
     if (x == d) return true;
     return (*vc)[d][(*lane_of)[x]] >= (*seq_of)[x];
   }
-  int32_t alloc(int64_t bytes, int32_t d, bool pinned = false) {
+  // fresh: never recycle a freed block (merge buffers: later producers of other
+  // ubatches write into them on lanes not ordered after the old tenant).
+  int32_t alloc(int64_t bytes, int32_t d, bool pinned = false, bool fresh = false) {
     bytes = align_up(std::max<int64_t>(bytes, 1));
     int32_t best = -1;
-    if (!pinned) {
+    if (!pinned && !fresh) {
       for (int32_t i = 0; i < static_cast<int32_t>(blocks.size()); ++i) {
         const Block& b = blocks[i];
         if (b.live || b.pinned || b.bytes < bytes) continue;
@@ -404,12 +406,18 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
       int32_t blk;
       int64_t base_row;
       if (full) {
-        if (merge_buf[t] < 0) merge_buf[t] = pl.alloc(tensor_bytes_rows(m, total_rows), di);
+        // MergeBuffer: one full-batch block; it stays live until every
+        // ubatch's slice has been produced AND consumed (pending = U).
+        if (merge_buf[t] < 0) {
+          merge_buf[t] = pl.alloc(tensor_bytes_rows(m, total_rows), di, false, /*fresh=*/true);
+          pending(merge_buf[t]) = U;
+        }
         blk = merge_buf[t];
         pl.use(blk, di);
         base_row = r0;
       } else {
         blk = pl.alloc(tensor_bytes_rows(m, nrows), di);
+        pending(blk) = d.u1 - d.u0;
         base_row = 0;
       }
       for (int32_t u = d.u0; u < d.u1; ++u) {
@@ -418,7 +426,6 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
         mb[u].states[t].buffer = blk;
         mb[u].states[t].row_offset = inst[t][u].row_off;
         mb[u].states[t].row_extent = sizes[u];
-        ++pending(blk);
       }
       view_of[t] = arena_view(blk, t, base_row, nrows);
     }
@@ -781,12 +788,14 @@ std::string Session::schedule_json() const {
                "\",\"block_off\":" + std::to_string(vs[k].block_off) +
                ",\"tensor\":" + std::to_string(vs[k].tensor) +
                ",\"elem_offset\":" + std::to_string(vs[k].elem_offset) +
+               ",\"elem_bytes\":" + std::to_string(dtype_bytes(vs[k].dtype)) +
                ",\"shape\":" + json::int_list(vs[k].shape) + "}";
         }
         return o + "]";
       };
       s += "{\"name\":" + json::quote(l.name) + ",\"op\":" + std::to_string(l.op) +
            ",\"copy\":" + (l.is_copy ? "true" : "false") + ",\"rows\":" + std::to_string(l.rows) +
+           ",\"ws_off\":" + std::to_string(l.ws_off) + ",\"ws_bytes\":" + std::to_string(l.ws_bytes) +
            ",\"in\":" + views(l.in) + ",\"out\":" + views(l.out) + "}";
     }
     s += "]}";
