@@ -260,3 +260,28 @@ def test_memory_kernels_vs_oracle(cuda):
               [tb(gu)], [a], rows)
     torch.cuda.synchronize()
     assert rel_err(a.float().cpu().numpy(), oracle.silu_mul(torch.from_numpy(gu).to(torch.bfloat16).float().numpy())) < 1e-2
+
+
+@pytest.mark.parametrize("S,nq,nkv,seqs", [(1024, 8, 2, 2), (128, 4, 4, 3), (200, 4, 1, 2), (64, 2, 2, 1)])
+def test_prefill_attention_tensor_core(cuda, S, nq, nkv, seqs):
+    """tcgen05-era prefill path (mma.sync FA kernel, hd=128) vs the fp64 oracle
+    and the SIMT kernel."""
+    import torch
+    rng = np.random.default_rng(S + nq)
+    hd = 128
+    rows = S * seqs
+    qkv = rng.uniform(-1, 1, (rows, (nq + 2 * nkv) * hd)).astype(np.float32)
+    t = torch.from_numpy(qkv).cuda().to(torch.bfloat16)
+    q32 = t.float().cpu().numpy()
+    want = oracle.attn_prefill(q32, nq, nkv, hd, S)
+    op = {"name": "a", "kind": "Custom", "inputs": [], "outputs": [],
+          "attrs": {"custom_name": "attn_prefill", "params": {"heads": nq, "kv_heads": nkv, "head_dim": hd, "seq_len": S}}}
+    out = torch.empty(rows, nq * hd, dtype=torch.bfloat16, device="cuda")
+    of.launch(op, [t], [out], rows)
+    op2 = json.loads(json.dumps(op))
+    op2["attrs"]["params"]["simt"] = 1
+    out2 = torch.empty_like(out)
+    of.launch(op2, [t], [out2], rows)
+    torch.cuda.synchronize()
+    assert rel_err(out.float().cpu().numpy(), want) < 1e-2
+    assert rel_err(out2.float().cpu().numpy(), want) < 1e-2
