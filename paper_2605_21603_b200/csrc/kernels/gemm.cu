@@ -346,6 +346,219 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
 }
 
+// ------------------------------------------------------------------ 2-CTA (cta_group::2) path
+// A CTA pair (cluster of 2 on one TPC) owns a 256x256 output tile.  Each CTA
+// TMA-loads its own 128 A rows and 128 of the 256 B rows per 64-deep k-block
+// (32 KB / stage instead of 48 KB: half the L2->SM operand traffic per MAC),
+// the leader's single thread issues M=256 N=256 tcgen05.mma over both CTAs'
+// shared memory, and each CTA's TMEM receives its 128 accumulator rows.
+// Full barriers live in the leader (TMA complete_tx from both CTAs lands
+// there); smem-slot and accumulator-ready commits multicast to both CTAs;
+// both CTAs' epilogue warps release the accumulator on the leader's barrier.
+constexpr int kStages2 = 6;
+constexpr uint32_t kStageBytes2 = kABytes + kBBytes / 2;  // 32 KB
+constexpr uint32_t kSmemBytes2 = 1024 + kStages2 * kStageBytes2 + kEpiWarps * 2 * kEpiBytes + 256;
+constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(256 >> 3) << 17) |
+                             (static_cast<uint32_t>(256 >> 4) << 24);
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clear the CTA-rank bit: address the pair leader
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                 int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+      "[%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc2), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+      "%1;" ::"r"(smem_u32(bar)),
+      "h"(static_cast<uint16_t>(0x3))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask)
+               : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                    const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_base = smem;
+  uint8_t* epi_base = smem + kStages2 * kStageBytes2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + kEpiWarps * 2 * kEpiBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages2;
+  uint64_t* tfull = bars + 2 * kStages2;
+  uint64_t* tempty = bars + 2 * kStages2 + kAccStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages2 + 2 * kAccStages);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int64_t m_blocks = (M + 2 * BM - 1) / (2 * BM), n_blocks = (N + BN - 1) / BN;
+  const int64_t tiles = m_blocks * n_blocks;
+  const int k_blocks = static_cast<int>((K + BK - 1) / BK);
+  const int64_t cluster = blockIdx.x / 2, n_clusters = gridDim.x / 2;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_c)) : "memory");
+    }
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  } else if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < kAccStages; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = cluster; t < tiles; t += n_clusters) {
+        int64_t mb, nb;
+        tile_coords(t, m_blocks, n_blocks, mb, nb);
+        const int32_t m0 = static_cast<int32_t>(mb * 2 * BM + rank * BM);
+        const int32_t n0 = static_cast<int32_t>(nb * BN + rank * (BN / 2));
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = stage_base + stage * kStageBytes2;
+          if (leader) mbar_expect_tx(&full[stage], 2 * kStageBytes2);
+          tma_load_2d_pair(sa, &map_a, &full[stage], kb * BK, m0);
+          tma_load_2d_pair(sa + kABytes, &map_b, &full[stage], kb * BK, n0);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader CTA)
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int64_t t = cluster; t < tiles; t += n_clusters) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(stage_base + stage * kStageBytes2);
+          const uint32_t sb = sa + kABytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_f16_pair(d_tmem, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32),
+                          (kb | k) != 0);
+          umma_commit_pair(&empty[stage]);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull[acc]);
+        if (++acc == kAccStages) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {  // ---------------- epilogue warps (both CTAs)
+    const int ew = warp - 2;
+    const int quarter = warp % 4;
+    uint8_t* stg[2] = {epi_base + (ew * 2) * kEpiBytes, epi_base + (ew * 2 + 1) * kEpiBytes};
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int buf = 0;
+    for (int64_t t = cluster; t < tiles; t += n_clusters) {
+      int64_t mb, nb;
+      tile_coords(t, m_blocks, n_blocks, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t row0 = mb * 2 * BM + rank * BM + quarter * 32;
+#pragma unroll 1
+      for (int chunk = 0; chunk < BN / 64; ++chunk) {
+        uint32_t v0[32], v1[32];
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                               static_cast<uint32_t>(acc * BN + chunk * 64);
+        tmem_ld32(taddr, v0);
+        tmem_ld32(taddr + 32, v1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint8_t* sbuf = stg[buf];
+        const int r = lane;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t* src = j < 4 ? &v0[8 * j] : &v1[8 * (j - 4)];
+          uint4 q;
+          q.x = pack_bf16(src[0], src[1]);
+          q.y = pack_bf16(src[2], src[3]);
+          q.z = pack_bf16(src[4], src[5]);
+          q.w = pack_bf16(src[6], src[7]);
+          *reinterpret_cast<uint4*>(sbuf + r * 128 + ((j ^ (r & 7)) * 16)) = q;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && row0 < M) {
+          tma_store_2d(&map_c, sbuf, static_cast<int32_t>(nb * BN + chunk * 64),
+                       static_cast<int32_t>(row0));
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        buf ^= 1;
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+      if (++acc == kAccStages) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+}
+
 // ------------------------------------------------------------------ host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -400,13 +613,30 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
   std::call_once(once, [] {
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBytes2)));
   });
+  static const int mode = [] {  // OPF_GEMM=1sm|2sm|auto
+    const char* e = std::getenv("OPF_GEMM");
+    if (e && std::string(e) == "1sm") return 1;
+    if (e && std::string(e) == "2sm") return 2;
+    return 0;
+  }();
+  const bool pair = mode == 2 || (mode == 0 && g.m > BM);
   const CUtensorMap ma = make_map(g.a, g.k, g.m, g.lda, BK, BM);
-  const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN);
   const CUtensorMap mc = make_map(g.c, g.n, g.m, g.ldc, 64, 32);
-  const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN);
   int grid = num_sms();
   if (g.max_ctas > 0 && g.max_ctas < grid) grid = g.max_ctas;
+  if (pair) {
+    const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN / 2);
+    const int64_t tiles = ((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n + BN - 1) / BN);
+    int clusters = grid / 2;
+    if (tiles < clusters) clusters = static_cast<int>(tiles);
+    gemm_tc2_kernel<<<2 * std::max(clusters, 1), kThreads, kSmemBytes2, s>>>(ma, mb, mc, g.m, g.n, g.k);
+    return;
+  }
+  const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN);
+  const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN);
   if (tiles < grid) grid = static_cast<int>(tiles);
   gemm_tc_kernel<<<grid, kThreads, kSmemBytes, s>>>(ma, mb, mc, g.m, g.n, g.k);
 }
