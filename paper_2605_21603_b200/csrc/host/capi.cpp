@@ -78,6 +78,7 @@ SessionConfig parse_config(const char* text) {
   if (const json::Value* x = v.get("cuda_graph")) c.cuda_graph = x->b;
   if (const json::Value* x = v.get("device")) c.device = static_cast<int>(x->as_i64());
   if (const json::Value* x = v.get("gemm_sm_budget")) c.gemm_sm_budget = static_cast<int>(x->as_i64());
+  if (const json::Value* x = v.get("fuse")) c.fuse = x->b;
   require(c.lanes >= 1 && c.lanes <= 16, Errc::ConfigError, "lanes must be in [1,16]");
   return c;
 }

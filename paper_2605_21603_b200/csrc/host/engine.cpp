@@ -97,6 +97,7 @@ Session::Session(const Graph& g, const PartitionPlan& p, SessionConfig cfg, opf_
   lanes_.assign(std::max(1, cfg_.lanes), nullptr);
   ext_.assign(g_.tensors.size(), opf_view{});
   prepacked_.assign(g_.tensors.size(), nullptr);
+  prepacked_act_.assign(g_.tensors.size(), nullptr);
   if (cfg_.device < 0) return;  // dry session
   OPF_CUDA(cudaSetDevice(cfg_.device));
   for (auto& s : lanes_) OPF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -118,6 +119,8 @@ Session::~Session() {
   for (auto& s : lanes_) cudaStreamDestroy(s);
   for (auto& e : events_) cudaEventDestroy(e);
   for (void* p : prepacked_)
+    if (p) cudaFree(p);
+  for (void* p : prepacked_act_)
     if (p) cudaFree(p);
   for (auto& kv : perms_) cudaFree(kv.second);
   if (arena_) cudaFree(arena_);
@@ -142,10 +145,11 @@ void Session::bind(const std::string& name, const opf_view& v) {
   if (changed) {
     if (m.role == TensorRole::kWeight) {
       prepack_dirty_ = true;
-      if (prepacked_[t]) {
-        cudaFree(prepacked_[t]);
-        prepacked_[t] = nullptr;
-      }
+      for (std::vector<void*>* v : {&prepacked_, &prepacked_act_})
+        if ((*v)[t]) {
+          cudaFree((*v)[t]);
+          (*v)[t] = nullptr;
+        }
     }
     // captured graphs embed pointers: drop them (plans are rebuilt lazily)
     for (auto& kv : cache_)
@@ -173,20 +177,26 @@ int64_t Session::rows() const {
   return rows == 0 ? 1 : rows;
 }
 
-void Session::ensure_prepacked(cudaStream_t s) {
-  if (!prepack_dirty_) return;
+void Session::ensure_prepacked(cudaStream_t) {}
+
+void Session::ensure_packed_for(const CompiledPlan& cp, cudaStream_t s) {
   // MatMul bf16 weights are [K,N] (reference layout); the tcgen05 GEMM wants
-  // K-major B, i.e. [N,K]: transpose once per binding.
-  for (const OperatorNode& op : g_.ops) {
-    if (op.kind != OperatorKind::kMatMul) continue;
-    const int32_t w = op.inputs[1];
-    const TensorMeta& m = g_.tensors[w];
-    if (m.dtype != Dtype::kBF16 || m.role != TensorRole::kWeight || prepacked_[w]) continue;
-    OPF_CUDA(cudaMalloc(&prepacked_[w], m.numel() * 2));
-    k_transpose_bf16(view_ptr(ext_[w]), prepacked_[w], m.shape[0], m.shape[1], s);
-  }
+  // K-major B ([N,K]), gate/up-interleaved for the SiLU-mul epilogue.  Packed
+  // once per binding, outside any capture.
+  for (const PlannedDispatch& pd : cp.dispatches)
+    for (const PlannedLaunch& l : pd.launches) {
+      if (l.prepacked < 0) continue;
+      const int32_t w = l.prepacked;
+      const TensorMeta& m = g_.tensors[w];
+      std::vector<void*>& slot = l.prepack_mode == 1 ? prepacked_act_ : prepacked_;
+      if (slot[w]) continue;
+      OPF_CUDA(cudaMalloc(&slot[w], m.numel() * 2));
+      if (l.prepack_mode == 1)
+        k_pack_gate_up(view_ptr(ext_[w]), slot[w], m.shape[0], m.shape[1] / 2, s);
+      else
+        k_transpose_bf16(view_ptr(ext_[w]), slot[w], m.shape[0], m.shape[1], s);
+    }
   OPF_CUDA(cudaGetLastError());
-  prepack_dirty_ = false;
 }
 
 void Session::warm_aux(const CompiledPlan& cp) {
@@ -459,9 +469,58 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
                   std::to_string(l.in.size()) + "->" + std::to_string(l.out.size()));
       pd.launches.push_back(std::move(l));
     } else {
+      // Epilogue fusion (per-subgraph compilation): a bf16
+      // MatMul whose output feeds only a silu_mul of the same dispatch runs as
+      // ONE tcgen05 GEMM with the SiLU-mul epilogue; its [T, 2I] output never
+      // touches HBM.
+      std::map<int32_t, int32_t> fused_act;  // matmul op -> silu_mul op
+      std::set<int32_t> skip;
+      if (cfg_.fuse) {
+        const std::set<int32_t> in_dispatch(ops.begin(), ops.end());
+        for (int32_t op : ops) {
+          const OperatorNode& node = g_.ops[op];
+          if (node.kind != OperatorKind::kMatMul) continue;
+          const TensorMeta& w = g_.tensors[node.inputs[1]];
+          const int32_t t = node.outputs[0];
+          const auto& cons = g_.tensors[t].consumers;
+          if (w.dtype != Dtype::kBF16 || w.role != TensorRole::kWeight || w.shape[1] % 256 != 0 ||
+              cons.size() != 1 || !in_dispatch.count(cons[0]) || g_.is_output(t) ||
+              std::find(b_out.begin(), b_out.end(), t) != b_out.end())
+            continue;
+          const OperatorNode& act = g_.ops[cons[0]];
+          if (act.kind != OperatorKind::kCustom || act.attrs.custom_name != "silu_mul") continue;
+          fused_act[op] = cons[0];
+          skip.insert(cons[0]);
+        }
+      }
       // internal tensors of the subgraph get scratch blocks for this dispatch
       for (int32_t op : ops) {
+        if (skip.count(op)) continue;
         const OperatorNode& node = g_.ops[op];
+        auto fa = fused_act.find(op);
+        if (fa != fused_act.end()) {
+          const OperatorNode& act = g_.ops[fa->second];
+          const int32_t a_out = act.outputs[0];
+          if (!view_of.count(a_out)) {
+            const int32_t blk = pl.alloc(tensor_bytes_rows(g_.tensors[a_out], nrows), di);
+            scratch.push_back(blk);
+            view_of[a_out] = arena_view(blk, a_out, 0, nrows);
+          }
+          PlannedLaunch l;
+          l.op = op;
+          l.kind = OperatorKind::kMatMul;
+          l.attrs = node.attrs;
+          l.attrs.params["epi"] = 1.0;
+          l.name = node.name + "+" + act.name;
+          l.rows = nrows;
+          l.in.push_back(view_of.at(node.inputs[0]));
+          l.in.push_back(weight_view(node.inputs[1], node));
+          l.out.push_back(view_of.at(a_out));
+          l.prepacked = node.inputs[1];
+          l.prepack_mode = 1;
+          pd.launches.push_back(std::move(l));
+          continue;
+        }
         for (int32_t t : node.outputs)
           if (!view_of.count(t)) {
             const int32_t blk = pl.alloc(tensor_bytes_rows(g_.tensors[t], nrows), di);
@@ -612,7 +671,7 @@ void Session::launch_one(const PlannedLaunch& l, cudaStream_t s) {
   c.param_values = pv.data();
   c.max_ctas = l.max_ctas;
   c.comm = comm_;
-  c.aux = l.prepacked >= 0 ? prepacked_[l.prepacked] : l.aux;
+  c.aux = l.prepacked >= 0 ? (l.prepack_mode == 1 ? prepacked_act_ : prepacked_)[l.prepacked] : l.aux;
   if (l.kind == OperatorKind::kAllToAll && l.fn.empty())
     c.aux = alltoall_perm_device(l.attrs.seed, view_row_elems(iv[0]));
   c.workspace = l.ws_off >= 0 ? static_cast<char*>(arena_) + l.ws_off : nullptr;
@@ -687,7 +746,7 @@ void Session::run(Scheduler& strat, const std::string& key_in, cudaStream_t stre
   require(!dry_, Errc::EngineStopped, "dry session cannot execute");
   CompiledPlan* cp = lookup_or_build(strat, key_in);
   last_ = cp;
-  ensure_prepacked(stream);
+  ensure_packed_for(*cp, stream);
   ensure_arena(cp->arena_bytes);
   warm_aux(*cp);
   if (!cfg_.cuda_graph) {

@@ -109,9 +109,12 @@ opf_status launch_kind(const opf_op_ctx& c, const opf_view* in, int n_in, opf_vi
       case OperatorKind::kMatMul: {
         if (n_in != 2) return op_error(Errc::ShapeMismatch, "MatMul takes 2 inputs");
         const int64_t K = in[0].shape[1];
-        const int64_t N = out[0].shape[1];
+        const int epi = static_cast<int>(ctx_param(c, "epi", 0.0));  // 1: fused SiLU-mul
+        const int64_t N = out[0].shape[1] * (epi == 1 ? 2 : 1);
         if (in[1].shape[0] != K || in[1].shape[1] != N)
           return op_error(Errc::ShapeMismatch, "MatMul weight must be [K,N]");
+        if (epi == 1 && (dt != Dtype::kBF16 || !c.aux))
+          return op_error(Errc::ShapeMismatch, "SiLU-mul epilogue needs the packed bf16 weight");
         if (dt == Dtype::kBF16) {
           GemmArgs g{};
           g.a = view_ptr(in[0]);
@@ -120,8 +123,9 @@ opf_status launch_kind(const opf_op_ctx& c, const opf_view* in, int n_in, opf_vi
           g.n = N;
           g.k = K;
           g.lda = K;
-          g.ldc = N;
+          g.ldc = out[0].shape[1];
           g.max_ctas = c.max_ctas;
+          g.epi = epi;
           if (c.aux) {  // pre-packed [N,K] weight -> tcgen05 path
             g.bt = c.aux;
             gemm_bf16_tc(g, s);

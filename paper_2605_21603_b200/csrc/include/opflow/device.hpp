@@ -119,8 +119,10 @@ struct GemmArgs {
   int64_t m, n, k, lda, ldc;
   int max_ctas;    // 0 = all SMs
   bool b_kn;       // simt path only: B given as [K,N] row-major instead of [N,K]
+  int epi;         // 0 plain; 1 SiLU-mul (Bt packed by k_pack_gate_up, C is [M, N/2])
 };
 void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s);
+void k_pack_gate_up(const void* src, void* dst, int64_t K, int64_t I, cudaStream_t s);
 // Reference CUDA-core GEMM (bf16 in, fp32 accumulate) used by tests as a
 // numerics cross-check of the tcgen05 path.
 void gemm_bf16_simt(const GemmArgs& g, cudaStream_t s);

@@ -137,6 +137,7 @@ struct SessionConfig {
   int lanes = 3;
   bool prealloc = true;       // Algorithm-1 zero-copy merge buffers; false = copying fallback
   bool cuda_graph = true;     // capture + replay; false = eager launches every run
+  bool fuse = true;           // GEMM epilogue fusion (MatMul -> silu_mul) inside a dispatch
   int device = 0;
   int gemm_sm_budget = 0;     // max CTAs for tensor-core GEMMs on lane 0 when overlapping
 };
@@ -162,6 +163,7 @@ struct PlannedLaunch {
   int64_t ws_off = -1, ws_bytes = 0;  // arena workspace
   const void* aux = nullptr;
   int32_t prepacked = -1;        // MatMul bf16: weight tensor whose [N,K] copy is aux
+  int prepack_mode = 0;          // 0 transposed, 1 gate/up interleaved (SiLU-mul epilogue)
   bool is_copy = false;          // concat fallback copy
   int max_ctas = 0;
 };
@@ -227,6 +229,8 @@ class Session {
   std::vector<cudaStream_t> lanes_;
   std::vector<opf_view> ext_;        // per tensor: bound external view (base == nullptr if unbound)
   std::vector<void*> prepacked_;     // per weight tensor: transposed bf16 copy for MatMul
+  std::vector<void*> prepacked_act_; // per weight tensor: gate/up interleaved copy (SiLU epilogue)
+  void ensure_packed_for(const CompiledPlan& cp, cudaStream_t s);
   bool prepack_dirty_ = true;
   void* arena_ = nullptr;
   int64_t arena_bytes_ = 0;

@@ -186,6 +186,63 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t m_blocks, int64_t
   nb = r / gm;
 }
 
+// Epilogue of one accumulator tile for one warp (32 rows): TMEM -> registers
+// -> (epilogue math) -> bf16 -> 128B-swizzled smem staging -> TMA store.
+//   EPI 0: plain, 256 output columns at nb*256.
+//   EPI 1: SiLU-mul, the weight was packed so tile columns [0,128) are gate and
+//          [128,256) the matching up columns; 128 outputs at nb*128.
+template <int EPI>
+__device__ __forceinline__ void store_tile(const CUtensorMap* map_c, uint32_t tmem_col0,
+                                           uint8_t* const (&stg)[2], int& buf, int lane, int64_t nb,
+                                           int64_t row0, int64_t M) {
+  constexpr int kChunks = EPI == 1 ? 2 : BN / 64;
+#pragma unroll 1
+  for (int chunk = 0; chunk < kChunks; ++chunk) {
+    uint32_t v0[32], v1[32];
+    const uint32_t taddr = tmem_col0 + static_cast<uint32_t>(chunk * 64);
+    tmem_ld32(taddr, v0);
+    tmem_ld32(taddr + 32, v1);
+    if constexpr (EPI == 1) {
+      uint32_t u0[32], u1[32];
+      tmem_ld32(taddr + 128, u0);
+      tmem_ld32(taddr + 160, u1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float g0 = __uint_as_float(v0[i]), g1 = __uint_as_float(v1[i]);
+        v0[i] = __float_as_uint(g0 / (1.0f + __expf(-g0)) * __uint_as_float(u0[i]));
+        v1[i] = __float_as_uint(g1 / (1.0f + __expf(-g1)) * __uint_as_float(u1[i]));
+      }
+    } else {
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    }
+    // staging buffer reuse: the TMA store issued two chunks ago must have read it
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+    uint8_t* sbuf = stg[buf];
+    const int r = lane;  // accumulator row within this warp's 32
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // 16-byte chunk j = columns 8j..8j+7
+      const uint32_t* src = j < 4 ? &v0[8 * j] : &v1[8 * (j - 4)];
+      uint4 q;
+      q.x = pack_bf16(src[0], src[1]);
+      q.y = pack_bf16(src[2], src[3]);
+      q.z = pack_bf16(src[4], src[5]);
+      q.w = pack_bf16(src[6], src[7]);
+      *reinterpret_cast<uint4*>(sbuf + r * 128 + ((j ^ (r & 7)) * 16)) = q;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0 && row0 < M) {
+      const int64_t col = EPI == 1 ? nb * (BN / 2) + chunk * 64 : nb * BN + chunk * 64;
+      tma_store_2d(map_c, sbuf, static_cast<int32_t>(col), static_cast<int32_t>(row0));
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    buf ^= 1;
+  }
+}
+
+template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K) {
@@ -296,38 +353,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t row0 = mb * BM + quarter * 32;
-#pragma unroll 1
-      for (int chunk = 0; chunk < BN / 64; ++chunk) {
-        uint32_t v0[32], v1[32];
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                               static_cast<uint32_t>(acc * BN + chunk * 64);
-        tmem_ld32(taddr, v0);
-        tmem_ld32(taddr + 32, v1);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        // staging buffer reuse: the TMA store issued two chunks ago must have read it
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        __syncwarp();
-        uint8_t* sbuf = stg[buf];
-        const int r = lane;  // accumulator row within this warp's 32
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {  // 16-byte chunk j = columns 8j..8j+7
-          const uint32_t* src = j < 4 ? &v0[8 * j] : &v1[8 * (j - 4)];
-          uint4 q;
-          q.x = pack_bf16(src[0], src[1]);
-          q.y = pack_bf16(src[2], src[3]);
-          q.z = pack_bf16(src[4], src[5]);
-          q.w = pack_bf16(src[6], src[7]);
-          *reinterpret_cast<uint4*>(sbuf + r * 128 + ((j ^ (r & 7)) * 16)) = q;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0 && row0 < M) {
-          tma_store_2d(&map_c, sbuf, static_cast<int32_t>(nb * BN + chunk * 64),
-                       static_cast<int32_t>(row0));
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        buf ^= 1;
-      }
+      store_tile<EPI>(&map_c,
+                      tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                          static_cast<uint32_t>(acc * BN),
+                      stg, buf, lane, nb, row0, M);
       // accumulator fully read: hand it back to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -397,6 +426,7 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
                : "memory");
 }
 
+template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K) {
@@ -511,37 +541,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t row0 = mb * 2 * BM + rank * BM + quarter * 32;
-#pragma unroll 1
-      for (int chunk = 0; chunk < BN / 64; ++chunk) {
-        uint32_t v0[32], v1[32];
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                               static_cast<uint32_t>(acc * BN + chunk * 64);
-        tmem_ld32(taddr, v0);
-        tmem_ld32(taddr + 32, v1);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        __syncwarp();
-        uint8_t* sbuf = stg[buf];
-        const int r = lane;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t* src = j < 4 ? &v0[8 * j] : &v1[8 * (j - 4)];
-          uint4 q;
-          q.x = pack_bf16(src[0], src[1]);
-          q.y = pack_bf16(src[2], src[3]);
-          q.z = pack_bf16(src[4], src[5]);
-          q.w = pack_bf16(src[6], src[7]);
-          *reinterpret_cast<uint4*>(sbuf + r * 128 + ((j ^ (r & 7)) * 16)) = q;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0 && row0 < M) {
-          tma_store_2d(&map_c, sbuf, static_cast<int32_t>(nb * BN + chunk * 64),
-                       static_cast<int32_t>(row0));
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        buf ^= 1;
-      }
+      store_tile<EPI>(&map_c,
+                      tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                          static_cast<uint32_t>(acc * BN),
+                      stg, buf, lane, nb, row0, M);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(&tempty[acc]);
@@ -609,11 +612,17 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
   require((reinterpret_cast<uintptr_t>(g.a) | reinterpret_cast<uintptr_t>(g.bt) |
            reinterpret_cast<uintptr_t>(g.c)) % 16 == 0,
           Errc::ShapeMismatch, "tcgen05 GEMM needs 16-byte aligned base pointers");
+  require(g.epi == 0 || g.n % BN == 0, Errc::ShapeMismatch,
+          "SiLU-mul epilogue needs N (= 2 x inter) to be a multiple of 256");
   static std::once_flag once;
   std::call_once(once, [] {
-    OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemBytes)));
-    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBytes2)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemBytes2)));
   });
   static const int mode = [] {  // OPF_GEMM=1sm|2sm|auto
@@ -623,8 +632,9 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     return 0;
   }();
   const bool pair = mode == 2 || (mode == 0 && g.m > BM);
+  const int64_t n_out = g.epi == 1 ? g.n / 2 : g.n;
   const CUtensorMap ma = make_map(g.a, g.k, g.m, g.lda, BK, BM);
-  const CUtensorMap mc = make_map(g.c, g.n, g.m, g.ldc, 64, 32);
+  const CUtensorMap mc = make_map(g.c, n_out, g.m, g.ldc, 64, 32);
   int grid = num_sms();
   if (g.max_ctas > 0 && g.max_ctas < grid) grid = g.max_ctas;
   if (pair) {
@@ -632,13 +642,49 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     const int64_t tiles = ((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n + BN - 1) / BN);
     int clusters = grid / 2;
     if (tiles < clusters) clusters = static_cast<int>(tiles);
-    gemm_tc2_kernel<<<2 * std::max(clusters, 1), kThreads, kSmemBytes2, s>>>(ma, mb, mc, g.m, g.n, g.k);
+    const unsigned blocks = 2u * static_cast<unsigned>(std::max(clusters, 1));
+    if (g.epi == 1)
+      gemm_tc2_kernel<1><<<blocks, kThreads, kSmemBytes2, s>>>(ma, mb, mc, g.m, g.n, g.k);
+    else
+      gemm_tc2_kernel<0><<<blocks, kThreads, kSmemBytes2, s>>>(ma, mb, mc, g.m, g.n, g.k);
     return;
   }
   const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN);
   const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN);
   if (tiles < grid) grid = static_cast<int>(tiles);
-  gemm_tc_kernel<<<grid, kThreads, kSmemBytes, s>>>(ma, mb, mc, g.m, g.n, g.k);
+  if (g.epi == 1)
+    gemm_tc_kernel<1><<<grid, kThreads, kSmemBytes, s>>>(ma, mb, mc, g.m, g.n, g.k);
+  else
+    gemm_tc_kernel<0><<<grid, kThreads, kSmemBytes, s>>>(ma, mb, mc, g.m, g.n, g.k);
+}
+
+// [K, 2I] gate|up weight -> K-major [2I, K] with gate/up interleaved in 128-row
+// blocks (rows 256b..256b+127 = gate block b, +128..+255 = up block b), the
+// layout the SiLU-mul epilogue consumes.
+__global__ void pack_gate_up_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                    int64_t K, int64_t I) {
+  __shared__ __nv_bfloat16 tile[32][33];
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32, r0 = static_cast<int64_t>(blockIdx.y) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < K && c < 2 * I) tile[i][threadIdx.x] = src[r * 2 * I + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;  // source column c -> packed row
+    if (r < K && c < 2 * I) {
+      const bool up = c >= I;
+      const int64_t j = up ? c - I : c;
+      const int64_t prow = (j / 128) * 256 + (up ? 128 : 0) + j % 128;
+      dst[prow * K + r] = tile[threadIdx.x][i];
+    }
+  }
+}
+
+void k_pack_gate_up(const void* src, void* dst, int64_t K, int64_t I, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((2 * I + 31) / 32), static_cast<unsigned>((K + 31) / 32));
+  pack_gate_up_kernel<<<grid, dim3(32, 8), 0, s>>>(static_cast<const __nv_bfloat16*>(src),
+                                                   static_cast<__nv_bfloat16*>(dst), K, I);
 }
 
 }  // namespace opflow
