@@ -53,6 +53,9 @@ def parse():
     p.add_argument("--strategies", default="auto")
     p.add_argument("--cpu-seconds", type=float, default=20.0)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-decode", action="store_true")
+    p.add_argument("--decode-batch", type=int, default=512)
+    p.add_argument("--decode-ctx", type=int, default=4096)
     return p.parse_args()
 
 
@@ -277,6 +280,12 @@ def run_ours(args):
     achieved, gemm_rows = gemm_roofline(of, torch, dev, shapes) if rank == 0 else (0.0, [])
     flops_layer = sum(2.0 * m * k * n for (m, k, n) in shapes.values())
     line = None
+    decode = None
+    if not args.no_decode:
+        del sess, bufs
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        decode = run_decode(of, torch, dev, args, tp, comm, rank, world, stream)
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(args, T, S, tp)
         line = {
@@ -306,6 +315,7 @@ def run_ours(args):
                          "gemm_share_of_step_at_roofline": round(
                              flops_layer * L / (PEAKS["bf16_tflops"] * 1e12) * 1e3 / best_ms, 4)},
             "cpu_baseline": cpu,
+            "decode": decode,
             "clocks": clk.summary(),
             "gpu_launches": int(launches) * args.steps,
             "plan": {"dispatches": stats["last"]["dispatches"], "launches_per_step": launches,
@@ -314,6 +324,86 @@ def run_ours(args):
         }
         print(json.dumps(line), flush=True)
     barrier(world)
+
+
+def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
+    """BASELINE configs[3]: Llama-3-8B-shaped decode, batch 512 x 4K context,
+    nano-batch split GEMM || paged decode attention vs sequential.  The 32
+    layers' KV pools alias one 8.6 GB (TP=1) pool — the full 275 GB KV does not
+    fit one GPU (SURVEY §7 hard part 5); every layer still streams its whole
+    KV from HBM (8.6 GB >> 126 MB L2)."""
+    B, ctx, page, L = args.decode_batch, args.decode_ctx, 16, args.layers
+    desc = of.llama_decode_graph(layers=L, tokens=B, ctx_len=ctx, page_size=page, tp=tp, dtype="bf16",
+                                 **LLAMA)
+    g = of.build_graph(desc)
+    rules = [of.PartitionRule.by_func("AllReduce"), of.PartitionRule.by_func("add_rmsnorm")] if tp > 1 else []
+    sess = of.Session(g, of.partition(g, rules), {"lanes": 3, "device": dev.index}, comm)
+    gen = torch.Generator(device=dev).manual_seed(99 + rank)
+    keep = {}
+    nkv, hd = LLAMA["kv_heads"] // tp, LLAMA["head_dim"]
+    max_pages = (ctx + page - 1) // page
+    pages = B * max_pages
+    kc = ((torch.rand(pages, page, nkv, hd, device=dev, generator=gen) * 2 - 1)).to(torch.bfloat16)
+    vc = ((torch.rand(pages, page, nkv, hd, device=dev, generator=gen) * 2 - 1)).to(torch.bfloat16)
+    for t in g.description["tensors"]:
+        name, shape = t["name"], t["shape"]
+        if t["role"] not in ("input", "weight", "output"):
+            continue
+        if name.endswith("k_cache"):
+            x = kc
+        elif name.endswith("v_cache"):
+            x = vc
+        elif name == "positions":
+            x = torch.full((B,), ctx - 1, dtype=torch.int64, device=dev)
+        elif name == "block_table":
+            x = torch.randperm(pages, device=dev, generator=gen).view(B, max_pages).to(torch.int64)
+        elif t["role"] == "output":
+            x = torch.empty(shape, dtype=torch.bfloat16, device=dev)
+        elif name.endswith("norm.w"):
+            x = (1.0 + 0.1 * (torch.rand(shape, device=dev, generator=gen) - 0.5)).to(torch.bfloat16)
+        elif t["role"] == "weight":
+            x = ((torch.rand(shape, device=dev, generator=gen) * 2 - 1) / shape[0] ** 0.5).to(torch.bfloat16)
+        else:
+            x = (torch.rand(shape, device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
+        keep[name] = x
+        sess.bind(name, x)
+    cands = {"sequential": {"name": "sequential"},
+             "nanoflow_u2": {"name": "split_overlap", "n_microbatches": 2, "lane_mode": "ubatch"},
+             "nanoflow_class": {"name": "split_overlap", "n_microbatches": 2}}
+    res = {k: time_steps(torch, lambda s=s: sess.run(s, stream), args.steps, args.warmup, stream, world)
+           for k, s in cands.items()}
+    best = min((k for k in res if k != "sequential"), key=lambda k: res[k])
+    # attention kernel alone: CUDA events around back-to-back launches on `stream`
+    op = {"name": "a", "kind": "Custom", "inputs": [], "outputs": [],
+          "attrs": {"custom_name": "attn_decode",
+                    "params": {"heads": LLAMA["heads"] // tp, "kv_heads": nkv, "head_dim": hd,
+                               "page_size": page}}}
+    qkv = torch.randn(B, (LLAMA["heads"] // tp + 2 * nkv) * hd, device=dev).to(torch.bfloat16)
+    out = torch.empty(B, LLAMA["heads"] // tp * hd, device=dev, dtype=torch.bfloat16)
+    ins = [qkv, kc, vc, keep["block_table"], keep["positions"]]
+    for _ in range(3):
+        of.launch(op, ins, [out], B, stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    e0.record(stream)
+    for _ in range(reps):
+        of.launch(op, ins, [out], B, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    attn_ms = e0.elapsed_time(e1) / reps
+    kv_bytes = 2.0 * B * ctx * nkv * hd * 2
+    achieved = kv_bytes / (attn_ms / 1e3) / 1e9
+    del sess
+    return {"workload": f"llama3-8b-shaped decode, {L} layers, batch {B} x ctx {ctx}, paged KV "
+                        f"(page {page}, random block table), TP={tp}",
+            "tokens_per_s": round(B / (res[best] / 1e3), 1), "strategy": best,
+            "sequential_tokens_per_s": round(B / (res["sequential"] / 1e3), 1),
+            "speedup_vs_sequential": round(res["sequential"] / res[best], 4),
+            "strategies_ms": {k: round(v, 3) for k, v in res.items()},
+            "roofline": {"bound": "hbm", "kernel": "decode_bf16_kernel (paged attention)",
+                         "achieved": round(achieved, 1), "peak": PEAKS["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(achieved / PEAKS["hbm_gbs"], 4), "ms_per_launch": round(attn_ms, 4),
+                         "algorithmic_bytes_per_launch": kv_bytes}}
 
 
 # ------------------------------------------------------------------ reference (CPU)
