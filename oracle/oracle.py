@@ -256,8 +256,12 @@ def topo_order(desc: dict) -> List[int]:
 
 
 def evaluate(desc_json: str, rows: int, bindings: Dict[str, np.ndarray],
-             exact: bool = True) -> Dict[str, np.ndarray]:
-    """eval_reference restated; bf16 graphs evaluate in fp32 (oracle precision)."""
+             exact: bool = True, allreduce=None) -> Dict[str, np.ndarray]:
+    """eval_reference restated; bf16 graphs evaluate in fp32 (oracle precision).
+
+    `allreduce(x, world_size)` overrides the reference's single-process
+    AllReduce stand-in (x * world_size, eval.cpp:63-70) with a real collective
+    (used by the tensor-parallel host tests)."""
     desc = json.loads(desc_json) if isinstance(desc_json, str) else desc_json
     tmeta = {t["name"]: t for t in desc["tensors"]}
     vals: Dict[str, np.ndarray] = {}
@@ -281,7 +285,8 @@ def evaluate(desc_json: str, rows: int, bindings: Dict[str, np.ndarray],
         elif k == "RowScale":
             r = [row_scale(x[0])]
         elif k == "AllReduce":
-            r = [scale(x[0], a.get("world_size", 1))]
+            r = [allreduce(x[0], a.get("world_size", 1)) if allreduce else
+                 scale(x[0], a.get("world_size", 1))]
         elif k == "AllToAll":
             perm = alltoall_permutation(a.get("seed", 0), x[0].shape[1])
             r = [x[0][:, perm]]

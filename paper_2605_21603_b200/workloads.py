@@ -100,3 +100,34 @@ def standin_inputs(desc_json, rows: int, seed: int = 0) -> Dict[str, np.ndarray]
         else:
             out[t["name"]] = rng.uniform(-1.0, 1.0, size=shape).astype(np.float32)
     return out
+
+
+def shard_llama_weights(full: Dict[str, np.ndarray], rank: int, world: int, heads: int,
+                        kv_heads: int, head_dim: int, inter: int) -> Dict[str, np.ndarray]:
+    """Megatron-style tensor-parallel shard of tp=1 Llama weights for `rank`:
+    QKV and gate_up column-parallel (this rank's q / k / v heads, gate / up
+    columns), O and down row-parallel; norms replicated.  The per-rank graph is
+    llama_graph(tp=world): the partial O / down outputs are summed by the
+    AllReduce the builder inserts."""
+    nq, nkv, I = heads // world, kv_heads // world, inter // world
+    hd = head_dim
+    out = {}
+    for name, w in full.items():
+        if name.endswith(".qkv.w"):
+            q = w[:, rank * nq * hd:(rank + 1) * nq * hd]
+            k0 = heads * hd
+            k = w[:, k0 + rank * nkv * hd:k0 + (rank + 1) * nkv * hd]
+            v0 = (heads + kv_heads) * hd
+            v = w[:, v0 + rank * nkv * hd:v0 + (rank + 1) * nkv * hd]
+            out[name] = np.ascontiguousarray(np.concatenate([q, k, v], axis=1))
+        elif name.endswith(".o.w"):
+            out[name] = np.ascontiguousarray(w[rank * nq * hd:(rank + 1) * nq * hd])
+        elif name.endswith(".gate_up.w"):
+            g = w[:, rank * I:(rank + 1) * I]
+            u = w[:, inter + rank * I:inter + (rank + 1) * I]
+            out[name] = np.ascontiguousarray(np.concatenate([g, u], axis=1))
+        elif name.endswith(".down.w"):
+            out[name] = np.ascontiguousarray(w[rank * I:(rank + 1) * I])
+        else:
+            out[name] = w
+    return out
