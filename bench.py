@@ -370,6 +370,11 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
     cands = {"sequential": {"name": "sequential"},
              "nanoflow_u2": {"name": "split_overlap", "n_microbatches": 2, "lane_mode": "ubatch"},
              "nanoflow_class": {"name": "split_overlap", "n_microbatches": 2}}
+    # NanoFlow SM partitioning: GEMMs (compute lane 0) on G SMs, paged attention
+    # and the memory-bound ops (lane 1) on the remaining SMs, concurrently.
+    for gsm in (24, 40, 56):
+        cands[f"nanoflow_class_sm{gsm}"] = {"name": "split_overlap", "n_microbatches": 2,
+                                            "lane_sm_budget": [gsm, 148 - gsm, 0]}
     res = {k: time_steps(torch, lambda s=s: sess.run(s, stream), args.steps, args.warmup, stream, world)
            for k, s in cands.items()}
     best = min((k for k in res if k != "sequential"), key=lambda k: res[k])

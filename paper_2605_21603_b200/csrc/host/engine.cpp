@@ -216,7 +216,9 @@ void Session::ensure_arena(int64_t bytes) {
   arena_bytes_ = bytes;
 }
 
-std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const std::string& key) {
+std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const std::string& key,
+                                               const std::vector<int>& budgets_in) {
+  const std::vector<int>& budgets = budgets_in.empty() ? cfg_.lane_sm_budget : budgets_in;
   auto cp = std::make_unique<CompiledPlan>();
   cp->key = key;
   const auto& ds = ctx.dispatches();
@@ -551,6 +553,7 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
     for (PlannedLaunch& l : pd.launches) {
       if (l.is_copy) continue;
       if (cfg_.gemm_sm_budget > 0 && d.lane == 0) l.max_ctas = cfg_.gemm_sm_budget;
+      if (d.lane < static_cast<int>(budgets.size()) && budgets[d.lane] > 0) l.max_ctas = budgets[d.lane];
       opf_op_ctx c{};
       c.kind = static_cast<int32_t>(l.kind);
       c.world_size = l.attrs.world_size;
@@ -732,7 +735,7 @@ CompiledPlan* Session::lookup_or_build(Scheduler& strat, const std::string& key_
   SchedContext ctx(g_, p_, r, static_cast<int>(lanes_.size()));
   strat.schedule(ctx);
   ctx.finish();
-  auto built = compile(ctx, key);
+  auto built = compile(ctx, key, strat.lane_budgets());
   CompiledPlan* cp = built.get();
   cache_[key] = std::move(built);
   return cp;

@@ -227,6 +227,7 @@ struct StrategyParams {
   int32_t lane_of[kNumResourceClasses] = {0, 1, 2};
   std::string replace_fn;         // fuse_norm_comm replacement name ("" = auto)
   std::vector<std::string> merged_labels = {"*.attn"};  // dbo: executed merged
+  std::vector<int> lane_budget;   // per-lane SM budgets
   std::string raw;
 };
 
@@ -256,6 +257,8 @@ StrategyParams parse_spec(const std::string& text) {
     if (const json::Value* c = x->get("network")) p.lane_of[2] = static_cast<int32_t>(c->as_i64());
   }
   if (const json::Value* x = v.get("replace_fn")) p.replace_fn = x->str();
+  if (const json::Value* x = v.get("lane_sm_budget"))
+    for (const json::Value& e : x->arr()) p.lane_budget.push_back(static_cast<int>(e.as_i64()));
   if (const json::Value* x = v.get("merged")) {
     p.merged_labels.clear();
     for (const json::Value& e : x->arr()) p.merged_labels.push_back(e.str());
@@ -296,6 +299,7 @@ int32_t lane_for(const StrategyParams& p, SchedContext& ctx, int32_t s, int32_t 
 class Sequential final : public Scheduler {
  public:
   explicit Sequential(StrategyParams p) : p_(std::move(p)) {}
+  std::vector<int> lane_budgets() const override { return p_.lane_budget; }
   void schedule(SchedContext& ctx) override { run_sequential(ctx); }
   std::string key() const override { return "sequential"; }
 
@@ -308,6 +312,7 @@ class Sequential final : public Scheduler {
 class SplitOverlap final : public Scheduler {
  public:
   explicit SplitOverlap(StrategyParams p) : p_(std::move(p)) {}
+  std::vector<int> lane_budgets() const override { return p_.lane_budget; }
   std::string key() const override { return p_.raw; }
   void schedule(SchedContext& ctx) override {
     if (ctx.rows() < p_.threshold || p_.n_ub == 1 || ctx.rows() < 2 * p_.align) {
@@ -339,6 +344,7 @@ class SplitOverlap final : public Scheduler {
 class Dbo final : public Scheduler {
  public:
   explicit Dbo(StrategyParams p) : p_(std::move(p)) {}
+  std::vector<int> lane_budgets() const override { return p_.lane_budget; }
   std::string key() const override { return p_.raw; }
   void schedule(SchedContext& ctx) override {
     const PartitionPlan& plan = ctx.plan();
@@ -393,6 +399,7 @@ class Dbo final : public Scheduler {
 class FuseNormComm final : public Scheduler {
  public:
   explicit FuseNormComm(StrategyParams p) : p_(std::move(p)) {}
+  std::vector<int> lane_budgets() const override { return p_.lane_budget; }
   std::string key() const override { return p_.raw; }
   void schedule(SchedContext& ctx) override {
     const Graph& g = ctx.graph();

@@ -128,6 +128,9 @@ class Scheduler {
   virtual ~Scheduler() = default;
   virtual void schedule(SchedContext& ctx) = 0;
   virtual std::string key() const = 0;  // plan-cache key component
+  // Per-lane SM budgets (max SMs a lane's GEMM / attention launches occupy;
+  // 0 = all).  NanoFlow-style SM partitioning between concurrent streams.
+  virtual std::vector<int> lane_budgets() const { return {}; }
 };
 
 std::unique_ptr<Scheduler> make_strategy(const std::string& spec_json);
@@ -140,6 +143,7 @@ struct SessionConfig {
   bool fuse = true;           // GEMM epilogue fusion (MatMul -> silu_mul) inside a dispatch
   int device = 0;
   int gemm_sm_budget = 0;     // max CTAs for tensor-core GEMMs on lane 0 when overlapping
+  std::vector<int> lane_sm_budget;  // per-lane SM budget defaults (strategy may override)
 };
 
 struct PlannedView {
@@ -214,7 +218,8 @@ class Session {
   int64_t rows() const;
 
  private:
-  std::unique_ptr<CompiledPlan> compile(const SchedContext& ctx, const std::string& key);
+  std::unique_ptr<CompiledPlan> compile(const SchedContext& ctx, const std::string& key,
+                                        const std::vector<int>& budgets);
   void ensure_arena(int64_t bytes);
   void ensure_prepacked(cudaStream_t s);
   opf_view resolve(const PlannedView& v) const;

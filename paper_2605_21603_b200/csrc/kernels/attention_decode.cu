@@ -3,9 +3,9 @@
 // cache [pages, 16, nkv, 128] bf16 with a per-sequence block table; the
 // sequence attends to its `ctx` cached tokens plus itself.
 //
-// One CTA per (sequence, kv head), 4 warps.  Warp w streams pages w, w+4, ...
+// Persistent: one CTA per SM (8 warps) walks (sequence, kv head) items; warp w streams pages w, w+8, ...
 // (16 tokens x 256 B of K and of V each) with cp.async into a 3-deep per-warp
-// ring (XOR-swizzled): 96 KB per CTA, 2 CTAs (192 KB) in flight per SM.  The GQA group is the
+// ring (XOR-swizzled): 192 KB per SM in flight.  The grid size is the SM budget.  The GQA group is the
 // MMA M dimension: S[16 x 16 tokens] = Q[16 x 128] K^T and O[16 x 128] += P V
 // are 32 mma.sync m16n8k16 per page per warp (rows >= group are zero padding),
 // i.e. ~2 tensor instructions per token instead of ~60 SIMT ones — the
@@ -24,11 +24,11 @@ namespace {
 
 constexpr int HD = 128;
 constexpr int PAGE = 16;
-constexpr int kWarps = 4;
+constexpr int kWarps = 8;
 constexpr int kDepth = 3;                  // pages in flight per warp
 constexpr int kPageBytes = PAGE * HD * 2;  // 4 KB (one tensor, one page, one kv head)
 constexpr int kWarpRing = kDepth * 2 * kPageBytes;
-constexpr int kSmemRing = kWarps * kWarpRing;  // 96 KB -> 2 CTAs per SM
+constexpr int kSmemRing = kWarps * kWarpRing;  // 192 KB -> 1 CTA per SM
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -65,10 +65,13 @@ __global__ void __launch_bounds__(kWarps * 32)
     decode_mma_kernel(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ kc,
                       const __nv_bfloat16* __restrict__ vc, const int64_t* __restrict__ table,
                       const int64_t* __restrict__ ctx_len, __nv_bfloat16* __restrict__ out, int nq,
-                      int nkv, int64_t max_pages, float scale_log2) {
+                      int nkv, int64_t max_pages, float scale_log2, int64_t n_items) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const int64_t b = blockIdx.x / nkv;
-  const int kh = static_cast<int>(blockIdx.x % nkv);
+  // persistent: a CTA (one per SM) walks (sequence, kv head) items, so the
+  // launch occupies exactly gridDim.x SMs (SM partitioning under overlap)
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+  const int64_t b = item / nkv;
+  const int kh = static_cast<int>(item % nkv);
   const int G = nq / nkv;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int g = lane >> 2, t = lane & 3;
@@ -228,22 +231,27 @@ __global__ void __launch_bounds__(kWarps * 32)
     out[b * static_cast<int64_t>(nq) * HD + static_cast<int64_t>(kh * G + h) * HD + d] =
         __float2bfloat16(A / L);
   }
+  __syncthreads();  // smem is reused by the next item's ring
+  }
 }
 
 }  // namespace
 
 bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                      const int64_t* table, const int64_t* ctx, __nv_bfloat16* out, int64_t B, int nq,
-                     int nkv, int hd, int page, int64_t max_pages, float scale, cudaStream_t s) {
+                     int nkv, int hd, int page, int64_t max_pages, float scale, int max_ctas,
+                     cudaStream_t s) {
   if (hd != HD || page != PAGE || nq % nkv != 0 || nq / nkv > 8) return false;
   static bool attr = [] {
     return cudaFuncSetAttribute(decode_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemRing) == cudaSuccess;
   }();
   if (!attr) return false;
-  const unsigned grid = static_cast<unsigned>(B * nkv);
-  decode_mma_kernel<<<grid, kWarps * 32, kSmemRing, s>>>(qkv, kc, vc, table, ctx, out, nq, nkv,
-                                                         max_pages, scale * 1.4426950408889634f);
+  const int64_t items = B * nkv;
+  int64_t grid = max_ctas > 0 ? std::min<int64_t>(max_ctas, num_sms()) : num_sms();
+  grid = std::max<int64_t>(1, std::min(grid, items));
+  decode_mma_kernel<<<static_cast<unsigned>(grid), kWarps * 32, kSmemRing, s>>>(
+      qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, scale * 1.4426950408889634f, items);
   return true;
 }
 
