@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--no-decode", action="store_true")
     p.add_argument("--decode-batch", type=int, default=512)
     p.add_argument("--decode-ctx", type=int, default=4096)
+    p.add_argument("--sm-sweep", type=int, nargs="*", default=None,
+                   help="decode: also try NanoFlow SM partitions with G SMs for the GEMM lane")
     return p.parse_args()
 
 
@@ -372,7 +374,7 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
              "nanoflow_class": {"name": "split_overlap", "n_microbatches": 2}}
     # NanoFlow SM partitioning: GEMMs (compute lane 0) on G SMs, paged attention
     # and the memory-bound ops (lane 1) on the remaining SMs, concurrently.
-    for gsm in (24, 40, 56):
+    for gsm in (args.sm_sweep or []):
         cands[f"nanoflow_class_sm{gsm}"] = {"name": "split_overlap", "n_microbatches": 2,
                                             "lane_sm_budget": [gsm, 148 - gsm, 0]}
     res = {k: time_steps(torch, lambda s=s: sess.run(s, stream), args.steps, args.warmup, stream, world)

@@ -115,6 +115,11 @@ opf_status opf_has_op(const char* name, int32_t* present);
 opf_status opf_launch(const char* op_json, const opf_view* in, int32_t n_in, opf_view* out,
                       int32_t n_out, int64_t rows, void* stream);
 opf_status opf_view_rows(const opf_view* v, int64_t row_off, int64_t nrows, opf_view* out);
+/* opf_launch with a communicator (TP collectives / fused comm ops) and an SM budget. */
+typedef struct opf_comm opf_comm;
+opf_status opf_launch_comm(const char* op_json, const opf_view* in, int32_t n_in, opf_view* out,
+                           int32_t n_out, int64_t rows, opf_comm* comm, int32_t max_ctas,
+                           void* stream);
 
 /* ---------------------------------------------------------------- comm (TP/EP) */
 typedef struct opf_comm opf_comm;
@@ -123,6 +128,14 @@ opf_status opf_comm_unique_id(uint8_t id_out[128]);
 opf_status opf_comm_init(const uint8_t id[128], int32_t world, int32_t rank, int32_t device,
                          opf_comm** out);
 void opf_comm_free(opf_comm* c);
+/* Symmetric peer window for the fused all-reduce+RMSNorm kernel: allocate my
+ * window (returns its 64-byte CUDA-IPC handle), exchange handles out of band,
+ * then open all peers' windows (handles: world x 64 bytes, rank order). */
+opf_status opf_comm_window_alloc(opf_comm* c, size_t stage_bytes, uint8_t ipc_handle_out[64]);
+opf_status opf_comm_window_open(opf_comm* c, const uint8_t* handles);
+/* `world` virtual ranks sharing one device (tests of the peer-memory protocol). */
+opf_status opf_comm_create_virtual(int32_t world, int32_t device, size_t stage_bytes, opf_comm** outs);
+opf_status opf_comm_window_error(opf_comm* c, uint32_t* err);
 
 /* ---------------------------------------------------------------- sessions */
 typedef struct opf_session opf_session;

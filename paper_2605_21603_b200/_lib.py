@@ -70,6 +70,12 @@ _SIGS = {
     "opf_comm_init": (C.c_int32, [C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32,
                                   C.POINTER(C.c_void_p)]),
     "opf_comm_free": (None, [C.c_void_p]),
+    "opf_comm_window_alloc": (C.c_int32, [C.c_void_p, C.c_size_t, C.POINTER(C.c_uint8)]),
+    "opf_comm_window_open": (C.c_int32, [C.c_void_p, C.POINTER(C.c_uint8)]),
+    "opf_comm_create_virtual": (C.c_int32, [C.c_int32, C.c_int32, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "opf_comm_window_error": (C.c_int32, [C.c_void_p, C.POINTER(C.c_uint32)]),
+    "opf_launch_comm": (C.c_int32, [C.c_char_p, C.POINTER(opf_view), C.c_int32, C.POINTER(opf_view),
+                                    C.c_int32, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p]),
     "opf_session_create": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_void_p,
                                        C.POINTER(C.c_void_p)]),
     "opf_session_free": (None, [C.c_void_p]),

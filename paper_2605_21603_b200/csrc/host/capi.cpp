@@ -246,6 +246,44 @@ opf_status opf_launch(const char* op_json, const opf_view* in, int32_t n_in, opf
   return g ? g : st;
 }
 
+opf_status opf_launch_comm(const char* op_json, const opf_view* in, int32_t n_in, opf_view* out,
+                           int32_t n_out, int64_t rows, opf_comm* comm, int32_t max_ctas,
+                           void* stream) {
+  opf_status st = 0;
+  const opf_status g = guard([&] {
+    need(op_json, "op");
+    GraphDescription d = description_from_json(std::string("{\"operators\":[") + op_json + "]}");
+    const OpDecl& od = d.operators.at(0);
+    std::vector<const char*> pn;
+    std::vector<double> pv;
+    for (const auto& kv : od.attrs.params) {
+      pn.push_back(kv.first.c_str());
+      pv.push_back(kv.second);
+    }
+    opf_op_ctx c{};
+    c.op_name = od.name.c_str();
+    c.kind = static_cast<int32_t>(od.kind);
+    c.custom_name = od.attrs.custom_name.c_str();
+    c.world_size = od.attrs.world_size;
+    c.seed = od.attrs.seed;
+    c.n_params = static_cast<int32_t>(pn.size());
+    c.param_names = pn.data();
+    c.param_values = pv.data();
+    c.comm = comm;
+    c.max_ctas = max_ctas;
+    auto s = static_cast<cudaStream_t>(stream);
+    if (od.kind == OperatorKind::kCustom) {
+      const OpEntry* e = OpRegistry::global().find(od.attrs.custom_name);
+      require(e != nullptr, Errc::ConfigError,
+              "no custom function registered for '" + od.attrs.custom_name + "'");
+      st = e->fn(&c, in, n_in, out, n_out, rows, s);
+    } else {
+      st = launch_kind(c, in, n_in, out, n_out, rows, s);
+    }
+  });
+  return g ? g : st;
+}
+
 opf_status opf_view_rows(const opf_view* v, int64_t row_off, int64_t nrows, opf_view* out) {
   return guard([&] {
     need(v, "view");
@@ -290,7 +328,50 @@ opf_status opf_comm_init(const uint8_t id[128], int32_t world, int32_t rank, int
 void opf_comm_free(opf_comm* c) {
   if (!c) return;
   if (c->nccl) nccl().CommDestroy(c->nccl);
+  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  if (c->window_base) cudaFree(c->window_base);
   delete c;
+}
+
+opf_status opf_comm_window_alloc(opf_comm* c, size_t stage_bytes, uint8_t ipc_handle_out[64]) {
+  return guard([&] {
+    need(c, "comm");
+    comm_window_alloc(c, stage_bytes, ipc_handle_out);
+  });
+}
+
+opf_status opf_comm_window_open(opf_comm* c, const uint8_t* handles) {
+  return guard([&] {
+    need(c, "comm");
+    need(handles, "handles");
+    comm_window_open(c, handles);
+  });
+}
+
+opf_status opf_comm_create_virtual(int32_t world, int32_t device, size_t stage_bytes, opf_comm** outs) {
+  return guard([&] {
+    require(world >= 1 && world <= 8, Errc::ConfigError, "virtual world must be 1..8");
+    OPF_CUDA(cudaSetDevice(device));
+    std::vector<opf_comm*> cs;
+    for (int r = 0; r < world; ++r) {
+      auto c = std::make_unique<opf_comm>();
+      c->world = world;
+      c->rank = r;
+      c->device = device;
+      c->virtual_rank = true;
+      comm_window_alloc(c.get(), stage_bytes, nullptr);
+      cs.push_back(c.release());
+    }
+    comm_window_link_local(cs.data(), world);
+    for (int r = 0; r < world; ++r) outs[r] = cs[r];
+  });
+}
+
+opf_status opf_comm_window_error(opf_comm* c, uint32_t* err) {
+  return guard([&] {
+    need(c, "comm");
+    *err = comm_window_error(c);
+  });
 }
 
 // ------------------------------------------------------------------ sessions

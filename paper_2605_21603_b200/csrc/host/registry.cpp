@@ -9,6 +9,9 @@
 
 namespace opflow {
 
+bool allreduce_p2p(const opf_comm* c, const opf_view& in, opf_view& out, int64_t rows, int max_ctas,
+                   cudaStream_t s);
+
 namespace {
 thread_local std::string g_last_error;
 }
@@ -148,6 +151,9 @@ opf_status launch_kind(const opf_op_ctx& c, const opf_view* in, int n_in, opf_vi
         return launch_status("RowScale");
       case OperatorKind::kAllReduce: {
         const opf_comm* comm = static_cast<const opf_comm*>(c.comm);
+        if (comm && comm->world > 1 && !comm->peer_buf.empty() && comm->world == c.world_size &&
+            allreduce_p2p(comm, in[0], out[0], rows, c.max_ctas, s))
+          return launch_status("AllReduce(p2p)");
         if (comm && comm->world > 1) {
           if (comm->world != c.world_size)
             return op_error(Errc::ConfigError, "AllReduce world_size " +

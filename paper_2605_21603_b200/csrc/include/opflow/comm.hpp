@@ -10,6 +10,8 @@
 #include <cstdint>
 #include <vector>
 
+#include "opflow_b200.h"
+
 struct opf_comm {
   ncclComm_t nccl = nullptr;
   int world = 1;
@@ -22,5 +24,17 @@ struct opf_comm {
   size_t peer_bytes = 0;
   void** d_peer_buf = nullptr;      // device copy of peer_buf
   uint32_t** d_peer_flag = nullptr;
-  uint32_t epoch = 0;               // barrier generation, bumped per fused call (host side)
+  uint32_t epoch = 0;               // (unused: epochs live in device memory)
+  void* window_base = nullptr;      // my symmetric window (staging | flags | epochs)
+  size_t window_bytes = 0;
+  std::vector<void*> opened;        // IPC-opened peer windows (closed on free)
+  bool virtual_rank = false;        // one-device test rank (no NCCL)
 };
+
+namespace opflow {
+void comm_window_alloc(opf_comm* c, size_t stage_bytes, void* ipc_handle_out);
+void comm_window_open(opf_comm* c, const void* handles);
+void comm_window_link_local(opf_comm* const* comms, int world);
+uint32_t comm_window_error(const opf_comm* c);
+struct opf_view_fwd;
+}  // namespace opflow

@@ -1,0 +1,287 @@
+// Fused all-reduce + residual add + RMSNorm over peer memory (TokenWeave's
+// partial-overlap kernel, Fig. 7; north star: "a fused
+// all-reduce+RMSNorm kernel that writes to peer buffers over NVSwitch").
+//
+// Every rank owns a symmetric window (one cudaMalloc, CUDA-IPC mapped into all
+// peers): [staging rows | per-CTA signal flags | per-CTA local epochs].
+// One launch per rank, same grid on every rank; CTA b owns rows b, b+G, ...:
+//   1. copy my partial rows into my staging window;
+//   2. barrier: bump my epoch for CTA b, store it into flag[b][me] of every
+//      peer (st.release.sys over NVLink), spin until flag[b][p] >= epoch for
+//      all p (ld.acquire.sys) — pairwise per CTA, no grid-wide sync;
+//   3. reduce: sum the W partial rows by P2P loads, add the residual, write
+//      x1, normalise and write h (one pass, rows in registers/smem);
+//   4. barrier again ("done reading") so peers may overwrite their staging.
+// Epochs live in device memory and advance inside the kernel, so the launch
+// is CUDA-graph capturable and replays stay in lock-step across ranks.  The
+// spin loops are bounded: on timeout the kernel raises an error flag instead
+// of hanging the GPU.
+#include <cuda_bf16.h>
+
+#include <cstring>
+
+#include "opflow/comm.hpp"
+#include "opflow/device.hpp"
+
+namespace opflow {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxWorld = 8;
+constexpr int kMaxCtas = 1024;
+constexpr int64_t kSpinLimit = 1ll << 28;
+
+struct PeerPtrs {
+  const __nv_bfloat16* buf[kMaxWorld];  // staging rows of each rank
+  uint32_t* flags[kMaxWorld];           // flag arrays of each rank [kMaxCtas][kMaxWorld]
+};
+
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ bool cta_barrier(const PeerPtrs& pp, uint32_t* my_epoch, int world, int rank,
+                            uint32_t* err) {
+  __syncthreads();
+  __shared__ uint32_t ok;
+  if (threadIdx.x == 0) {
+    ok = 1;
+    const uint32_t e = ++my_epoch[blockIdx.x];
+    __threadfence_system();
+    for (int p = 0; p < world; ++p) st_release(pp.flags[p] + blockIdx.x * kMaxWorld + rank, e);
+    for (int p = 0; p < world; ++p) {
+      int64_t spins = 0;
+      while (ld_acquire(pp.flags[rank] + blockIdx.x * kMaxWorld + p) < e) {
+        if (++spins > kSpinLimit) {
+          atomicExch(err, 1u);
+          ok = 0;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return ok != 0;
+}
+
+__global__ void __launch_bounds__(kThreads) ar_add_rmsnorm_p2p_kernel(
+    PeerPtrs pp, int world, int rank, const __nv_bfloat16* __restrict__ partial,
+    __nv_bfloat16* __restrict__ my_stage, uint32_t* my_epoch, const __nv_bfloat16* __restrict__ resid,
+    const __nv_bfloat16* __restrict__ gamma, __nv_bfloat16* __restrict__ x_out,
+    __nv_bfloat16* __restrict__ y, int64_t rows, int64_t H, float eps, uint32_t* err) {
+  extern __shared__ float rowbuf[];
+  __shared__ float red[kThreads / 32];
+  const int64_t n8 = H / 8;
+  // 1. publish my partial rows
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x)
+    for (int64_t c = threadIdx.x; c < n8; c += kThreads)
+      reinterpret_cast<uint4*>(my_stage + r * H)[c] = reinterpret_cast<const uint4*>(partial + r * H)[c];
+  // 2. all peers' rows for this CTA are in place
+  if (!cta_barrier(pp, my_epoch, world, rank, err)) return;
+  // 3. reduce + residual + norm
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    float ss = 0.0f;
+    for (int64_t c = threadIdx.x; c < n8; c += kThreads) {
+      float acc[8];
+      {
+        const uint4 u = reinterpret_cast<const uint4*>(resid + r * H)[c];
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h2[i]);
+          acc[2 * i] = f.x;
+          acc[2 * i + 1] = f.y;
+        }
+      }
+      for (int p = 0; p < world; ++p) {
+        const uint4 u = reinterpret_cast<const uint4*>(pp.buf[p] + r * H)[c];
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h2[i]);
+          acc[2 * i] += f.x;
+          acc[2 * i + 1] += f.y;
+        }
+      }
+      uint4 o;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        o2[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+        rowbuf[c * 8 + 2 * i] = acc[2 * i];
+        rowbuf[c * 8 + 2 * i + 1] = acc[2 * i + 1];
+        ss += acc[2 * i] * acc[2 * i] + acc[2 * i + 1] * acc[2 * i + 1];
+      }
+      reinterpret_cast<uint4*>(x_out + r * H)[c] = o;
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, s);
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = ss;
+    __syncthreads();
+    float tot = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) tot += red[w];
+    const float inv = rsqrtf(tot / static_cast<float>(H) + eps);
+    for (int64_t c = threadIdx.x; c < H; c += kThreads)
+      y[r * H + c] = __float2bfloat16(rowbuf[c] * inv * __bfloat162float(gamma[c]));
+    __syncthreads();
+  }
+  // 4. peers are done reading my staging rows
+  cta_barrier(pp, my_epoch, world, rank, err);
+}
+
+// One-shot all-reduce (sum) over peer memory: same protocol, no norm.
+__global__ void __launch_bounds__(kThreads) allreduce_p2p_kernel(
+    PeerPtrs pp, int world, int rank, const __nv_bfloat16* __restrict__ partial,
+    __nv_bfloat16* __restrict__ my_stage, uint32_t* my_epoch, __nv_bfloat16* __restrict__ out,
+    int64_t rows, int64_t H, uint32_t* err) {
+  const int64_t n8 = H / 8;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x)
+    for (int64_t c = threadIdx.x; c < n8; c += kThreads)
+      reinterpret_cast<uint4*>(my_stage + r * H)[c] = reinterpret_cast<const uint4*>(partial + r * H)[c];
+  if (!cta_barrier(pp, my_epoch, world, rank, err)) return;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x)
+    for (int64_t c = threadIdx.x; c < n8; c += kThreads) {
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int p = 0; p < world; ++p) {
+        const uint4 u = reinterpret_cast<const uint4*>(pp.buf[p] + r * H)[c];
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h2[i]);
+          acc[2 * i] += f.x;
+          acc[2 * i + 1] += f.y;
+        }
+      }
+      uint4 o;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o2[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+      reinterpret_cast<uint4*>(out + r * H)[c] = o;
+    }
+  cta_barrier(pp, my_epoch, world, rank, err);
+}
+
+size_t window_layout(size_t stage_bytes, size_t* flags_off, size_t* epoch_off) {
+  const size_t s = (stage_bytes + 255) / 256 * 256;
+  *flags_off = s;
+  *epoch_off = s + sizeof(uint32_t) * kMaxCtas * kMaxWorld;
+  return *epoch_off + sizeof(uint32_t) * kMaxCtas + sizeof(uint32_t) /*error flag*/;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- window API
+void comm_window_alloc(opf_comm* c, size_t stage_bytes, void* ipc_handle_out) {
+  size_t fo, eo;
+  const size_t total = window_layout(stage_bytes, &fo, &eo);
+  void* base = nullptr;
+  OPF_CUDA(cudaMalloc(&base, total));
+  OPF_CUDA(cudaMemset(base, 0, total));
+  c->window_base = base;
+  c->window_bytes = total;
+  c->peer_bytes = stage_bytes;
+  if (ipc_handle_out) {
+    cudaIpcMemHandle_t h;
+    OPF_CUDA(cudaIpcGetMemHandle(&h, base));
+    std::memcpy(ipc_handle_out, &h, sizeof(h));
+  }
+}
+
+void comm_window_open(opf_comm* c, const void* handles) {
+  require(c->world <= kMaxWorld, Errc::ConfigError, "peer window supports world <= 8");
+  size_t fo, eo;
+  window_layout(c->peer_bytes, &fo, &eo);
+  c->peer_buf.assign(c->world, nullptr);
+  c->peer_flag.assign(c->world, nullptr);
+  for (int p = 0; p < c->world; ++p) {
+    void* base = c->window_base;
+    if (p != c->rank) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const char*>(handles) + p * sizeof(cudaIpcMemHandle_t), sizeof(h));
+      OPF_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+      c->opened.push_back(base);
+    }
+    c->peer_buf[p] = base;
+    c->peer_flag[p] = reinterpret_cast<uint32_t*>(static_cast<char*>(base) + fo);
+  }
+}
+
+// virtual ranks on ONE device (tests): windows are plain allocations wired
+// together without IPC.
+void comm_window_link_local(opf_comm* const* comms, int world) {
+  size_t fo, eo;
+  for (int r = 0; r < world; ++r) {
+    opf_comm* c = comms[r];
+    window_layout(c->peer_bytes, &fo, &eo);
+    c->peer_buf.assign(world, nullptr);
+    c->peer_flag.assign(world, nullptr);
+    for (int p = 0; p < world; ++p) {
+      c->peer_buf[p] = comms[p]->window_base;
+      c->peer_flag[p] = reinterpret_cast<uint32_t*>(static_cast<char*>(comms[p]->window_base) + fo);
+    }
+  }
+}
+
+uint32_t comm_window_error(const opf_comm* c) {
+  size_t fo, eo;
+  window_layout(c->peer_bytes, &fo, &eo);
+  uint32_t e = 0;
+  OPF_CUDA(cudaMemcpy(&e, static_cast<char*>(c->window_base) + eo + sizeof(uint32_t) * kMaxCtas,
+                      sizeof(e), cudaMemcpyDeviceToHost));
+  return e;
+}
+
+bool ar_add_rmsnorm_p2p(const opf_comm* c, const opf_view& o, const opf_view& x, const opf_view& g,
+                        opf_view& x_out, opf_view& y, int64_t rows, float eps, int max_ctas,
+                        cudaStream_t s) {
+  if (!c || c->peer_buf.empty() || o.dtype != OPF_BF16) return false;
+  const int64_t H = view_row_elems(o);
+  if (H % 8 || static_cast<size_t>(rows * H * 2) > c->peer_bytes || H * 4 > 48 * 1024) return false;
+  size_t fo, eo;
+  window_layout(c->peer_bytes, &fo, &eo);
+  PeerPtrs pp{};
+  for (int p = 0; p < c->world; ++p) {
+    pp.buf[p] = static_cast<const __nv_bfloat16*>(c->peer_buf[p]);
+    pp.flags[p] = c->peer_flag[p];
+  }
+  char* base = static_cast<char*>(c->window_base);
+  int grid = max_ctas > 0 ? max_ctas : num_sms();
+  grid = static_cast<int>(std::min<int64_t>(std::min(grid, kMaxCtas), rows));
+  ar_add_rmsnorm_p2p_kernel<<<std::max(grid, 1), kThreads, H * sizeof(float), s>>>(
+      pp, c->world, c->rank, vptr<__nv_bfloat16>(o), reinterpret_cast<__nv_bfloat16*>(base),
+      reinterpret_cast<uint32_t*>(base + eo), vptr<__nv_bfloat16>(x), vptr<__nv_bfloat16>(g),
+      vptr<__nv_bfloat16>(x_out), vptr<__nv_bfloat16>(y), rows, H, eps,
+      reinterpret_cast<uint32_t*>(base + eo + sizeof(uint32_t) * kMaxCtas));
+  return true;
+}
+
+bool allreduce_p2p(const opf_comm* c, const opf_view& in, opf_view& out, int64_t rows, int max_ctas,
+                   cudaStream_t s) {
+  if (!c || c->peer_buf.empty() || in.dtype != OPF_BF16) return false;
+  const int64_t H = view_row_elems(in);
+  if (H % 8 || static_cast<size_t>(rows * H * 2) > c->peer_bytes) return false;
+  size_t fo, eo;
+  window_layout(c->peer_bytes, &fo, &eo);
+  PeerPtrs pp{};
+  for (int p = 0; p < c->world; ++p) {
+    pp.buf[p] = static_cast<const __nv_bfloat16*>(c->peer_buf[p]);
+    pp.flags[p] = c->peer_flag[p];
+  }
+  char* base = static_cast<char*>(c->window_base);
+  int grid = max_ctas > 0 ? max_ctas : num_sms();
+  grid = static_cast<int>(std::min<int64_t>(std::min(grid, kMaxCtas), rows));
+  allreduce_p2p_kernel<<<std::max(grid, 1), kThreads, 0, s>>>(
+      pp, c->world, c->rank, vptr<__nv_bfloat16>(in), reinterpret_cast<__nv_bfloat16*>(base),
+      reinterpret_cast<uint32_t*>(base + eo), vptr<__nv_bfloat16>(out), rows, H,
+      reinterpret_cast<uint32_t*>(base + eo + sizeof(uint32_t) * kMaxCtas));
+  return true;
+}
+
+}  // namespace opflow

@@ -512,6 +512,34 @@ class Comm:
         check(lib().opf_comm_unique_id(arr))
         return bytes(arr)
 
+    def enable_window(self, stage_bytes: int) -> None:
+        """Symmetric peer window (CUDA IPC) for the one-shot all-reduce and the
+        fused all-reduce+RMSNorm kernels; handles travel over torch.distributed."""
+        import torch.distributed as dist
+        h = (C.c_uint8 * 64)()
+        check(lib().opf_comm_window_alloc(self._h, stage_bytes, h))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, bytes(h))
+        flat = (C.c_uint8 * (64 * self.world))(*b"".join(allh))
+        check(lib().opf_comm_window_open(self._h, flat))
+
+    @staticmethod
+    def virtual(world: int, device: int, stage_bytes: int) -> List["Comm"]:
+        """`world` ranks sharing ONE device (tests of the peer-memory protocol)."""
+        arr = (C.c_void_p * world)()
+        check(lib().opf_comm_create_virtual(world, device, stage_bytes, arr))
+        out = []
+        for r in range(world):
+            c = Comm.__new__(Comm)
+            c.world, c.rank, c._h = world, r, C.c_void_p(arr[r])
+            out.append(c)
+        return out
+
+    def window_error(self) -> int:
+        e = C.c_uint32()
+        check(lib().opf_comm_window_error(self._h, C.byref(e)))
+        return e.value
+
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value:
             lib().opf_comm_free(self._h)
@@ -572,10 +600,15 @@ class Session:
             self._h = C.c_void_p()
 
 
-def launch(op: OpDecl | dict, inputs: Sequence, outputs: Sequence, rows: int, stream=None) -> None:
+def launch(op: OpDecl | dict, inputs: Sequence, outputs: Sequence, rows: int, stream=None,
+           comm: Optional[Comm] = None, max_ctas: int = 0) -> None:
     """Device eval_op_into: run one operator into caller-provided tensors."""
     opj = json.dumps(op.to_json() if isinstance(op, OpDecl) else op)
     iv = (opf_view * max(1, len(inputs)))(*[view_of(t) for t in inputs])
     ov = (opf_view * max(1, len(outputs)))(*[view_of(t) for t in outputs])
     s = stream.cuda_stream if stream is not None and hasattr(stream, "cuda_stream") else stream
+    if comm is not None or max_ctas:
+        check(lib().opf_launch_comm(opj.encode(), iv, len(inputs), ov, len(outputs), rows,
+                                    comm._h if comm else None, max_ctas, s))
+        return
     check(lib().opf_launch(opj.encode(), iv, len(inputs), ov, len(outputs), rows, s))

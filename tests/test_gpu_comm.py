@@ -1,0 +1,52 @@
+"""GPU: the peer-memory collectives (one-shot all-reduce, fused all-reduce +
+residual add + RMSNorm) run their full cross-rank flag protocol with W
+"virtual ranks" sharing one B200 (each rank = its own window, launch and
+stream).  The real multi-GPU path differs only in how the windows are mapped
+(CUDA IPC over NVLink instead of same-device pointers)."""
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2605_21603_b200 import opflow as of
+from paper_2605_21603_b200.workloads import rel_err
+
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("built")]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_fused_allreduce_add_rmsnorm_virtual_ranks(cuda, world):
+    import torch
+    rows, H = 64, 4096
+    comms = of.Comm.virtual(world, 0, rows * H * 2)
+    rng = np.random.default_rng(world)
+    tb = lambda a: torch.from_numpy(a.astype(np.float32)).cuda().to(torch.bfloat16)
+    x = tb(rng.uniform(-1, 1, (rows, H)))
+    g = tb(1 + 0.1 * rng.uniform(-1, 1, H))
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    op = {"name": "f", "kind": "Custom", "inputs": [], "outputs": [],
+          "attrs": {"custom_name": "allreduce_add_rmsnorm", "world_size": world, "params": {"eps": 1e-5}}}
+    for it in range(3):  # epochs advance on the device across calls
+        parts = [tb(rng.uniform(-1, 1, (rows, H))) for _ in range(world)]
+        outs = [(torch.empty_like(x), torch.empty_like(x)) for _ in range(world)]
+        torch.cuda.synchronize()
+        for r in range(world):
+            of.launch(op, [parts[r], x, g], list(outs[r]), rows, streams[r], comm=comms[r], max_ctas=8)
+        torch.cuda.synchronize()
+        for c in comms:
+            assert c.window_error() == 0
+        s = x.float().cpu().numpy() + sum(p.float().cpu().numpy() for p in parts)
+        want_h = oracle.rmsnorm(s, g.float().cpu().numpy(), 1e-5)
+        for r in range(world):
+            assert rel_err(outs[r][0].float().cpu().numpy(), s) < 1e-2
+            assert rel_err(outs[r][1].float().cpu().numpy(), want_h) < 1e-2
+    # one-shot all-reduce (the AllReduce kind with a windowed communicator)
+    ar = {"name": "ar", "kind": "AllReduce", "inputs": [], "outputs": [], "attrs": {"world_size": world}}
+    parts = [tb(rng.uniform(-1, 1, (rows, H))) for _ in range(world)]
+    outs = [torch.empty_like(x) for _ in range(world)]
+    torch.cuda.synchronize()
+    for r in range(world):
+        of.launch(ar, [parts[r]], [outs[r]], rows, streams[r], comm=comms[r], max_ctas=8)
+    torch.cuda.synchronize()
+    want = sum(p.float().cpu().numpy() for p in parts)
+    for r in range(world):
+        assert rel_err(outs[r].float().cpu().numpy(), want) < 1e-2
