@@ -128,4 +128,33 @@ void k_pack_gate_up(const void* src, void* dst, int64_t K, int64_t I, cudaStream
 void gemm_bf16_simt(const GemmArgs& g, cudaStream_t s);
 int num_sms();
 
+// ---- Programmatic Dependent Launch (PDL) -----------------------------------------
+// Hot-path kernels are launched with programmatic stream serialization: the
+// next kernel on a stream may be scheduled before this one finishes; it runs
+// its prologue (barrier init, TMEM alloc, descriptor prefetch) and blocks in
+// pdl_wait() until the previous grid has completed and flushed.  Inside CUDA
+// graphs this becomes a programmatic edge.  OPF_PDL=0 disables it.
+bool pdl_enabled();
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+#endif
+
 }  // namespace opflow

@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(kWarps * 32)
                       const int64_t* __restrict__ ctx_len, __nv_bfloat16* __restrict__ out, int nq,
                       int nkv, int64_t max_pages, float scale_log2, int64_t n_items) {
   extern __shared__ __align__(128) uint8_t smem[];
+  pdl_wait();
+  pdl_trigger();
   // persistent: a CTA (one per SM) walks (sequence, kv head) items, so the
   // launch occupies exactly gridDim.x SMs (SM partitioning under overlap)
   for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -250,8 +252,8 @@ bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __
   const int64_t items = B * nkv;
   int64_t grid = max_ctas > 0 ? std::min<int64_t>(max_ctas, num_sms()) : num_sms();
   grid = std::max<int64_t>(1, std::min(grid, items));
-  decode_mma_kernel<<<static_cast<unsigned>(grid), kWarps * 32, kSmemRing, s>>>(
-      qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, scale * 1.4426950408889634f, items);
+  launch_pdl(decode_mma_kernel, dim3(static_cast<unsigned>(grid)), dim3(kWarps * 32), kSmemRing, s,
+             qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, scale * 1.4426950408889634f, items);
   return true;
 }
 

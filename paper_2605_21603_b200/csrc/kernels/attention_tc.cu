@@ -93,6 +93,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     fa_prefill_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
                       int nq, int nkv, int S, int q_tiles, float scale_log2) {
   extern __shared__ __align__(128) uint8_t smem[];
+  pdl_wait();
+  pdl_trigger();
   uint8_t* sQ = smem;
   uint8_t* sK[2] = {smem + kQBytes, smem + kQBytes + 2 * kKVBytes};
   uint8_t* sV[2] = {smem + kQBytes + kKVBytes, smem + kQBytes + 3 * kKVBytes};
@@ -274,7 +276,8 @@ bool prefill_bf16_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t rows,
   const int q_tiles = (S + BQ - 1) / BQ;
   const unsigned grid = static_cast<unsigned>(q_tiles * nq * n_seqs);
   const float scale_log2 = scale * 1.4426950408889634f;
-  fa_prefill_kernel<<<grid, kThreads, kSmem, s>>>(qkv, out, nq, nkv, S, q_tiles, scale_log2);
+  launch_pdl(fa_prefill_kernel, dim3(grid), dim3(kThreads), kSmem, s, qkv, out, nq, nkv, S, q_tiles,
+             scale_log2);
   return true;
 }
 

@@ -30,7 +30,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kMaxWorld = 8;
 constexpr int kMaxCtas = 1024;
-constexpr int64_t kSpinLimit = 1ll << 28;
+constexpr int64_t kSpinLimit = 1ll << 24;  // ~seconds: error flag instead of a hung GPU
 
 struct PeerPtrs {
   const __nv_bfloat16* buf[kMaxWorld];  // staging rows of each rank

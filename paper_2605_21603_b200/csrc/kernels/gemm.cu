@@ -287,6 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -473,6 +475,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync_all();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();     // inputs of the previous kernel on this stream are visible from here
+  pdl_trigger();  // persistent grid: let the next kernel stage its prologue on freed SMs
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
@@ -644,18 +648,18 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     if (tiles < clusters) clusters = static_cast<int>(tiles);
     const unsigned blocks = 2u * static_cast<unsigned>(std::max(clusters, 1));
     if (g.epi == 1)
-      gemm_tc2_kernel<1><<<blocks, kThreads, kSmemBytes2, s>>>(ma, mb, mc, g.m, g.n, g.k);
+      launch_pdl(gemm_tc2_kernel<1>, dim3(blocks), dim3(kThreads), kSmemBytes2, s, ma, mb, mc, g.m, g.n, g.k);
     else
-      gemm_tc2_kernel<0><<<blocks, kThreads, kSmemBytes2, s>>>(ma, mb, mc, g.m, g.n, g.k);
+      launch_pdl(gemm_tc2_kernel<0>, dim3(blocks), dim3(kThreads), kSmemBytes2, s, ma, mb, mc, g.m, g.n, g.k);
     return;
   }
   const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN);
   const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN);
   if (tiles < grid) grid = static_cast<int>(tiles);
   if (g.epi == 1)
-    gemm_tc_kernel<1><<<grid, kThreads, kSmemBytes, s>>>(ma, mb, mc, g.m, g.n, g.k);
+    launch_pdl(gemm_tc_kernel<1>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, g.n, g.k);
   else
-    gemm_tc_kernel<0><<<grid, kThreads, kSmemBytes, s>>>(ma, mb, mc, g.m, g.n, g.k);
+    launch_pdl(gemm_tc_kernel<0>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, g.n, g.k);
 }
 
 // [K, 2I] gate|up weight -> K-major [2I, K] with gate/up interleaved in 128-row

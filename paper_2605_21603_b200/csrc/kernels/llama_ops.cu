@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const T* __restrict__
                                                            const T* __restrict__ g,
                                                            T* __restrict__ s_out,
                                                            T* __restrict__ y, int64_t H, float eps) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int V = Vec<T>::N;
   __shared__ float red[kThreads / 32];
   const int64_t row = blockIdx.x;
@@ -118,6 +120,8 @@ __global__ void __launch_bounds__(256) rope_kernel(const T* __restrict__ qkv,
                                                    const int64_t* __restrict__ pos,
                                                    T* __restrict__ out, int n_rot_heads,
                                                    int n_v_heads, int hd, float log2_theta) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int V = Vec<T>::N;
   const int64_t row = blockIdx.x;
   const int64_t W = static_cast<int64_t>(n_rot_heads + n_v_heads) * hd;
@@ -155,6 +159,8 @@ __global__ void __launch_bounds__(256) rope_kernel(const T* __restrict__ qkv,
 template <typename T>
 __global__ void silu_mul_kernel(const T* __restrict__ gu, T* __restrict__ out, int64_t rows,
                                 int64_t I) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int V = Vec<T>::N;
   const int64_t per_row = I / V, n = rows * per_row;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -177,11 +183,13 @@ opf_status run_rmsnorm(const opf_view* in, opf_view* out, int64_t rows, float ep
     return op_error(Errc::ShapeMismatch, "rmsnorm: hidden " + std::to_string(H) + " unsupported");
   if (rows == 0) return 0;
   if (res)
-    rmsnorm_kernel<T, true><<<static_cast<unsigned>(rows), kThreads, 0, s>>>(
-        vptr<T>(in[0]), vptr<T>(in[1]), vptr<T>(in[2]), vptr<T>(out[0]), vptr<T>(out[1]), H, eps);
+    launch_pdl(rmsnorm_kernel<T, true>, dim3(static_cast<unsigned>(rows)), dim3(kThreads), 0, s,
+               static_cast<const T*>(vptr<T>(in[0])), static_cast<const T*>(vptr<T>(in[1])),
+               static_cast<const T*>(vptr<T>(in[2])), vptr<T>(out[0]), vptr<T>(out[1]), H, eps);
   else
-    rmsnorm_kernel<T, false><<<static_cast<unsigned>(rows), kThreads, 0, s>>>(
-        vptr<T>(in[0]), nullptr, vptr<T>(in[1]), nullptr, vptr<T>(out[0]), H, eps);
+    launch_pdl(rmsnorm_kernel<T, false>, dim3(static_cast<unsigned>(rows)), dim3(kThreads), 0, s,
+               static_cast<const T*>(vptr<T>(in[0])), static_cast<const T*>(nullptr),
+               static_cast<const T*>(vptr<T>(in[1])), static_cast<T*>(nullptr), vptr<T>(out[0]), H, eps);
   return launch_status("rmsnorm");
 }
 
@@ -220,8 +228,9 @@ opf_status op_rope(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_vi
   const int64_t* pos = vptr<int64_t>(in[1]);
   if (in[0].dtype == OPF_BF16) {
     if ((hd / 2) % 8) return op_error(Errc::ShapeMismatch, "rope: head_dim/2 must be a multiple of 8");
-    rope_kernel<__nv_bfloat16><<<static_cast<unsigned>(rows), 256, 0, s>>>(
-        vptr<__nv_bfloat16>(in[0]), pos, vptr<__nv_bfloat16>(out[0]), nq + nkv, nkv, hd, l2t);
+    launch_pdl(rope_kernel<__nv_bfloat16>, dim3(static_cast<unsigned>(rows)), dim3(256), 0, s,
+               static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[0])), pos,
+               vptr<__nv_bfloat16>(out[0]), nq + nkv, nkv, hd, l2t);
   } else if (in[0].dtype == OPF_F32) {
     if ((hd / 2) % 4) return op_error(Errc::ShapeMismatch, "rope: head_dim/2 must be a multiple of 4");
     rope_kernel<float><<<static_cast<unsigned>(rows), 256, 0, s>>>(vptr<float>(in[0]), pos,
@@ -245,8 +254,9 @@ opf_status op_silu_mul(const opf_op_ctx*, const opf_view* in, int32_t n_in, opf_
     if (I % 8) return op_error(Errc::ShapeMismatch, "silu_mul: inter % 8");
     const int64_t n = rows * I / 8;
     const int g = static_cast<int>(std::min<int64_t>((n + threads - 1) / threads, num_sms() * 16LL));
-    silu_mul_kernel<__nv_bfloat16><<<g, threads, 0, s>>>(vptr<__nv_bfloat16>(in[0]),
-                                                         vptr<__nv_bfloat16>(out[0]), rows, I);
+    launch_pdl(silu_mul_kernel<__nv_bfloat16>, dim3(g), dim3(threads), 0, s,
+               static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[0])), vptr<__nv_bfloat16>(out[0]),
+               rows, I);
   } else if (in[0].dtype == OPF_F32) {
     if (I % 4) return op_error(Errc::ShapeMismatch, "silu_mul: inter % 4");
     const int64_t n = rows * I / 4;

@@ -247,6 +247,14 @@ int grid_for(int64_t n, int threads) {
 
 }  // namespace
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("OPF_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int num_sms() {
   static int n = [] {
     int dev = 0, v = 148;
