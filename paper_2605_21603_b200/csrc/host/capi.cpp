@@ -403,8 +403,9 @@ opf_status opf_session_run(opf_session* s, const char* strategy, void* stream) {
   return guard([&] {
     need(s, "session");
     const std::string spec = strategy ? strategy : "{}";
-    auto strat = make_strategy(spec);
-    s->s->run(*strat, "builtin:" + spec, static_cast<cudaStream_t>(stream));
+    auto cs = s->s->choose(spec, static_cast<cudaStream_t>(stream));
+    auto strat = make_strategy(cs);
+    s->s->run(*strat, "builtin:" + cs, static_cast<cudaStream_t>(stream));
   });
 }
 

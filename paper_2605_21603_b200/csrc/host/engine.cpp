@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <functional>
 #include <numeric>
 
 #include "opflow/json.hpp"
@@ -745,6 +746,79 @@ void Session::plan_only(Scheduler& strat, const std::string& key) {
   last_ = lookup_or_build(strat, key);
 }
 
+std::string Session::choose(const std::string& spec, cudaStream_t stream) {
+  json::Value v;
+  try {
+    v = json::parse(spec.empty() ? "{}" : spec);
+  } catch (const std::exception& e) {
+    fail(Errc::ConfigError, std::string("strategy spec: ") + e.what());
+  }
+  const json::Value* name = v.get("name");
+  if (!name || name->t != json::Value::T::String || name->str() != "auto") return spec;
+  const json::Value* cands = v.get("candidates");
+  require(cands && cands->t == json::Value::T::Array && !cands->arr().empty(), Errc::ConfigError,
+          "auto strategy needs a non-empty 'candidates' list");
+  const std::string key = spec + "|rows=" + std::to_string(rows());
+  auto hit = auto_choice_.find(key);
+  if (hit != auto_choice_.end()) return hit->second;
+  require(!dry_, Errc::EngineStopped, "auto strategy selection needs a device session");
+  const int reps = v.get("reps") ? static_cast<int>(v.get("reps")->as_i64()) : 5;
+  // serialise candidate specs back to text (they are plain objects of scalars / arrays)
+  std::function<std::string(const json::Value&)> dump = [&](const json::Value& x) -> std::string {
+    switch (x.t) {
+      case json::Value::T::Null: return "null";
+      case json::Value::T::Bool: return x.b ? "true" : "false";
+      case json::Value::T::Int: return x.is_neg ? std::to_string(x.i) : std::to_string(x.u);
+      case json::Value::T::Double: {
+        char b[64];
+        std::snprintf(b, sizeof b, "%.17g", x.d);
+        return b;
+      }
+      case json::Value::T::String: return json::quote(x.s);
+      case json::Value::T::Array: {
+        std::string o = "[";
+        for (std::size_t i = 0; i < x.a->size(); ++i) o += (i ? "," : "") + dump((*x.a)[i]);
+        return o + "]";
+      }
+      case json::Value::T::Object: {
+        std::string o = "{";
+        for (std::size_t i = 0; i < x.o->size(); ++i)
+          o += (i ? "," : "") + json::quote((*x.o)[i].first) + ":" + dump((*x.o)[i].second);
+        return o + "}";
+      }
+    }
+    return "null";
+  };
+  cudaEvent_t e0, e1;
+  OPF_CUDA(cudaEventCreate(&e0));
+  OPF_CUDA(cudaEventCreate(&e1));
+  std::vector<double> times;
+  std::string best;
+  double best_ms = 1e300;
+  for (const json::Value& c : cands->arr()) {
+    const std::string cs = dump(c);
+    auto strat = make_strategy(cs);
+    run(*strat, "builtin:" + cs, stream);  // build + capture + warm-up
+    OPF_CUDA(cudaEventRecord(e0, stream));
+    for (int i = 0; i < reps; ++i) run(*strat, "builtin:" + cs, stream);
+    OPF_CUDA(cudaEventRecord(e1, stream));
+    OPF_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.0f;
+    OPF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    times.push_back(ms / reps);
+    if (ms / reps < best_ms) {
+      best_ms = ms / reps;
+      best = cs;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  auto_choice_[key] = best;
+  auto_times_[key] = times;
+  log_info("auto strategy for rows=" + std::to_string(rows()) + ": " + best);
+  return best;
+}
+
 void Session::run(Scheduler& strat, const std::string& key_in, cudaStream_t stream) {
   require(!dry_, Errc::EngineStopped, "dry session cannot execute");
   CompiledPlan* cp = lookup_or_build(strat, key_in);
@@ -807,6 +881,20 @@ std::string Session::stats_json() const {
                   ",\"plan_cache_misses\":" + std::to_string(misses_) +
                   ",\"arena_bytes\":" + std::to_string(arena_bytes_) +
                   ",\"cached_plans\":" + std::to_string(cache_.size());
+  s += ",\"auto\":[";
+  bool first = true;
+  for (const auto& [k, v] : auto_choice_) {
+    s += std::string(first ? "" : ",") + "{\"key\":" + json::quote(k) + ",\"chosen\":" + json::quote(v);
+    std::string ts = "[";
+    for (std::size_t i = 0; i < auto_times_.at(k).size(); ++i) {
+      char b[32];
+      std::snprintf(b, sizeof b, "%s%.4f", i ? "," : "", auto_times_.at(k)[i]);
+      ts += b;
+    }
+    s += ",\"ms\":" + ts + "]}";
+    first = false;
+  }
+  s += "]";
   if (last_) {
     s += ",\"last\":{\"key\":" + json::quote(last_->key) +
          ",\"dispatches\":" + std::to_string(last_->dispatches.size()) +

@@ -207,6 +207,11 @@ class Session {
   ~Session();
 
   void bind(const std::string& tensor, const opf_view& v);
+  // Context-aware strategy selection: for
+  // {"name":"auto","candidates":[spec, ...]} time every candidate's captured
+  // schedule on the device for the current row count, cache the winner per
+  // rows, and return its spec; any other spec is returned unchanged.
+  std::string choose(const std::string& spec, cudaStream_t stream);
   void run(Scheduler& strat, const std::string& key, cudaStream_t stream);
   opf_view output(const std::string& tensor);
   std::string stats_json() const;
@@ -244,6 +249,8 @@ class Session {
   CompiledPlan* last_ = nullptr;
   std::vector<cudaEvent_t> events_;
   int64_t hits_ = 0, misses_ = 0, runs_ = 0;
+  std::map<std::string, std::string> auto_choice_;        // (auto spec | rows) -> winner spec
+  std::map<std::string, std::vector<double>> auto_times_;  // (auto spec | rows) -> ms per candidate
   bool dry_ = false;
   int64_t dry_rows_ = 0;
   CompiledPlan* lookup_or_build(Scheduler& strat, const std::string& key);
