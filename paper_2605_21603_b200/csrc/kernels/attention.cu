@@ -15,6 +15,8 @@
 #include <cuda_bf16.h>
 
 #include <cfloat>
+#include <cstdlib>
+#include <string>
 
 #include "opflow/device.hpp"
 
@@ -277,6 +279,9 @@ bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __
 // shape is not supported there.
 bool prefill_bf16_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t rows, int nq, int nkv,
                      int hd, int S, float scale, cudaStream_t s);
+// attention_fa_tc.cu: tcgen05/TMEM flash attention (hd 128, S % 128 == 0)
+bool prefill_bf16_tcgen05(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t rows, int nq, int nkv,
+                          int hd, int S, float scale, int max_ctas, cudaStream_t s);
 
 opf_status attn_prefill_simt(const opf_view& in, opf_view& out, int64_t rows, int nq, int nkv,
                              int hd, int S, cudaStream_t s) {
@@ -311,10 +316,23 @@ opf_status op_attn_prefill(const opf_op_ctx* c, const opf_view* in, int32_t n_in
                                              " not a multiple of seq_len " + std::to_string(S));
   if (rows == 0) return 0;
   auto s = static_cast<cudaStream_t>(stream);
-  const bool force_simt = ctx_param(*c, "simt", 0.0) != 0.0;
-  if (in[0].dtype == OPF_BF16 && !force_simt &&
+  // impl: 0 auto (tcgen05 -> mma.sync -> SIMT), 1 mma.sync FA2, 2 SIMT; OPF_PREFILL=fa2|simt overrides auto
+  static const int env_impl = [] {
+    const char* e = std::getenv("OPF_PREFILL");
+    if (!e) return 0;
+    return std::string(e) == "fa2" ? 1 : std::string(e) == "simt" ? 2 : 0;
+  }();
+  int impl = static_cast<int>(ctx_param(*c, "impl", 0.0));
+  if (ctx_param(*c, "simt", 0.0) != 0.0) impl = 2;
+  if (impl == 0) impl = env_impl;
+  const float scale = 1.0f / sqrtf(static_cast<float>(hd));
+  if (in[0].dtype == OPF_BF16 && impl == 0 &&
+      prefill_bf16_tcgen05(vptr<__nv_bfloat16>(in[0]), vptr<__nv_bfloat16>(out[0]), rows, nq, nkv, hd, S,
+                           scale, c->max_ctas, s))
+    return launch_status("attn_prefill_tcgen05");
+  if (in[0].dtype == OPF_BF16 && impl <= 1 &&
       prefill_bf16_tc(vptr<__nv_bfloat16>(in[0]), vptr<__nv_bfloat16>(out[0]), rows, nq, nkv, hd, S,
-                      1.0f / sqrtf(static_cast<float>(hd)), s))
+                      scale, s))
     return launch_status("attn_prefill_tc");
   return attn_prefill_simt(in[0], out[0], rows, nq, nkv, hd, S, s);
 }

@@ -36,3 +36,59 @@ def test_decode_variants(cuda, nq, nkv, impl):
     got = out.float().cpu().numpy()
     for b in range(B):
         assert rel_err(got[b], want[b]) < 1e-2, (b, ctx[b], rel_err(got[b], want[b]))
+
+
+def _prefill(t, nq, nkv, S, rows, **extra):
+    import torch
+    op = {"name": "a", "kind": "Custom", "inputs": [], "outputs": [],
+          "attrs": {"custom_name": "attn_prefill",
+                    "params": dict({"heads": nq, "kv_heads": nkv, "head_dim": 128, "seq_len": S}, **extra)}}
+    out = torch.empty(rows, nq * 128, dtype=torch.bfloat16, device="cuda")
+    of.launch(op, [t], [out], rows)
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy()
+
+
+@pytest.mark.parametrize("S,nq,nkv,seqs,ramp", [
+    (128, 2, 2, 1, 0.0), (256, 4, 1, 3, 0.0), (1024, 8, 2, 2, 0.0), (512, 4, 4, 2, 6.0),
+    (2048, 2, 1, 1, 3.0), (384, 6, 2, 5, 0.0)])
+def test_prefill_tcgen05_vs_oracle(cuda, S, nq, nkv, seqs, ramp):
+    """tcgen05/TMEM prefill (impl 0) vs the fp64 oracle and the mma.sync FA2
+    kernel (impl 1).  `ramp` grows |q|,|k| along the sequence so later key tiles
+    raise the row max by more than the lazy-rescale threshold (exercises the
+    TMEM O rescale); persistent CTAs see several items each (seqs x heads x tiles
+    > 148 for the larger cases)."""
+    import torch
+    rng = np.random.default_rng(S * 7 + nq + seqs)
+    hd, rows = 128, S * seqs
+    qkv = rng.uniform(-1, 1, (rows, (nq + 2 * nkv) * hd)).astype(np.float32)
+    if ramp:
+        pos = (np.arange(rows) % S) / S
+        qkv[:, :(nq + nkv) * hd] *= (1.0 + ramp * pos)[:, None]
+    t = torch.from_numpy(qkv).cuda().to(torch.bfloat16)
+    want = oracle.attn_prefill(t.float().cpu().numpy(), nq, nkv, hd, S)
+    got = _prefill(t, nq, nkv, S, rows)
+    fa2 = _prefill(t, nq, nkv, S, rows, impl=1)
+    assert np.isfinite(got).all()
+    assert rel_err(got, want) < 1e-2
+    assert rel_err(fa2, want) < 1e-2
+    # per-row check too (a wrong tile hides in a normwise error)
+    row_err = np.abs(got - want).max(axis=1) / (np.abs(want).max(axis=1) + 1e-6)
+    assert row_err.max() < 5e-2, int(row_err.argmax())
+
+
+def test_prefill_tcgen05_capped_ctas(cuda):
+    """SM-budgeted launch (max_ctas, NanoFlow lane budgets) keeps results."""
+    import torch
+    rng = np.random.default_rng(5)
+    S, nq, nkv, seqs = 512, 4, 2, 2
+    qkv = rng.uniform(-1, 1, (S * seqs, (nq + 2 * nkv) * 128)).astype(np.float32)
+    t = torch.from_numpy(qkv).cuda().to(torch.bfloat16)
+    want = oracle.attn_prefill(t.float().cpu().numpy(), nq, nkv, 128, S)
+    op = {"name": "a", "kind": "Custom", "inputs": [], "outputs": [],
+          "attrs": {"custom_name": "attn_prefill", "params": {"heads": nq, "kv_heads": nkv, "head_dim": 128, "seq_len": S}}}
+    for cap in (1, 3, 17):
+        out = torch.empty(S * seqs, nq * 128, dtype=torch.bfloat16, device="cuda")
+        of.launch(op, [t], [out], S * seqs, max_ctas=cap)
+        torch.cuda.synchronize()
+        assert rel_err(out.float().cpu().numpy(), want) < 1e-2, cap
