@@ -17,7 +17,9 @@ Restated algorithms (each cites the reference file:line it follows):
     compiled reference in tests/test_oracle.py.
 Extensions (parity unpinned in the reference, which has no Llama semantics;
 SURVEY.md §8c.6): rmsnorm, add_rmsnorm, rope, attn_prefill, attn_decode,
-silu_mul — fp32/fp64 numpy, cross-checked against oracle/ref_shim.cpp and torch.
+silu_mul — fp32/fp64 numpy, cross-checked against oracle/ref_shim.cpp and torch;
+qk_norm_rope and the MoE ops (moe_topk / moe_route / dispatch / experts / combine),
+restating the published Qwen3-MoE layer (parity unpinned, pinned here by tests).
 """
 from __future__ import annotations
 
@@ -178,6 +180,97 @@ def silu_mul(gu):
     return (g / (1.0 + np.exp(-g)) * gu[:, I:]).astype(np.float32)
 
 
+def round_bf16(a):
+    """Round-to-nearest-even to bf16, returned as float32 (storage contract of bf16 tensors)."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return u.view(np.float32)
+
+
+# ------------------------------------------------------------------ Qwen3 extensions
+# No Qwen3 / MoE semantics exist in the reference (SURVEY §8c gotcha 6): these
+# restate the published Qwen3 layer (HF modeling_qwen3_moe: q_norm/k_norm before
+# RoPE; router softmax over the selected top-k when norm_topk_prob) in fp64.
+def qk_norm_rope(qkv, pos, qn, kn, heads, kv_heads, head_dim, theta, eps):
+    y = qkv.astype(np.float64).copy()
+    for h in range(heads + kv_heads):
+        blk = y[:, h * head_dim:(h + 1) * head_dim]
+        g = (qn if h < heads else kn).astype(np.float64)
+        y[:, h * head_dim:(h + 1) * head_dim] = blk / np.sqrt((blk * blk).mean(axis=1, keepdims=True) + eps) * g
+    return rope(y, pos, heads, kv_heads, head_dim, theta)
+
+
+def moe_topk(logits, k, renorm=True):
+    """ids = top-k by (value desc, index asc); w = softmax over the selected k
+    logits (renorm) or the full-softmax probabilities of the selected experts."""
+    l64 = logits.astype(np.float64)
+    order = np.argsort(-l64, axis=1, kind="stable")
+    ids = order[:, :k].astype(np.int64)
+    v = np.take_along_axis(l64, ids, axis=1)
+    e = np.exp(v - v[:, :1])
+    denom = e.sum(axis=1, keepdims=True) if renorm else np.exp(l64 - v[:, :1]).sum(axis=1, keepdims=True)
+    return ids, (e / denom).astype(np.float32)
+
+
+def moe_route(ids, experts):
+    """Stable counting sort of the T*k (token, j) slots by expert: slot[t, j] =
+    row of (t, j) in the expert-sorted layout (-1 for ids outside [0, E)), and
+    the expert of every sorted row."""
+    flat = ids.reshape(-1)
+    valid = (flat >= 0) & (flat < experts)
+    key = np.where(valid, flat, experts)
+    order = np.argsort(key, kind="stable")
+    pos = np.empty(flat.size, dtype=np.int64)
+    pos[order] = np.arange(flat.size)
+    slot = np.where(valid, pos, -1).reshape(ids.shape)
+    return slot, key[order]
+
+
+def moe_dispatch(x, ids, experts):
+    T, k = ids.shape
+    H = x.shape[1]
+    slot, _ = moe_route(ids, experts)
+    xd = np.zeros((T * k, H), dtype=np.float32)
+    s = slot.reshape(-1)
+    tok = np.repeat(np.arange(T), k)
+    ok = s >= 0
+    xd[s[ok]] = x[tok[ok]]
+    return xd.reshape(T, k * H), slot
+
+
+def moe_experts(act, ids, w, experts, gate_up):
+    """Grouped expert MatMul over the dispatched rows; w = [E, K, N] per-expert
+    [K, N] weights; gate_up fuses SiLU(gate) * up (gate = columns [0, N/2))."""
+    T, k = ids.shape
+    _, row_expert = moe_route(ids, experts)
+    K = w.shape[1]
+    a = act.reshape(T * k, K).astype(np.float64)
+    n_out = w.shape[2] // 2 if gate_up else w.shape[2]
+    out = np.zeros((T * k, n_out), dtype=np.float32)
+    for e in range(experts):
+        rows = np.nonzero(row_expert == e)[0]
+        if rows.size == 0:
+            continue
+        y = a[rows] @ w[e].astype(np.float64)
+        if gate_up:
+            g, u = y[:, :n_out], y[:, n_out:]
+            y = g / (1.0 + np.exp(-g)) * u
+        out[rows] = y
+    return out.reshape(T, k * n_out)
+
+
+def moe_combine(yd, slot, w):
+    T, k = slot.shape
+    H = yd.shape[1] // k
+    rows = yd.reshape(T * k, H).astype(np.float64)
+    y = np.zeros((T, H), dtype=np.float64)
+    for j in range(k):
+        s = slot[:, j]
+        ok = s >= 0
+        y[ok] += w[ok, j:j + 1].astype(np.float64) * rows[s[ok]]
+    return y.astype(np.float32)
+
+
 def attn_prefill(qkv, heads, kv_heads, head_dim, seq_len):
     rows = qkv.shape[0]
     out = np.zeros((rows, heads * head_dim), dtype=np.float32)
@@ -307,6 +400,18 @@ def evaluate(desc_json: str, rows: int, bindings: Dict[str, np.ndarray],
             elif fn == "attn_prefill":
                 r = [attn_prefill(x[0], int(p["heads"]), int(p["kv_heads"]), int(p["head_dim"]),
                                   int(p["seq_len"]))]
+            elif fn == "qk_norm_rope":
+                r = [qk_norm_rope(x[0], x[1], x[2], x[3], int(p["heads"]), int(p["kv_heads"]),
+                                  int(p["head_dim"]), p.get("theta", 1e6), p.get("eps", 1e-6)).astype(np.float32)]
+            elif fn == "moe_topk":
+                lg = round_bf16(x[0]) if tmeta[o["inputs"][0]].get("dtype") == "bf16" else x[0]
+                r = list(moe_topk(lg, int(p.get("topk", 8)), bool(p.get("renorm", 1))))
+            elif fn == "moe_dispatch":
+                r = list(moe_dispatch(x[0], x[1], int(p.get("experts", 128))))
+            elif fn in ("moe_gate_up", "moe_down"):
+                r = [moe_experts(x[0], x[1], x[2], int(p.get("experts", 128)), fn == "moe_gate_up")]
+            elif fn == "moe_combine":
+                r = [moe_combine(x[0], x[1], x[2])]
             elif fn == "attn_decode":
                 r = [attn_decode(x[0], x[1], x[2], x[3], x[4], int(p["heads"]), int(p["kv_heads"]),
                                  int(p["head_dim"]), int(p.get("page_size", 16)))]

@@ -1,5 +1,7 @@
 #include "opflow/builders.hpp"
 
+#include <map>
+
 #include "opflow/json.hpp"
 
 namespace opflow::builders {
@@ -120,6 +122,8 @@ GraphDescription llama_graph(const LlamaShape& s) {
           Errc::ConfigError, "llama: tp must divide heads, kv_heads and inter");
   require(s.decode || s.tokens % s.seq_len == 0, Errc::ConfigError,
           "llama: tokens must be a multiple of seq_len");
+  require(s.experts == 0 || (s.tp == 1 && s.topk >= 1 && s.topk <= s.experts), Errc::ConfigError,
+          "moe: experts need tp == 1 and 1 <= topk <= experts");
   DescWriter w(s.dtype);
   const int64_t T = s.tokens, H = s.hidden, hd = s.head_dim;
   const int64_t nq = s.heads / s.tp, nkv = s.kv_heads / s.tp, I = s.inter / s.tp;
@@ -153,8 +157,11 @@ GraphDescription llama_graph(const LlamaShape& s) {
     const std::string wqkv = w.weight(p + ".qkv.w", {H, nqkv});
     const std::string wo = w.weight(p + ".o.w", {nq * hd, H});
     const std::string g2 = w.weight(p + ".mlp_norm.w", {H});
-    const std::string wgu = w.weight(p + ".gate_up.w", {H, 2 * I});
-    const std::string wd = w.weight(p + ".down.w", {I, H});
+    const bool moe = s.experts > 0;
+    const int64_t E = s.experts, K = s.topk, MI = s.moe_inter;
+    const std::string wgu = moe ? w.weight(p + ".experts.gate_up.w", {E, H, 2 * MI})
+                                : w.weight(p + ".gate_up.w", {H, 2 * I});
+    const std::string wd = moe ? w.weight(p + ".experts.down.w", {E, MI, H}) : w.weight(p + ".down.w", {I, H});
     if (s.decode) {
       const int64_t pages = s.num_pages ? s.num_pages : T * max_pages;
       kc = w.weight(p + ".k_cache", {pages, s.page_size, nkv, hd});
@@ -166,16 +173,22 @@ GraphDescription llama_graph(const LlamaShape& s) {
     const std::string o = w.act(p + ".o", {T, H});
     const std::string x1 = w.act(p + ".x1", {T, H});
     const std::string h2 = w.act(p + ".h2", {T, H});
-    const std::string gu = w.act(p + ".gu", {T, 2 * I});
-    const std::string a = w.act(p + ".act", {T, I});
     const std::string dn = w.act(p + ".down_out", {T, H});
 
     w.op(p + ".qkv_proj", OperatorKind::kMatMul, {h1, wqkv}, {qkv}, p + ".attn.qkv",
          gemm_cost(H, nqkv));
-    w.custom(p + ".rope", "rope", {qkv, pos}, {qkvr}, p + ".attn.rope", ResourceClass::kMemory,
-             mem_cost)
-        .attrs.params = {{"heads", double(nq)}, {"kv_heads", double(nkv)},
-                         {"head_dim", double(hd)}, {"theta", s.theta}};
+    if (s.qk_norm) {
+      w.custom(p + ".rope", "qk_norm_rope",
+               {qkv, pos, w.weight(p + ".q_norm.w", {hd}), w.weight(p + ".k_norm.w", {hd})}, {qkvr},
+               p + ".attn.rope", ResourceClass::kMemory, mem_cost)
+          .attrs.params = {{"heads", double(nq)}, {"kv_heads", double(nkv)}, {"head_dim", double(hd)},
+                           {"theta", s.theta}, {"eps", s.eps}};
+    } else {
+      w.custom(p + ".rope", "rope", {qkv, pos}, {qkvr}, p + ".attn.rope", ResourceClass::kMemory,
+               mem_cost)
+          .attrs.params = {{"heads", double(nq)}, {"kv_heads", double(nkv)},
+                           {"head_dim", double(hd)}, {"theta", s.theta}};
+    }
     if (s.decode) {
       w.custom(p + ".attn", "attn_decode", {qkvr, kc, vc, table, pos}, {ctx}, p + ".attn.core",
                ResourceClass::kMemory, mem_cost)
@@ -199,10 +212,50 @@ GraphDescription llama_graph(const LlamaShape& s) {
     w.custom(p + ".attn_resid_norm", "add_rmsnorm", {x, o_in, g2}, {x1, h2}, p + ".attn.resid",
              ResourceClass::kMemory, mem_cost)
         .attrs.params = {{"eps", s.eps}};
-    w.op(p + ".gate_up", OperatorKind::kMatMul, {h2, wgu}, {gu}, p + ".mlp.gate_up",
-         gemm_cost(H, 2 * I));
-    w.custom(p + ".act", "silu_mul", {gu}, {a}, p + ".mlp.act", ResourceClass::kMemory, mem_cost);
-    w.op(p + ".down", OperatorKind::kMatMul, {a, wd}, {dn}, p + ".mlp.down", gemm_cost(I, H));
+    if (moe) {
+      // Qwen3 MoE FFN: router GEMM -> top-k -> dispatch (EP all-to-all site)
+      // -> grouped expert GEMMs -> combine (EP all-to-all site)
+      const std::string logits = w.act(p + ".router_logits", {T, E});
+      const std::string ids = w.tensor(p + ".topk_ids", {T, K}, BatchSemantics::kBatched,
+                                       TensorRole::kIntermediate, Dtype::kI64);
+      const std::string wts = w.tensor(p + ".topk_w", {T, K}, BatchSemantics::kBatched,
+                                       TensorRole::kIntermediate, Dtype::kF32);
+      const std::string xd = w.act(p + ".dispatched", {T, K * H});
+      const std::string slot = w.tensor(p + ".slot", {T, K}, BatchSemantics::kBatched,
+                                        TensorRole::kIntermediate, Dtype::kI64);
+      const std::string hd_ = w.act(p + ".expert_act", {T, K * MI});
+      const std::string yd = w.act(p + ".expert_out", {T, K * H});
+      const std::vector<std::pair<std::string, double>> mp = {{"experts", double(E)}, {"topk", double(K)}};
+      auto params = [&](std::initializer_list<std::pair<const std::string, double>> extra) {
+        std::map<std::string, double> m(mp.begin(), mp.end());
+        for (const auto& kv : extra) m[kv.first] = kv.second;
+        return m;
+      };
+      w.op(p + ".router", OperatorKind::kMatMul, {h2, w.weight(p + ".router.w", {H, E})}, {logits},
+           p + ".moe.router", gemm_cost(H, E));
+      w.custom(p + ".topk", "moe_topk", {logits}, {ids, wts}, p + ".moe.topk", ResourceClass::kMemory,
+               CostParams{2.0, E * 2.0 / 6.5e6})
+          .attrs.params = params({{"renorm", 1.0}});
+      w.custom(p + ".dispatch", "moe_dispatch", {h2, ids}, {xd, slot}, p + ".moe.dispatch",
+               ResourceClass::kNetwork, CostParams{5.0, K * H * 4.0 / 6.5e6})
+          .attrs.params = params({});
+      w.custom(p + ".experts_gate_up", "moe_gate_up", {xd, ids, wgu}, {hd_}, p + ".moe.experts",
+               ResourceClass::kCompute, CostParams{2.0, K * 2.0 * H * 2 * MI / 1.4e9})
+          .attrs.params = params({});
+      w.custom(p + ".experts_down", "moe_down", {hd_, ids, wd}, {yd}, p + ".moe.experts",
+               ResourceClass::kCompute, CostParams{2.0, K * 2.0 * MI * H / 1.4e9})
+          .attrs.params = params({});
+      w.custom(p + ".combine", "moe_combine", {yd, slot, wts}, {dn}, p + ".moe.combine",
+               ResourceClass::kNetwork, CostParams{5.0, K * H * 2.0 / 6.5e6})
+          .attrs.params = params({});
+    } else {
+      const std::string gu = w.act(p + ".gu", {T, 2 * I});
+      const std::string a = w.act(p + ".act", {T, I});
+      w.op(p + ".gate_up", OperatorKind::kMatMul, {h2, wgu}, {gu}, p + ".mlp.gate_up",
+           gemm_cost(H, 2 * I));
+      w.custom(p + ".act", "silu_mul", {gu}, {a}, p + ".mlp.act", ResourceClass::kMemory, mem_cost);
+      w.op(p + ".down", OperatorKind::kMatMul, {a, wd}, {dn}, p + ".mlp.down", gemm_cost(I, H));
+    }
     std::string d_in = dn;
     if (s.tp > 1) {
       d_in = w.act(p + ".down_ar", {T, H});
@@ -273,8 +326,22 @@ std::string build_json(const std::string& name, const std::string& params_json) 
                                              : fuse_chain_graph(layers, B, H, k, dt);
     return description_to_json(d);
   }
-  if (name == "llama" || name == "llama_decode" || name == "toy_decoder") {
+  if (name == "llama" || name == "llama_decode" || name == "toy_decoder" || name == "qwen3_moe") {
     LlamaShape s;
+    if (name == "qwen3_moe") {  // BASELINE.json configs[4]: Qwen3-30B-A3B-shaped layer
+      s.layers = 1;
+      s.hidden = 2048;
+      s.heads = 32;
+      s.kv_heads = 4;
+      s.head_dim = 128;
+      s.inter = 6144;
+      s.eps = 1e-6;
+      s.theta = 1000000.0;
+      s.qk_norm = true;
+      s.experts = 128;
+      s.topk = 8;
+      s.moe_inter = 768;
+    }
     if (name == "toy_decoder") {  // BASELINE.json configs[0]
       s.layers = 2;
       s.tokens = 8 * 128;
@@ -305,6 +372,10 @@ std::string build_json(const std::string& name, const std::string& params_json) 
     s.ctx_len = geti(p, "ctx_len", s.ctx_len);
     s.page_size = geti(p, "page_size", s.page_size);
     s.num_pages = geti(p, "num_pages", s.num_pages);
+    s.experts = geti(p, "experts", s.experts);
+    s.topk = geti(p, "topk", s.topk);
+    s.moe_inter = geti(p, "moe_inter", s.moe_inter);
+    s.qk_norm = geti(p, "qk_norm", s.qk_norm ? 1 : 0) != 0;
     if (dtv) s.dtype = dt;
     return description_to_json(llama_graph(s));
   }

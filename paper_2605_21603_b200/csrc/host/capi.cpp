@@ -64,6 +64,21 @@ void need(const void* p, const char* what) {
   if (!p) fail(Errc::ConfigError, std::string("null ") + what);
 }
 
+// Direct (session-less) launch of a registered op: allocate its workspace
+// stream-ordered for this one call (a Session plans it inside the arena instead).
+opf_status call_with_workspace(const OpEntry& e, opf_op_ctx& c, const opf_view* in, int32_t n_in,
+                               opf_view* out, int32_t n_out, int64_t rows, cudaStream_t s) {
+  const size_t bytes = e.workspace ? e.workspace(c, in, n_in, out, n_out, rows) : 0;
+  if (bytes == 0) return e.fn(&c, in, n_in, out, n_out, rows, s);
+  void* ws = nullptr;
+  OPF_CUDA(cudaMallocAsync(&ws, bytes, s));
+  c.workspace = ws;
+  c.workspace_bytes = bytes;
+  const opf_status st = e.fn(&c, in, n_in, out, n_out, rows, s);
+  OPF_CUDA(cudaFreeAsync(ws, s));
+  return st;
+}
+
 SessionConfig parse_config(const char* text) {
   SessionConfig c;
   if (!text || !*text) return c;
@@ -238,7 +253,7 @@ opf_status opf_launch(const char* op_json, const opf_view* in, int32_t n_in, opf
       const OpEntry* e = OpRegistry::global().find(od.attrs.custom_name);
       require(e != nullptr, Errc::ConfigError,
               "no custom function registered for '" + od.attrs.custom_name + "'");
-      st = e->fn(&c, in, n_in, out, n_out, rows, s);
+      st = call_with_workspace(*e, c, in, n_in, out, n_out, rows, s);
     } else {
       st = launch_kind(c, in, n_in, out, n_out, rows, s);
     }
@@ -276,7 +291,7 @@ opf_status opf_launch_comm(const char* op_json, const opf_view* in, int32_t n_in
       const OpEntry* e = OpRegistry::global().find(od.attrs.custom_name);
       require(e != nullptr, Errc::ConfigError,
               "no custom function registered for '" + od.attrs.custom_name + "'");
-      st = e->fn(&c, in, n_in, out, n_out, rows, s);
+      st = call_with_workspace(*e, c, in, n_in, out, n_out, rows, s);
     } else {
       st = launch_kind(c, in, n_in, out, n_out, rows, s);
     }

@@ -192,9 +192,20 @@ void Session::ensure_packed_for(const CompiledPlan& cp, cudaStream_t s) {
       std::vector<void*>& slot = l.prepack_mode == 1 ? prepacked_act_ : prepacked_;
       if (slot[w]) continue;
       OPF_CUDA(cudaMalloc(&slot[w], m.numel() * 2));
-      if (l.prepack_mode == 1)
+      if (l.prepack_mode == 1) {
         k_pack_gate_up(view_ptr(ext_[w]), slot[w], m.shape[0], m.shape[1] / 2, s);
-      else
+      } else if (l.prepack_mode == 2 || l.prepack_mode == 3) {  // per-expert [E,K,N]
+        require(m.shape.size() == 3, Errc::ShapeMismatch, "expert weight '" + m.name + "' must be [E,K,N]");
+        const int64_t E = m.shape[0], K = m.shape[1], N = m.shape[2];
+        const char* src = static_cast<const char*>(view_ptr(ext_[w]));
+        char* dst = static_cast<char*>(slot[w]);
+        for (int64_t e = 0; e < E; ++e) {
+          if (l.prepack_mode == 2)
+            k_pack_gate_up(src + e * K * N * 2, dst + e * K * N * 2, K, N / 2, s);
+          else
+            k_transpose_bf16(src + e * K * N * 2, dst + e * K * N * 2, K, N, s);
+        }
+      } else
         k_transpose_bf16(view_ptr(ext_[w]), slot[w], m.shape[0], m.shape[1], s);
     }
   OPF_CUDA(cudaGetLastError());
@@ -544,9 +555,16 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
         if (node.kind == OperatorKind::kMatMul && g_.tensors[node.inputs[1]].dtype == Dtype::kBF16 &&
             g_.tensors[node.inputs[1]].role == TensorRole::kWeight)
           l.prepacked = node.inputs[1];  // aux = [N,K] copy, resolved at launch
-        if (node.kind == OperatorKind::kCustom)
-          require(OpRegistry::global().find(node.attrs.custom_name) != nullptr, Errc::ConfigError,
+        if (node.kind == OperatorKind::kCustom) {
+          const OpEntry* e = OpRegistry::global().find(node.attrs.custom_name);
+          require(e != nullptr, Errc::ConfigError,
                   "no device op registered for '" + node.attrs.custom_name + "'");
+          if (e->prepack_input >= 0 && e->prepack_input < static_cast<int>(node.inputs.size()) &&
+              g_.tensors[node.inputs[e->prepack_input]].role == TensorRole::kWeight) {
+            l.prepacked = node.inputs[e->prepack_input];
+            l.prepack_mode = e->prepack_mode;
+          }
+        }
         pd.launches.push_back(std::move(l));
       }
     }

@@ -52,6 +52,7 @@ OpRegistry::OpRegistry() {
   register_llama_ops(*this);
   register_attention_ops(*this);
   register_comm_ops(*this);
+  register_moe_ops(*this);
 }
 
 OpRegistry& OpRegistry::global() {

@@ -47,6 +47,11 @@ struct LlamaShape {
   int64_t ctx_len = 4096;    // cached context per sequence
   int64_t page_size = 16;
   int64_t num_pages = 0;     // 0 = tokens * ctx_len / page_size
+  // Qwen3 options: per-head q/k RMSNorm before RoPE; MoE FFN when experts > 0
+  bool qk_norm = false;
+  int64_t experts = 0;
+  int64_t topk = 8;
+  int64_t moe_inter = 768;
 };
 
 GraphDescription llama_graph(const LlamaShape& s);

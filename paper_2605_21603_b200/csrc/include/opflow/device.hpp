@@ -39,6 +39,11 @@ struct OpEntry {
   int n_in = -1;   // -1: any arity
   int n_out = -1;
   WorkspaceFn workspace;
+  // weight input packed once per binding by the session (ctx.aux = packed copy):
+  // mode 2 = per-expert gate|up pack ([E,K,2I] -> [E,2I,K] interleaved),
+  // mode 3 = per-expert transpose ([E,K,N] -> [E,N,K])
+  int prepack_input = -1;
+  int prepack_mode = 0;
 };
 
 class OpRegistry {
@@ -97,6 +102,7 @@ void register_norm_ops(OpRegistry& r);
 void register_llama_ops(OpRegistry& r);
 void register_attention_ops(OpRegistry& r);
 void register_comm_ops(OpRegistry& r);
+void register_moe_ops(OpRegistry& r);
 
 // ---- kernel launchers used across translation units -------------------------------
 // Stand-in kinds (bit-exact with the reference kernels for i64 / f32).
@@ -122,6 +128,10 @@ struct GemmArgs {
   int epi;         // 0 plain; 1 SiLU-mul (Bt packed by k_pack_gate_up, C is [M, N/2])
 };
 void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s);
+// Grouped per-expert GEMM (MoE): gtab = device tile table [n, (row0, row_end, expert) x n],
+// bt = [n_groups * group_n, K]; g.m bounds the rows of a / c, g.n is unused.
+void gemm_bf16_grouped(const GemmArgs& g, const int32_t* gtab, int64_t max_mtiles, int64_t group_n,
+                       int64_t n_groups, cudaStream_t s);
 void k_pack_gate_up(const void* src, void* dst, int64_t K, int64_t I, cudaStream_t s);
 // Reference CUDA-core GEMM (bf16 in, fp32 accumulate) used by tests as a
 // numerics cross-check of the tcgen05 path.

@@ -242,10 +242,57 @@ __device__ __forceinline__ void store_tile(const CUtensorMap* map_c, uint32_t tm
   }
 }
 
+// Grouped (MoE) epilogue: expert segments are not tile-aligned, so rows past
+// the segment end belong to the next expert's tile and must not be written;
+// each lane stores its own row (512 B contiguous per chunk pair) when valid.
 template <int EPI>
+__device__ __forceinline__ void store_tile_direct(uint32_t tmem_col0, __nv_bfloat16* __restrict__ c,
+                                                  int64_t ldc, int64_t row, int64_t row_end, int64_t nb) {
+  constexpr int kChunks = EPI == 1 ? 2 : BN / 64;
+#pragma unroll 1
+  for (int chunk = 0; chunk < kChunks; ++chunk) {
+    uint32_t v0[32], v1[32];
+    const uint32_t taddr = tmem_col0 + static_cast<uint32_t>(chunk * 64);
+    tmem_ld32(taddr, v0);
+    tmem_ld32(taddr + 32, v1);
+    if constexpr (EPI == 1) {
+      uint32_t u0[32], u1[32];
+      tmem_ld32(taddr + 128, u0);
+      tmem_ld32(taddr + 160, u1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float g0 = __uint_as_float(v0[i]), g1 = __uint_as_float(v1[i]);
+        v0[i] = __float_as_uint(g0 / (1.0f + __expf(-g0)) * __uint_as_float(u0[i]));
+        v1[i] = __float_as_uint(g1 / (1.0f + __expf(-g1)) * __uint_as_float(u1[i]));
+      }
+    } else {
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    }
+    if (row < row_end) {
+      const int64_t col = EPI == 1 ? nb * (BN / 2) + chunk * 64 : nb * BN + chunk * 64;
+      uint4* dst = reinterpret_cast<uint4*>(c + row * ldc + col);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t* src = j < 4 ? &v0[8 * j] : &v1[8 * (j - 4)];
+        uint4 q;
+        q.x = pack_bf16(src[0], src[1]);
+        q.y = pack_bf16(src[2], src[3]);
+        q.z = pack_bf16(src[4], src[5]);
+        q.w = pack_bf16(src[6], src[7]);
+        dst[j] = q;
+      }
+    }
+  }
+}
+
+template <int EPI, bool GROUPED = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K) {
+                   const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K,
+                   const int32_t* __restrict__ gtab, __nv_bfloat16* __restrict__ c_out, int64_t ldc) {
+  // GROUPED: gtab = [n_tiles, (row0, row_end, expert) x n_tiles]; N is the per-expert
+  // width, expert e's B rows start at e * N; M bounds the A rows.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;
@@ -258,8 +305,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAccStages);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t m_blocks = (M + BM - 1) / BM, n_blocks = (N + BN - 1) / BN;
-  const int64_t tiles = m_blocks * n_blocks;
+  int64_t m_blocks = (M + BM - 1) / BM;
+  const int64_t n_blocks = (N + BN - 1) / BN;
   const int k_blocks = static_cast<int>((K + BK - 1) / BK);
 
   if (warp == 0) {
@@ -289,6 +336,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();
   pdl_trigger();
+  if constexpr (GROUPED) m_blocks = *reinterpret_cast<const volatile int32_t*>(gtab);  // written by the routing kernel
+  const int64_t tiles = m_blocks * n_blocks;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -297,12 +346,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         int64_t mb, nb;
         tile_coords(t, m_blocks, n_blocks, mb, nb);
+        int32_t a_row = static_cast<int32_t>(mb * BM), b_row = static_cast<int32_t>(nb * BN);
+        if constexpr (GROUPED) {
+          a_row = gtab[1 + 3 * mb];
+          b_row += static_cast<int32_t>(gtab[3 + 3 * mb] * N);
+        }
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = stage_base + stage * kStageBytes;
           mbar_expect_tx(&full[stage], kStageBytes);
-          tma_load_2d(sa, &map_a, &full[stage], kb * BK, static_cast<int32_t>(mb * BM));
-          tma_load_2d(sa + kABytes, &map_b, &full[stage], kb * BK, static_cast<int32_t>(nb * BN));
+          tma_load_2d(sa, &map_a, &full[stage], kb * BK, a_row);
+          tma_load_2d(sa + kABytes, &map_b, &full[stage], kb * BK, b_row);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -354,11 +408,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_coords(t, m_blocks, n_blocks, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int64_t row0 = mb * BM + quarter * 32;
-      store_tile<EPI>(&map_c,
-                      tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                          static_cast<uint32_t>(acc * BN),
-                      stg, buf, lane, nb, row0, M);
+      const uint32_t tcol = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN);
+      if constexpr (GROUPED) {
+        store_tile_direct<EPI>(tcol, c_out, ldc, gtab[1 + 3 * mb] + quarter * 32 + lane, gtab[2 + 3 * mb], nb);
+      } else {
+        store_tile<EPI>(&map_c, tcol, stg, buf, lane, nb, mb * BM + quarter * 32, M);
+      }
       // accumulator fully read: hand it back to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -602,6 +657,24 @@ CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld_
 
 }  // namespace
 
+void gemm_bf16_tc_init() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBytes2)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBytes2)));
+  });
+}
+
 void gemm_bf16_simt(const GemmArgs& g, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>((g.n + 63) / 64), static_cast<unsigned>((g.m + 63) / 64));
   gemm_simt_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(g.a),
@@ -618,17 +691,7 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
           Errc::ShapeMismatch, "tcgen05 GEMM needs 16-byte aligned base pointers");
   require(g.epi == 0 || g.n % BN == 0, Errc::ShapeMismatch,
           "SiLU-mul epilogue needs N (= 2 x inter) to be a multiple of 256");
-  static std::once_flag once;
-  std::call_once(once, [] {
-    OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSmemBytes)));
-    OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSmemBytes)));
-    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSmemBytes2)));
-    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSmemBytes2)));
-  });
+  gemm_bf16_tc_init();
   static const int mode = [] {  // OPF_GEMM=1sm|2sm|auto
     const char* e = std::getenv("OPF_GEMM");
     if (e && std::string(e) == "1sm") return 1;
@@ -657,9 +720,35 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
   const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN);
   if (tiles < grid) grid = static_cast<int>(tiles);
   if (g.epi == 1)
-    launch_pdl(gemm_tc_kernel<1>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, g.n, g.k);
+    launch_pdl(gemm_tc_kernel<1>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, g.n, g.k,
+               static_cast<const int32_t*>(nullptr), static_cast<__nv_bfloat16*>(nullptr), int64_t{0});
   else
-    launch_pdl(gemm_tc_kernel<0>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, g.n, g.k);
+    launch_pdl(gemm_tc_kernel<0>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, g.n, g.k,
+               static_cast<const int32_t*>(nullptr), static_cast<__nv_bfloat16*>(nullptr), int64_t{0});
+}
+
+// Grouped (per-expert) GEMM: rows of `a` are expert-sorted segments, gtab the
+// device tile table built by the routing kernel, bt = [E * group_n, K] packed
+// expert weights.  max_mtiles bounds the tile count (grid sizing happens on the
+// host; the actual count is read on the device, so the launch is capturable).
+void gemm_bf16_grouped(const GemmArgs& g, const int32_t* gtab, int64_t max_mtiles, int64_t group_n,
+                       int64_t n_groups, cudaStream_t s) {
+  require(g.k % 8 == 0 && g.lda % 8 == 0 && g.ldc % 8 == 0 && group_n % BN == 0, Errc::ShapeMismatch,
+          "grouped GEMM needs K, lda, ldc multiples of 8 and a per-expert N multiple of 256");
+  gemm_bf16_tc_init();
+  const CUtensorMap ma = make_map(g.a, g.k, g.m, g.lda, BK, BM);
+  const CUtensorMap mb = make_map(g.bt, g.k, group_n * n_groups, g.k, BK, BN);
+  int grid = num_sms();
+  if (g.max_ctas > 0 && g.max_ctas < grid) grid = g.max_ctas;
+  const int64_t tiles = max_mtiles * (group_n / BN);
+  if (tiles < grid) grid = static_cast<int>(std::max<int64_t>(tiles, 1));
+  auto* c = static_cast<__nv_bfloat16*>(g.c);
+  if (g.epi == 1)
+    launch_pdl(gemm_tc_kernel<1, true>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, ma, g.m, group_n, g.k,
+               gtab, c, g.ldc);
+  else
+    launch_pdl(gemm_tc_kernel<0, true>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, ma, g.m, group_n, g.k,
+               gtab, c, g.ldc);
 }
 
 // [K, 2I] gate|up weight -> K-major [2I, K] with gate/up interleaved in 128-row

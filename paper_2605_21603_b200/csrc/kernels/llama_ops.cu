@@ -156,6 +156,66 @@ __global__ void __launch_bounds__(256) rope_kernel(const T* __restrict__ qkv,
   }
 }
 
+// Qwen3 attention prologue: per-head RMSNorm of every q and k head (weights
+// q_norm / k_norm, [hd]) followed by rotate-half RoPE; v heads copied.  One
+// warp per head (hd = 128: 4 elements per lane, rotate-half partner = lane ^ 16).
+__global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv,
+                                                           const int64_t* __restrict__ pos,
+                                                           const __nv_bfloat16* __restrict__ qn,
+                                                           const __nv_bfloat16* __restrict__ kn,
+                                                           __nv_bfloat16* __restrict__ out, int nq, int nkv,
+                                                           float log2_theta, float eps) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int HD = 128;
+  const int64_t row = blockIdx.x;
+  const int64_t W = static_cast<int64_t>(nq + 2 * nkv) * HD;
+  const __nv_bfloat16* in = qkv + row * W;
+  __nv_bfloat16* o = out + row * W;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const float p = static_cast<float>(pos[row]);
+  const int i0 = lane * 4;
+  for (int h = warp; h < nq + nkv; h += blockDim.x / 32) {
+    const uint2 u = *reinterpret_cast<const uint2*>(in + h * HD + i0);
+    const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+    const uint2 gu = *reinterpret_cast<const uint2*>((h < nq ? qn : kn) + i0);
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gu);
+    float x[4], g[4];
+    for (int k = 0; k < 2; ++k) {
+      const float2 a = __bfloat1622float2(x2[k]), b = __bfloat1622float2(g2[k]);
+      x[2 * k] = a.x;
+      x[2 * k + 1] = a.y;
+      g[2 * k] = b.x;
+      g[2 * k + 1] = b.y;
+    }
+    float ss = x[0] * x[0] + x[1] * x[1] + x[2] * x[2] + x[3] * x[3];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    const float inv = rsqrtf(ss / HD + eps);
+    float y[4], r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) y[k] = x[k] * inv * g[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float partner = __shfl_xor_sync(0xffffffffu, y[k], 16);
+      const int j = (i0 + k) % (HD / 2);
+      const float inv_freq = exp2f(-2.0f * static_cast<float>(j) / HD * log2_theta);
+      float sn, cs;
+      sincosf(p * inv_freq, &sn, &cs);
+      r[k] = lane < 16 ? y[k] * cs - partner * sn : y[k] * cs + partner * sn;
+    }
+    uint2 w;
+    __nv_bfloat162* w2 = reinterpret_cast<__nv_bfloat162*>(&w);
+    w2[0] = __floats2bfloat162_rn(r[0], r[1]);
+    w2[1] = __floats2bfloat162_rn(r[2], r[3]);
+    *reinterpret_cast<uint2*>(o + h * HD + i0) = w;
+  }
+  // v heads: straight copy
+  const int64_t v0 = static_cast<int64_t>(nq + nkv) * HD;
+  for (int64_t c = threadIdx.x * 8; c < static_cast<int64_t>(nkv) * HD; c += blockDim.x * 8)
+    *reinterpret_cast<uint4*>(o + v0 + c) = *reinterpret_cast<const uint4*>(in + v0 + c);
+}
+
 template <typename T>
 __global__ void silu_mul_kernel(const T* __restrict__ gu, T* __restrict__ out, int64_t rows,
                                 int64_t I) {
@@ -268,6 +328,28 @@ opf_status op_silu_mul(const opf_op_ctx*, const opf_view* in, int32_t n_in, opf_
   return launch_status("silu_mul");
 }
 
+opf_status op_qk_norm_rope(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out,
+                           int32_t n_out, int64_t rows, void* stream) {
+  if (n_in != 4 || n_out != 1)
+    return op_error(Errc::ShapeMismatch, "qk_norm_rope takes (qkv, pos, q_norm, k_norm) -> qkv");
+  const int nq = static_cast<int>(ctx_param(*c, "heads", 1));
+  const int nkv = static_cast<int>(ctx_param(*c, "kv_heads", 1));
+  const int hd = static_cast<int>(ctx_param(*c, "head_dim", 128));
+  const float l2t = static_cast<float>(std::log2(ctx_param(*c, "theta", 1000000.0)));
+  const float eps = static_cast<float>(ctx_param(*c, "eps", 1e-6));
+  if (hd != 128 || in[0].dtype != OPF_BF16 || view_row_elems(in[0]) != static_cast<int64_t>(nq + 2 * nkv) * hd ||
+      view_numel(in[2]) != hd || view_numel(in[3]) != hd)
+    return op_error(Errc::ShapeMismatch, "qk_norm_rope: bf16, head_dim 128, norm weights [head_dim]");
+  if (rows == 0) return 0;
+  launch_pdl(qk_norm_rope_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), 0, static_cast<cudaStream_t>(stream),
+             static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[0])),
+             static_cast<const int64_t*>(vptr<int64_t>(in[1])),
+             static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[2])),
+             static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[3])), vptr<__nv_bfloat16>(out[0]), nq, nkv,
+             l2t, eps);
+  return launch_status("qk_norm_rope");
+}
+
 }  // namespace
 
 void register_llama_ops(OpRegistry& r) {
@@ -275,6 +357,7 @@ void register_llama_ops(OpRegistry& r) {
   r.add({"add_rmsnorm", op_add_rmsnorm, ResourceClass::kMemory, 3, 2, {}});
   r.add({"rope", op_rope, ResourceClass::kMemory, 2, 1, {}});
   r.add({"silu_mul", op_silu_mul, ResourceClass::kMemory, 1, 1, {}});
+  r.add({"qk_norm_rope", op_qk_norm_rope, ResourceClass::kMemory, 4, 1, {}});
 }
 
 }  // namespace opflow

@@ -1,0 +1,407 @@
+// Mixture-of-experts operators (Qwen3-30B-A3B-shaped MoE layer).
+//
+// Graph-level decomposition (one Custom op each, so strategies can place the
+// dispatch/combine — the expert-parallel all-to-all sites — on the network lane
+// and overlap them with the other micro-batch's expert GEMMs, DBO-style):
+//
+//   logits [T,E] = MatMul(x_norm, W_router)                  (tcgen05 GEMM)
+//   moe_topk     logits -> ids [T,k] (i64), w [T,k] (f32)     top-k by (value desc,
+//                index asc); w = softmax over the k selected logits (renorm=1, Qwen3
+//                norm_topk_prob) or the full-softmax probabilities (renorm=0)
+//   moe_dispatch x [T,H], ids -> xd [T, k*H] (= [T*k, H] rows sorted by expert,
+//                stable in (token, j) order), slot [T,k] (i64 row of (t,j) in xd)
+//   moe_gate_up  xd, ids, W_gu [E,H,2I] -> hd [T, k*I]       grouped tcgen05 GEMM,
+//                SiLU-mul fused in the epilogue
+//   moe_down     hd, ids, W_d [E,I,H] -> yd [T, k*H]         grouped tcgen05 GEMM
+//   moe_combine  yd, slot, w -> y [T,H] = sum_j w[t,j] * yd[slot[t,j]]  (j ascending)
+//
+// Routing is a stable counting sort over the T*k (token, j) slots: per-chunk
+// expert histograms, one scan CTA, then one warp per chunk ranks equal experts
+// with __match_any_sync so positions follow slot order — bit-identical to a
+// stable argsort (the oracle's restatement).  Ids outside [0,E) are dropped
+// (slot = -1, no contribution).  All index work is exact; the grouped GEMM's
+// tile table (row0, row_end, expert per 128-row tile) is rebuilt on the device
+// by each GEMM op from `ids`, so every launch is graph-capturable (no host sync).
+#include <cuda_bf16.h>
+
+#include <cfloat>
+
+#include "opflow/device.hpp"
+
+namespace opflow {
+
+namespace {
+
+constexpr int kChunk = 1024;  // slots per routing chunk
+constexpr int kMaxE = 1024;
+
+__device__ __forceinline__ bool valid_id(int64_t e, int E) { return e >= 0 && e < E; }
+
+// ---------------------------------------------------------------- top-k
+template <typename T>
+__device__ __forceinline__ float ldf(const T* p);
+template <>
+__device__ __forceinline__ float ldf<float>(const float* p) { return *p; }
+template <>
+__device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+// One warp per token; lane l holds logits l, l+32, ...  k rounds of a warp
+// argmax with (value desc, index asc) ordering.
+template <typename T, int PER>
+__global__ void __launch_bounds__(256) topk_kernel(const T* __restrict__ logits, int64_t* __restrict__ ids,
+                                                   float* __restrict__ w, int64_t rows, int E, int k,
+                                                   int renorm) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (t >= rows) return;
+  float v[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int e = lane + 32 * i;
+    v[i] = e < E ? ldf<T>(logits + t * E + e) : -FLT_MAX;
+  }
+  float vmax = -FLT_MAX;
+  float sel[32];
+  int64_t* out_ids = ids + t * k;
+  for (int j = 0; j < k; ++j) {
+    float bv = -FLT_MAX;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E && (v[i] > bv || (v[i] == bv && e < bi))) {
+        bv = v[i];
+        bi = e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i)  // remove the winner (owner lane)
+      if (lane + 32 * i == bi) v[i] = -INFINITY;
+    if (j == 0) vmax = bv;
+    sel[j & 31] = bv;
+    if (lane == 0) out_ids[j] = bi;
+  }
+  float denom = 0.0f;
+  if (renorm) {
+    for (int j = 0; j < k; ++j) denom += __expf(sel[j & 31] - vmax);
+  } else {  // full softmax over all E logits (restore the removed values first)
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E) denom += __expf(ldf<T>(logits + t * E + e) - vmax);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, o);
+  }
+  if (lane == 0)
+    for (int j = 0; j < k; ++j) w[t * k + j] = __expf(sel[j & 31] - vmax) / denom;
+}
+
+// ---------------------------------------------------------------- routing
+// per-chunk expert histograms: cnt[c * E + e]
+__global__ void __launch_bounds__(256) route_hist_kernel(const int64_t* __restrict__ ids, int64_t n, int E,
+                                                         int32_t* __restrict__ cnt) {
+  pdl_wait();
+  __shared__ int32_t h[kMaxE];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) h[e] = 0;
+  __syncthreads();
+  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kChunk;
+  for (int i = threadIdx.x; i < kChunk && s0 + i < n; i += blockDim.x) {
+    const int64_t e = ids[s0 + i];
+    if (valid_id(e, E)) atomicAdd(&h[e], 1);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[static_cast<int64_t>(blockIdx.x) * E + e] = h[e];
+  pdl_trigger();
+}
+
+// One CTA: base[c][e] = off[e] + sum_{c' < c} cnt[c'][e]  (in place over cnt),
+// and (optionally) the grouped-GEMM tile table.
+__global__ void __launch_bounds__(1024) route_scan_kernel(int32_t* __restrict__ cnt, int chunks, int E,
+                                                          int32_t* __restrict__ gtab, int tile_m) {
+  pdl_wait();
+  __shared__ int32_t tot[kMaxE], off[kMaxE + 1], toff[kMaxE + 1];
+  const int e = threadIdx.x;
+  int32_t run = 0;
+  if (e < E)
+    for (int c = 0; c < chunks; ++c) {
+      const int32_t v = cnt[static_cast<int64_t>(c) * E + e];
+      cnt[static_cast<int64_t>(c) * E + e] = run;
+      run += v;
+    }
+  if (e < E) tot[e] = run;
+  __syncthreads();
+  if (e == 0) {
+    int32_t a = 0, b = 0;
+    for (int i = 0; i < E; ++i) {
+      off[i] = a;
+      toff[i] = b;
+      a += tot[i];
+      b += (tot[i] + tile_m - 1) / tile_m;
+    }
+    off[E] = a;
+    toff[E] = b;
+    if (gtab) gtab[0] = b;
+  }
+  __syncthreads();
+  if (e < E) {
+    const int32_t o = off[e];
+    for (int c = 0; c < chunks; ++c) cnt[static_cast<int64_t>(c) * E + e] += o;
+    if (gtab) {
+      const int32_t end = o + tot[e];
+      int32_t* g = gtab + 1 + 3 * toff[e];
+      for (int32_t r = o, i = 0; r < end; r += tile_m, ++i) {
+        g[3 * i] = r;
+        g[3 * i + 1] = end;
+        g[3 * i + 2] = e;
+      }
+    }
+  }
+  pdl_trigger();
+}
+
+// One warp per chunk: stable positions.  slot[s] = row of slot s in the
+// expert-sorted layout (or -1 for an invalid id).
+__global__ void __launch_bounds__(32) route_assign_kernel(const int64_t* __restrict__ ids, int64_t n, int E,
+                                                          const int32_t* __restrict__ base,
+                                                          int64_t* __restrict__ slot) {
+  __shared__ int32_t run[kMaxE];
+  const int lane = threadIdx.x;
+  for (int e = lane; e < E; e += 32) run[e] = base[static_cast<int64_t>(blockIdx.x) * E + e];
+  __syncwarp();
+  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kChunk;
+  for (int step = 0; step < kChunk / 32; ++step) {
+    const int64_t s = s0 + step * 32 + lane;
+    int key = E + lane;  // unique sentinel for lanes without a valid slot
+    if (s < n) {
+      const int64_t e = ids[s];
+      if (valid_id(e, E)) key = static_cast<int>(e);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const unsigned lt = (1u << lane) - 1u;
+    if (s < n) slot[s] = key < E ? static_cast<int64_t>(run[key] + __popc(peers & lt)) : -1;
+    __syncwarp();
+    if (key < E && (__ffs(peers) - 1) == lane) run[key] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+// xd[slot[s]] = x[s / k]   (one warp per slot, 16-byte vectors)
+__global__ void __launch_bounds__(256) gather_rows_kernel(const __nv_bfloat16* __restrict__ x,
+                                                          const int64_t* __restrict__ slot, int64_t n, int k,
+                                                          int64_t H, __nv_bfloat16* __restrict__ xd) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t s = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (s >= n) return;
+  const int64_t d = slot[s];
+  if (d < 0) return;
+  const uint4* src = reinterpret_cast<const uint4*>(x + (s / k) * H);
+  uint4* dst = reinterpret_cast<uint4*>(xd + d * H);
+  for (int64_t i = lane; i < H / 8; i += 32) dst[i] = src[i];
+}
+
+// y[t] = sum_j w[t,j] * yd[slot[t,j]]  (fp32, j ascending), one CTA per token
+__global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __restrict__ yd,
+                                                      const int64_t* __restrict__ slot, const float* __restrict__ w,
+                                                      int k, int64_t H, __nv_bfloat16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t t = blockIdx.x;
+  for (int64_t c = threadIdx.x; c < H / 8; c += blockDim.x) {
+    float acc[8] = {};
+    for (int j = 0; j < k; ++j) {
+      const int64_t d = slot[t * k + j];
+      if (d < 0) continue;
+      const float wj = w[t * k + j];
+      const uint4 u = *reinterpret_cast<const uint4*>(yd + d * H + c * 8);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h2[i]);
+        acc[2 * i] += wj * f.x;
+        acc[2 * i + 1] += wj * f.y;
+      }
+    }
+    uint4 o;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o2[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+    *reinterpret_cast<uint4*>(y + t * H + c * 8) = o;
+  }
+}
+
+// ---------------------------------------------------------------- host ops
+int64_t chunks_of(int64_t n) { return (n + kChunk - 1) / kChunk; }
+int64_t max_tiles(int64_t n, int E) { return n / 128 + E + 1; }
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+int topk_param(const opf_op_ctx& c) { return static_cast<int>(ctx_param(c, "topk", 8)); }
+int experts_param(const opf_op_ctx& c) { return static_cast<int>(ctx_param(c, "experts", 128)); }
+
+// route: histogram + scan (+ tile table); returns the per-chunk bases in ws
+void route_plan(const int64_t* ids, int64_t n, int E, char* ws, int32_t* gtab, cudaStream_t s) {
+  auto* cnt = reinterpret_cast<int32_t*>(ws);
+  const int64_t C = chunks_of(n);
+  if (C > 0) launch_pdl(route_hist_kernel, dim3(static_cast<unsigned>(C)), dim3(256), 0, s, ids, n, E, cnt);
+  launch_pdl(route_scan_kernel, dim3(1), dim3(1024), 0, s, cnt, static_cast<int>(C), E, gtab, 128);
+}
+
+opf_status op_moe_topk(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out, int32_t n_out,
+                       int64_t rows, void* stream) {
+  if (n_in != 1 || n_out != 2) return op_error(Errc::ShapeMismatch, "moe_topk takes (logits) -> (ids, w)");
+  const int E = static_cast<int>(view_row_elems(in[0]));
+  const int k = topk_param(*c);
+  if (E > 256 || k > 32 || k > E || k < 1) return op_error(Errc::ShapeMismatch, "moe_topk: E <= 256, 1 <= k <= min(32, E)");
+  if (view_row_elems(out[0]) != k || view_row_elems(out[1]) != k || out[0].dtype != OPF_I64 || out[1].dtype != OPF_F32)
+    return op_error(Errc::ShapeMismatch, "moe_topk: outputs are ids [T,k] i64 and w [T,k] f32");
+  if (rows == 0) return 0;
+  const int renorm = static_cast<int>(ctx_param(*c, "renorm", 1));
+  auto s = static_cast<cudaStream_t>(stream);
+  const unsigned grid = static_cast<unsigned>((rows * 32 + 255) / 256);
+  int64_t* ids = vptr<int64_t>(out[0]);
+  float* w = vptr<float>(out[1]);
+  const int per = (E + 31) / 32;
+#define OPF_TOPK(T, P)                                                                                 \
+  launch_pdl(topk_kernel<T, P>, dim3(grid), dim3(256), 0, s, static_cast<const T*>(vptr<T>(in[0])), ids, w, \
+             rows, E, k, renorm)
+  if (in[0].dtype == OPF_BF16) {
+    if (per <= 4) OPF_TOPK(__nv_bfloat16, 4); else OPF_TOPK(__nv_bfloat16, 8);
+  } else if (in[0].dtype == OPF_F32) {
+    if (per <= 4) OPF_TOPK(float, 4); else OPF_TOPK(float, 8);
+  } else {
+    return op_error(Errc::ShapeMismatch, "moe_topk: logits dtype");
+  }
+#undef OPF_TOPK
+  return launch_status("moe_topk");
+}
+
+size_t ws_dispatch(const opf_op_ctx& c, const opf_view*, int, const opf_view*, int, int64_t rows) {
+  return align256(static_cast<size_t>(chunks_of(rows * topk_param(c))) * experts_param(c) * 4) + 256;
+}
+size_t ws_grouped(const opf_op_ctx& c, const opf_view*, int, const opf_view*, int, int64_t rows) {
+  const int64_t n = rows * topk_param(c);
+  return align256(static_cast<size_t>(chunks_of(n)) * experts_param(c) * 4) +
+         align256(static_cast<size_t>(1 + 3 * max_tiles(n, experts_param(c))) * 4) + 256;
+}
+
+opf_status need_ws(const opf_op_ctx* c, size_t bytes, const char* who) {
+  if (!c->workspace || c->workspace_bytes < bytes)
+    return op_error(Errc::ConfigError, std::string(who) + ": workspace missing or too small");
+  return 0;
+}
+
+opf_status op_moe_dispatch(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out,
+                           int32_t n_out, int64_t rows, void* stream) {
+  if (n_in != 2 || n_out != 2) return op_error(Errc::ShapeMismatch, "moe_dispatch takes (x, ids) -> (xd, slot)");
+  const int k = topk_param(*c), E = experts_param(*c);
+  const int64_t H = view_row_elems(in[0]);
+  if (in[0].dtype != OPF_BF16 || out[0].dtype != OPF_BF16 || H % 8 || E > kMaxE ||
+      view_row_elems(in[1]) != k || view_row_elems(out[0]) != k * H || view_row_elems(out[1]) != k ||
+      out[1].dtype != OPF_I64)
+    return op_error(Errc::ShapeMismatch, "moe_dispatch: x [T,H] bf16, ids [T,k] -> xd [T,k*H], slot [T,k] i64");
+  if (rows == 0) return 0;
+  if (opf_status e = need_ws(c, ws_dispatch(*c, in, n_in, out, n_out, rows), "moe_dispatch")) return e;
+  auto s = static_cast<cudaStream_t>(stream);
+  const int64_t n = rows * k;
+  const int64_t* ids = vptr<int64_t>(in[1]);
+  int64_t* slot = vptr<int64_t>(out[1]);
+  char* ws = static_cast<char*>(c->workspace);
+  route_plan(ids, n, E, ws, nullptr, s);
+  route_assign_kernel<<<static_cast<unsigned>(chunks_of(n)), 32, 0, s>>>(ids, n, E,
+                                                                          reinterpret_cast<int32_t*>(ws), slot);
+  launch_pdl(gather_rows_kernel, dim3(static_cast<unsigned>((n * 32 + 255) / 256)), dim3(256), 0, s,
+             static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[0])), static_cast<const int64_t*>(slot), n,
+             k, H, vptr<__nv_bfloat16>(out[0]));
+  return launch_status("moe_dispatch");
+}
+
+// shared body of the two grouped expert GEMMs
+opf_status grouped(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out, int32_t n_out,
+                   int64_t rows, void* stream, bool gate_up) {
+  const char* who = gate_up ? "moe_gate_up" : "moe_down";
+  if (n_in != 3 || n_out != 1) return op_error(Errc::ShapeMismatch, std::string(who) + " takes (act, ids, w) -> out");
+  const int k = topk_param(*c), E = experts_param(*c);
+  // w: [E, K, N] reference layout (per-expert [K,N] MatMul weight)
+  if (in[2].rank != 3 || in[2].shape[0] != E || in[0].dtype != OPF_BF16 || in[2].dtype != OPF_BF16 ||
+      out[0].dtype != OPF_BF16 || view_row_elems(in[1]) != k)
+    return op_error(Errc::ShapeMismatch, std::string(who) + ": w must be [E, K, N] bf16, ids [T, k]");
+  const int64_t K = in[2].shape[1], N = in[2].shape[2];
+  const int64_t n_out_cols = gate_up ? N / 2 : N;
+  if (view_row_elems(in[0]) != k * K || view_row_elems(out[0]) != k * n_out_cols)
+    return op_error(Errc::ShapeMismatch, std::string(who) + ": activation widths");
+  if (rows == 0) return 0;
+  const void* packed = c->aux ? c->aux : (ctx_param(*c, "packed", 0.0) != 0.0 ? view_ptr(in[2]) : nullptr);
+  if (!packed)
+    return op_error(Errc::ConfigError, std::string(who) + ": expert weights not packed (run through a Session, "
+                                                          "or pass packed [E,N,K] weights with params.packed=1)");
+  if (opf_status e = need_ws(c, ws_grouped(*c, in, n_in, out, n_out, rows), who)) return e;
+  auto s = static_cast<cudaStream_t>(stream);
+  const int64_t n = rows * k;
+  char* ws = static_cast<char*>(c->workspace);
+  auto* gtab = reinterpret_cast<int32_t*>(ws + align256(static_cast<size_t>(chunks_of(n)) * E * 4));
+  route_plan(vptr<int64_t>(in[1]), n, E, ws, gtab, s);
+  GemmArgs g{};
+  g.a = view_ptr(in[0]);
+  g.bt = packed;
+  g.c = view_ptr(out[0]);
+  g.m = n;
+  g.n = N;
+  g.k = K;
+  g.lda = K;
+  g.ldc = n_out_cols;
+  g.max_ctas = c->max_ctas;
+  g.epi = gate_up ? 1 : 0;
+  gemm_bf16_grouped(g, gtab, max_tiles(n, E), N, E, s);
+  return launch_status(who);
+}
+
+opf_status op_moe_gate_up(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out, int32_t n_out,
+                          int64_t rows, void* stream) {
+  return grouped(c, in, n_in, out, n_out, rows, stream, true);
+}
+opf_status op_moe_down(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out, int32_t n_out,
+                       int64_t rows, void* stream) {
+  return grouped(c, in, n_in, out, n_out, rows, stream, false);
+}
+
+opf_status op_moe_combine(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out, int32_t n_out,
+                          int64_t rows, void* stream) {
+  if (n_in != 3 || n_out != 1) return op_error(Errc::ShapeMismatch, "moe_combine takes (yd, slot, w) -> y");
+  const int k = topk_param(*c);
+  const int64_t H = view_row_elems(out[0]);
+  if (in[0].dtype != OPF_BF16 || out[0].dtype != OPF_BF16 || in[1].dtype != OPF_I64 || in[2].dtype != OPF_F32 ||
+      H % 8 || view_row_elems(in[0]) != k * H || view_row_elems(in[1]) != k || view_row_elems(in[2]) != k)
+    return op_error(Errc::ShapeMismatch, "moe_combine: yd [T,k*H] bf16, slot [T,k] i64, w [T,k] f32 -> y [T,H]");
+  if (rows == 0) return 0;
+  auto s = static_cast<cudaStream_t>(stream);
+  launch_pdl(combine_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), 0, s,
+             static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[0])),
+             static_cast<const int64_t*>(vptr<int64_t>(in[1])), static_cast<const float*>(vptr<float>(in[2])), k,
+             H, vptr<__nv_bfloat16>(out[0]));
+  return launch_status("moe_combine");
+}
+
+}  // namespace
+
+void register_moe_ops(OpRegistry& r) {
+  r.add({"moe_topk", op_moe_topk, ResourceClass::kMemory, 1, 2, {}});
+  r.add({"moe_dispatch", op_moe_dispatch, ResourceClass::kNetwork, 2, 2, ws_dispatch});
+  r.add({"moe_gate_up", op_moe_gate_up, ResourceClass::kCompute, 3, 1, ws_grouped, 2, 2});
+  r.add({"moe_down", op_moe_down, ResourceClass::kCompute, 3, 1, ws_grouped, 2, 3});
+  r.add({"moe_combine", op_moe_combine, ResourceClass::kNetwork, 3, 1, {}});
+}
+
+}  // namespace opflow

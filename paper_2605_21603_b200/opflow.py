@@ -360,6 +360,12 @@ def toy_decoder_graph(**params: Any) -> str:
     return builder_json("toy_decoder", **params)
 
 
+def qwen3_moe_graph(**params: Any) -> str:
+    """Qwen3-30B-A3B-shaped layer(s): q/k-norm attention + routed MoE FFN
+    (router GEMM, top-k, dispatch, grouped expert GEMMs, combine); BASELINE configs[4]."""
+    return builder_json("qwen3_moe", **params)
+
+
 def alltoall_permutation(seed: int, cols: int) -> List[int]:
     buf = (C.c_uint32 * cols)()
     check(lib().opf_alltoall_permutation(C.c_uint64(seed & (2**64 - 1)), cols, buf))

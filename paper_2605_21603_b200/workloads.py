@@ -75,7 +75,7 @@ def llama_inputs(desc_json, rows: int, seed: int = 0, ctx_len: int | None = None
         elif name.endswith("norm.w"):
             out[name] = rnd(1.0 + rng.uniform(-0.1, 0.1, size=shape).astype(np.float32))
         elif role == "weight":
-            k = shape[0]
+            k = shape[-2] if len(shape) == 3 else shape[0]  # [E, K, N] expert weights
             out[name] = rnd((rng.uniform(-1.0, 1.0, size=shape) / np.sqrt(k)).astype(np.float32))
         elif t.get("dtype") == "i64":
             out[name] = rng.integers(-4, 5, size=shape).astype(np.int64)
