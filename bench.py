@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=20.0)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-decode", action="store_true")
+    p.add_argument("--no-moe", action="store_true")
+    p.add_argument("--moe-layers", type=int, default=1)
     p.add_argument("--decode-batch", type=int, default=512)
     p.add_argument("--decode-ctx", type=int, default=4096)
     p.add_argument("--sm-sweep", type=int, nargs="*", default=None,
@@ -138,7 +140,6 @@ def build_session(of, desc, rules, dev, comm, seed):
     sess = of.Session(g, plan, {"lanes": 3, "device": dev.index}, comm)
     gen = torch.Generator(device=dev).manual_seed(seed)
     bufs = {}
-    seq = int(json.loads(desc)["operators"][3]["attrs"]["params"].get("seq_len", 1)) if False else None
     for t in g.description["tensors"]:
         if t["role"] not in ("input", "weight", "output"):
             continue
@@ -151,7 +152,8 @@ def build_session(of, desc, rules, dev, comm, seed):
         elif t["name"].endswith("norm.w"):
             x = (1.0 + 0.1 * (torch.rand(shape, device=dev, generator=gen) - 0.5)).to(dt)
         elif t["role"] == "weight":
-            x = ((torch.rand(shape, device=dev, generator=gen) * 2 - 1) / shape[0] ** 0.5).to(dt)
+            fan_in = shape[-2] if len(shape) == 3 else shape[0]  # [E, K, N] expert weights
+            x = ((torch.rand(shape, device=dev, generator=gen) * 2 - 1) / fan_in ** 0.5).to(dt)
         else:
             x = (torch.rand(shape, device=dev, generator=gen) * 2 - 1).to(dt)
         bufs[t["name"]] = x
@@ -288,6 +290,11 @@ def run_ours(args):
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
         decode = run_decode(of, torch, dev, args, tp, comm, rank, world, stream)
+    moe = None
+    if not args.no_moe and tp == 1:
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        moe = run_moe(of, torch, dev, args, rank, world, stream)
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(args, T, S, tp)
         line = {
@@ -318,6 +325,7 @@ def run_ours(args):
                              flops_layer * L / (PEAKS["bf16_tflops"] * 1e12) * 1e3 / best_ms, 4)},
             "cpu_baseline": cpu,
             "decode": decode,
+            "moe": moe,
             "clocks": clk.summary(),
             "gpu_launches": int(launches) * args.steps,
             "plan": {"dispatches": stats["last"]["dispatches"], "launches_per_step": launches,
@@ -407,10 +415,114 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
             "sequential_tokens_per_s": round(B / (res["sequential"] / 1e3), 1),
             "speedup_vs_sequential": round(res["sequential"] / res[best], 4),
             "strategies_ms": {k: round(v, 3) for k, v in res.items()},
-            "roofline": {"bound": "hbm", "kernel": "decode_bf16_kernel (paged attention)",
+            "roofline": {"bound": "hbm", "kernel": "decode_mma_kernel (paged attention, mma.sync)",
                          "achieved": round(achieved, 1), "peak": PEAKS["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / PEAKS["hbm_gbs"], 4), "ms_per_launch": round(attn_ms, 4),
                          "algorithmic_bytes_per_launch": kv_bytes}}
+
+
+QWEN3 = dict(hidden=2048, heads=32, kv_heads=4, head_dim=128, experts=128, topk=8, moe_inter=768)
+
+
+def time_op(of, torch, dev, stream, fn, ins, outs, params, rows, reps=20):
+    """One registered op through a one-op Session (prepack + workspace planned
+    by the engine), CUDA events on `stream` around back-to-back graph replays."""
+    tensors = []
+    for name, x, role in ins + outs:
+        dt = {torch.bfloat16: "bf16", torch.int64: "i64", torch.float32: "f32"}[x.dtype]
+        t = {"name": name, "shape": list(x.shape), "dtype": dt, "role": role}
+        if role == "weight":
+            t["batch"] = "replicated"
+        tensors.append(t)
+    desc = json.dumps({"tensors": tensors, "operators": [
+        {"name": "op", "kind": "Custom", "inputs": [i[0] for i in ins], "outputs": [o[0] for o in outs],
+         "attrs": {"custom_name": fn, "params": params}}]})
+    g = of.build_graph(desc)
+    sess = of.Session(g, of.partition(g, []), {"lanes": 1, "device": dev.index})
+    for name, x, _ in ins + outs:
+        sess.bind(name, x)
+    for _ in range(3):
+        sess.run(None, stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        sess.run(None, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    del sess
+    return e0.elapsed_time(e1) / reps
+
+
+def run_moe(of, torch, dev, args, rank, world, stream):
+    """BASELINE configs[4]: Qwen3-30B-A3B-shaped MoE layer (q/k-norm GQA
+    attention + 128-expert top-8 FFN), 8192 tokens (8 x 1024), dual-batch
+    overlap vs sequential on one GPU (EP=1: dispatch/combine are local
+    permutations at the all-to-all sites).  Roofline: the grouped tcgen05
+    expert GEMMs (tensor) and dispatch/combine (HBM), timed alone."""
+    T, S, L = args.tokens, args.seq_len, args.moe_layers
+    Q = QWEN3
+    desc = of.qwen3_moe_graph(layers=L, tokens=T, seq_len=S, dtype="bf16", **Q)
+    R = of.PartitionRule
+    rules = [R.by_module("layer*.attn"), R.by_module("layer*.moe.dispatch"),
+             R.by_module("layer*.moe.experts"), R.by_module("layer*.moe.combine")]
+    g, plan, sess, bufs = build_session(of, desc, rules, dev, None, seed=4321 + rank)
+    pos = (torch.arange(T, device=dev) % S).to(torch.int64)
+    bufs["positions"] = pos
+    sess.bind("positions", pos)
+    cands = {"sequential": {"name": "sequential"}, "dbo": {"name": "dbo", "align": S},
+             "nanoflow_u2": {"name": "split_overlap", "n_microbatches": 2, "align": S, "lane_mode": "ubatch"}}
+    res = {k: time_steps(torch, lambda s=s: sess.run(s, stream), args.steps, args.warmup, stream, world)
+           for k, s in cands.items()}
+    best = min((k for k in res if k != "sequential"), key=lambda k: res[k])
+    launches = sess.stats()["last"]["launches"]
+    del sess, bufs
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    # ---- per-op rooflines at the layer's shapes (balanced random top-8 routing)
+    E, k, H, MI = Q["experts"], Q["topk"], Q["hidden"], Q["moe_inter"]
+    gen = torch.Generator(device=dev).manual_seed(7)
+    ids = torch.argsort(torch.rand(T, E, device=dev, generator=gen), dim=1)[:, :k].contiguous().to(torch.int64)
+    x = (torch.rand(T, H, device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
+    xd = torch.empty(T, k * H, device=dev, dtype=torch.bfloat16)
+    slot = torch.empty(T, k, device=dev, dtype=torch.int64)
+    wgu = ((torch.rand(E, H, 2 * MI, device=dev, generator=gen) * 2 - 1) / H ** 0.5).to(torch.bfloat16)
+    wd = ((torch.rand(E, MI, H, device=dev, generator=gen) * 2 - 1) / MI ** 0.5).to(torch.bfloat16)
+    hd = torch.empty(T, k * MI, device=dev, dtype=torch.bfloat16)
+    yd = torch.empty(T, k * H, device=dev, dtype=torch.bfloat16)
+    wts = torch.full((T, k), 1.0 / k, device=dev, dtype=torch.float32)
+    y = torch.empty(T, H, device=dev, dtype=torch.bfloat16)
+    prm = {"experts": E, "topk": k}
+    ms_disp = time_op(of, torch, dev, stream, "moe_dispatch", [("x", x, "input"), ("ids", ids, "input")],
+                      [("xd", xd, "output"), ("slot", slot, "output")], prm, T)
+    ms_gu = time_op(of, torch, dev, stream, "moe_gate_up",
+                    [("xd", xd, "input"), ("ids", ids, "input"), ("w", wgu, "weight")], [("hd", hd, "output")], prm, T)
+    ms_dn = time_op(of, torch, dev, stream, "moe_down",
+                    [("hd", hd, "input"), ("ids", ids, "input"), ("w", wd, "weight")], [("yd", yd, "output")], prm, T)
+    ms_cb = time_op(of, torch, dev, stream, "moe_combine",
+                    [("yd", yd, "input"), ("slot", slot, "input"), ("w", wts, "input")], [("y", y, "output")],
+                    prm, T)
+    fl_gu, fl_dn = 2.0 * T * k * H * 2 * MI, 2.0 * T * k * MI * H
+    achieved = (fl_gu + fl_dn) / ((ms_gu + ms_dn) / 1e3) / 1e12
+    b_disp = T * k * H * 2 + T * H * 2 + T * k * 8 * 2  # write xd, read x, ids + slot
+    b_comb = T * k * H * 2 + T * H * 2 + T * k * 12    # read yd, write y, slot + w
+    per_op = [{"op": "moe_gate_up", "ms": round(ms_gu, 4), "tflops": round(fl_gu / ms_gu / 1e9, 1)},
+              {"op": "moe_down", "ms": round(ms_dn, 4), "tflops": round(fl_dn / ms_dn / 1e9, 1)},
+              {"op": "moe_dispatch", "ms": round(ms_disp, 4), "gbs": round(b_disp / ms_disp / 1e6, 1),
+               "hbm_frac": round(b_disp / ms_disp / 1e6 / PEAKS["hbm_gbs"], 4)},
+              {"op": "moe_combine", "ms": round(ms_cb, 4), "gbs": round(b_comb / ms_cb / 1e6, 1),
+               "hbm_frac": round(b_comb / ms_cb / 1e6 / PEAKS["hbm_gbs"], 4)}]
+    return {"workload": f"qwen3-30b-a3b-shaped MoE layer x{L} (q/k-norm GQA attention + {E}-expert top-{k} "
+                        f"FFN, moe_inter {MI}), {T} tokens ({T // S} seqs x {S}), EP=1",
+            "tokens_per_s": round(T / (res[best] / 1e3), 1), "strategy": best,
+            "sequential_tokens_per_s": round(T / (res["sequential"] / 1e3), 1),
+            "speedup_vs_sequential": round(res["sequential"] / res[best], 4),
+            "strategies_ms": {k_: round(v, 3) for k_, v in res.items()},
+            "launches_per_step": launches,
+            "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel<GROUPED> (moe_gate_up + moe_down)",
+                         "achieved": round(achieved, 1), "peak": PEAKS["bf16_tflops"], "unit": "TFLOP/s",
+                         "frac": round(achieved / PEAKS["bf16_tflops"], 4),
+                         "algorithmic_flops": fl_gu + fl_dn, "per_op": per_op}}
 
 
 # ------------------------------------------------------------------ reference (CPU)

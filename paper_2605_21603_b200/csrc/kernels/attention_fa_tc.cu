@@ -2,8 +2,9 @@
 //
 // Persistent CTAs (one per SM, 224 KB smem) walk (q-tile, head, sequence)
 // items longest-first.  Per item (128 query rows of one head):
-//   warp 0  TMA: Q tile once; K_j, V_j tiles (128 keys x 128 dims, two 64-dim
-//           128B-swizzled halves each) into a 2-stage ring.  One tensor map over
+//   warp 0  TMA: Q tile once, K_j tiles; warp 3 TMA: V_j tiles (128 keys x 128 dims,
+//           two 64-dim 128B-swizzled halves each), separate 2-stage K and V rings
+//           (K_j's slot frees when S_j retires, V_j's when PV_j retires).  One tensor map over
 //           the whole qkv buffer serves Q, K and V (column = head * 128).
 //   warp 1  MMA (one thread): S_j = Q K_j^T -> TMEM S[j % 2] (M=N=K=128, both
 //           operands K-major); O += P_j V_j -> TMEM O (A = P from smem,
@@ -13,12 +14,14 @@
 //   warp 2  completion tracker: waits every PV commit in order and publishes a
 //           running count in smem (softmax warps read it before touching O or
 //           overwriting a P buffer).
-//   warps 4..7  softmax: thread = one query row (TMEM lane), whole 128-key row
-//           in registers (tcgen05.ld 32x32b), row max / exp2 / sum without
-//           shuffles, causal mask on the diagonal tile, P (bf16) written to a
-//           double-buffered K-major SW128 smem tile.  Lazy rescaling: the
-//           exponent base m only moves when the row max grows by > 8 (log2), then
-//           O (TMEM) and l are rescaled; final O / l in the epilogue.
+//   warps 4..11 softmax: two warps per TMEM lane quarter, thread = one query
+//           row x 64 key columns (tcgen05.ld 32x32b); causal mask on the diagonal
+//           tile, row max halves exchanged through smem (64-thread named barrier),
+//           exp2 with the scale folded into one FFMA, P (bf16) packed in registers
+//           and stored to the single K-major SW128 P tile once PV_{j-1} retired.
+//           Lazy rescaling: the exponent base m only moves when the row max grows
+//           by > 8 (log2), then each half rescales its 64 O columns in TMEM;
+//           final O / l (halves' sums exchanged) in the epilogue.
 // FLOPs per item = 4 * 128 * 128 * 128 * (#key tiles) (diagonal tile half-masked).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -33,20 +36,22 @@ namespace opflow {
 namespace {
 
 constexpr int HD = 128, BQ = 128, BKV = 128;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // 4 role warps + 8 softmax warps
 constexpr uint32_t kHalf = 128 * 64 * 2;   // 16 KB: 128 rows x 64 bf16 (one swizzled half)
 constexpr uint32_t kTile = 2 * kHalf;      // 32 KB: 128 rows x 128 bf16
 constexpr int kStages = 2;
 constexpr uint32_t kSmemQ = 0;
 constexpr uint32_t kSmemK = kTile;                      // [kStages]
 constexpr uint32_t kSmemV = kSmemK + kStages * kTile;   // [kStages]
-constexpr uint32_t kSmemP = kSmemV + kStages * kTile;   // [2]
-constexpr uint32_t kSmemBar = kSmemP + 2 * kTile;
-constexpr uint32_t kSmemTotal = kSmemBar + 256 + 1024;  // + barriers + alignment slack
+constexpr uint32_t kSmemBar = kSmemV + kStages * kTile;
+// TMEM columns: S[0] 0..127, S[1] 128..255, O 256..383, P[0] 384..447, P[1] 448..511
+constexpr uint32_t kColO = 256, kColP = 384;
+constexpr uint32_t kSmemXch = kSmemBar + 256;           // row max / sum exchange [2][2][128] f32
+constexpr uint32_t kSmemTotal = kSmemXch + 2048 + 1024;  // + alignment slack
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
 // kind::f16, D f32, A/B bf16, M=128, N=128; b_mn: B operand MN-major
-constexpr uint32_t idesc(bool b_mn) {
+__host__ __device__ constexpr uint32_t idesc(bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn ? 1u : 0u) << 16) | ((128u >> 3) << 17) |
          ((128u >> 4) << 24);
 }
@@ -90,6 +95,24 @@ __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint3
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
       "l"(a), "l"(b), "r"(id), "r"(acc));
 }
+// A operand from TMEM (P: lane = query row, 32-bit column = 2 consecutive bf16 keys)
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void tst32u(uint32_t a, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31, %32};" ::"r"(a),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
 __device__ __forceinline__ void commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b))
                : "memory");
@@ -127,6 +150,14 @@ __device__ __forceinline__ void tst32(uint32_t a, const float (&v)[32]) {
       "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
       : "memory");
 }
+__device__ __forceinline__ void st_release(uint32_t a, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint32_t bf2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -136,6 +167,34 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe: x = k + f (k = round(x) via the 1.5*2^23 magic add,
+// f in [-0.5, 0.5]), 2^f by a cubic (max rel err ~1e-4, below bf16's 4e-3),
+// 2^k added into the exponent bits.  x is clamped at -126 (result ~1e-38).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;
+  const float f = x - (t - 12582912.0f);
+  float p = fmaf(fmaf(fmaf(0.0555041086648216f, f, 0.2402264923172690f), f, 0.6931471805599453f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+#ifndef FA_POLY
+#define FA_POLY 8
+#endif
+constexpr int kPolyPairs = FA_POLY;  // of the 32 element pairs each softmax thread exponentiates
+
+#ifdef FA_TRACE  // per-phase clock64 timeline of CTA 0 (tools/fa_trace.cu); compiled out otherwise
+__device__ long long g_fa_trace[12][64];
+#define FA_T(ev, j)                                       \
+  do {                                                    \
+    const int fa_j_ = (j);                                \
+    if (blockIdx.x == 0 && fa_j_ < 64) g_fa_trace[ev][fa_j_] = clock64(); \
+  } while (0)
+#else
+#define FA_T(ev, j) \
+  do {              \
+    (void)(j);      \
+  } while (0)
+#endif
 
 __global__ void __launch_bounds__(kThreads, 1)
     fa_tc_kernel(const __grid_constant__ CUtensorMap mqkv, __nv_bfloat16* __restrict__ out, int nq,
@@ -147,21 +206,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* q_empty = bars + 1;
   uint64_t* k_full = bars + 2;   // [2]
   uint64_t* v_full = bars + 4;   // [2]
-  uint64_t* kv_empty = bars + 6; // [2]
+  uint64_t* k_empty = bars + 6;  // [2]  S_j retired (K slot free)
+  uint64_t* v_empty = bars + 18; // [2]  PV_j retired (V slot free)
   uint64_t* s_full = bars + 8;   // [2]
   uint64_t* s_free = bars + 10;  // [2]
-  uint64_t* p_full = bars + 12;  // [2]
+  uint64_t* p_full = bars + 12;  // single P buffer
   uint64_t* o_done = bars + 14;  // one phase per PV
   uint64_t* o_free = bars + 15;  // epilogue finished reading O
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
   volatile uint32_t* pv_count = reinterpret_cast<volatile uint32_t*>(bars + 17);
+  const uint32_t pv_count_addr = su32(bars + 17);
+  static_assert(20 * 8 <= 256, "barrier area");
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q_tiles = S / BQ;
   const int64_t per_q = static_cast<int64_t>(nq) * n_seqs;
   const int64_t n_items = per_q * q_tiles;
   const int grp = nq / nkv;
-  const int W = (nq + 2 * nkv) * HD;  // qkv row width (elements)
 
   if (warp == 0) {
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mqkv)) : "memory");
@@ -173,13 +234,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       bar_init(&k_full[i], 1);
       bar_init(&v_full[i], 1);
-      bar_init(&kv_empty[i], 1);
+      bar_init(&k_empty[i], 1);
+      bar_init(&v_empty[i], 1);
       bar_init(&s_full[i], 1);
-      bar_init(&s_free[i], 4);
-      bar_init(&p_full[i], 4);
+      bar_init(&s_free[i], 8);
     }
+    bar_init(p_full, 8);
     bar_init(o_done, 1);
-    bar_init(o_free, 4);
+    bar_init(o_free, 8);
     *pv_count = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -187,6 +249,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;  // S[0] cols 0..127, S[1] 128..255, O 256..383
+  int tile_k = 0, tile_v = 0, tile_s = 0, tile_pv = 0, tile_sm = 0;  // trace indices
+  (void)tile_k, (void)tile_v, (void)tile_s, (void)tile_pv, (void)tile_sm;
   pdl_wait();
   pdl_trigger();
 
@@ -212,14 +276,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma2d(su32(sm + kSmemQ), &mqkv, q_full, h * HD, row0 + qt * BQ);
         tma2d(su32(sm + kSmemQ + kHalf), &mqkv, q_full, h * HD + 64, row0 + qt * BQ);
         for (int j = 0; j <= qt; ++j) {
-          bar_wait(&kv_empty[stage], ph ^ 1);
-          const uint32_t kd = su32(sm + kSmemK + stage * kTile), vd = su32(sm + kSmemV + stage * kTile);
+          bar_wait(&k_empty[stage], ph ^ 1);
+          const uint32_t kd = su32(sm + kSmemK + stage * kTile);
           bar_expect(&k_full[stage], kTile);
           tma2d(kd, &mqkv, &k_full[stage], (nq + kh) * HD, row0 + j * BKV);
           tma2d(kd + kHalf, &mqkv, &k_full[stage], (nq + kh) * HD + 64, row0 + j * BKV);
+          FA_T(0, tile_k++);
+          if (++stage == kStages) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer (V)
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        int qt, h, seq;
+        decode_item(it, qt, h, seq);
+        const int kh = h / grp;
+        const int row0 = seq * S;
+        for (int j = 0; j <= qt; ++j) {
+          bar_wait(&v_empty[stage], ph ^ 1);
+          const uint32_t vd = su32(sm + kSmemV + stage * kTile);
           bar_expect(&v_full[stage], kTile);
           tma2d(vd, &mqkv, &v_full[stage], (nq + nkv + kh) * HD, row0 + j * BKV);
           tma2d(vd + kHalf, &mqkv, &v_full[stage], (nq + nkv + kh) * HD + 64, row0 + j * BKV);
+          FA_T(1, tile_v++);
           if (++stage == kStages) {
             stage = 0;
             ph ^= 1;
@@ -230,9 +315,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
       int stage = 0;
-      uint32_t ph = 0, qph = 0, ofree_ph = 0;
-      uint32_t sfree_ph[2] = {0, 0}, pfull_ph[2] = {0, 0};
-      int sbuf_uses[2] = {0, 0};
+      uint32_t ph = 0, qph = 0, ofree_ph = 0, pfull_ph = 0;
+      uint32_t sfree_ph = 0, sbuf_used = 0;  // per-S-buffer bits
       bool first_item = true;
       const uint32_t S_id = idesc(false), PV_id = idesc(true);
       const uint32_t qa = su32(sm + kSmemQ);
@@ -245,21 +329,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         int pv_stage = stage;
         uint32_t pv_ph = ph;
         auto issue_pv = [&](int j) {
-          const int b = j & 1;
-          bar_wait(&p_full[b], pfull_ph[b]);
-          pfull_ph[b] ^= 1;
+          bar_wait(p_full, pfull_ph);
+          pfull_ph ^= 1;
           bar_wait(&v_full[pv_stage], pv_ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t pa = su32(sm + kSmemP + b * kTile);
           const uint32_t vb = su32(sm + kSmemV + pv_stage * kTile);
+          const uint32_t pt = tmem + kColP + (j & 1) * 64;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {  // 16 keys per step
-            const uint64_t ad = sdesc(pa + (k >> 2) * kHalf + (k & 3) * 32, 16, 1024);
+          for (int k = 0; k < 8; ++k) {  // 16 keys (8 TMEM columns of P) per step
             const uint64_t bd = sdesc(vb + k * 2048, kHalf, 1024);
-            mma_ss(tmem + 256, ad, bd, PV_id, (j | k) != 0);
+            mma_ts(tmem + kColO, pt + k * 8, bd, PV_id, (j | k) != 0);
           }
-          commit(&kv_empty[pv_stage]);
+          commit(&v_empty[pv_stage]);
           commit(o_done);
+          FA_T(3, tile_pv++);
           if (++pv_stage == kStages) {
             pv_stage = 0;
             pv_ph ^= 1;
@@ -267,10 +350,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         for (int j = 0; j < n; ++j) {
           const int b = j & 1;
-          if (sbuf_uses[b]++ > 0) {  // S buffer b last held S_{j-2}: softmax must be done reading
-            bar_wait(&s_free[b], sfree_ph[b]);
-            sfree_ph[b] ^= 1;
+          if (sbuf_used & (1u << b)) {  // S buffer b last held S_{j-2}: softmax must be done reading
+            bar_wait(&s_free[b], (sfree_ph >> b) & 1u);
+            sfree_ph ^= 1u << b;
           }
+          sbuf_used |= 1u << b;
           bar_wait(&k_full[stage], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t kb = su32(sm + kSmemK + stage * kTile);
@@ -281,6 +365,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_ss(tmem + b * 128, ad, bd, S_id, k != 0);
           }
           commit(&s_full[b]);
+          FA_T(2, tile_s++);
+          commit(&k_empty[stage]);
           if (++stage == kStages) {
             stage = 0;
             ph ^= 1;
@@ -312,45 +398,71 @@ __global__ void __launch_bounds__(kThreads, 1)
           bar_wait(o_done, oph);
           oph ^= 1;
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          *pv_count = ++count;
-          __threadfence_block();
+          st_release(pv_count_addr, ++count);
+          FA_T(4, static_cast<int>(count) - 1);
         }
       }
     }
   } else if (warp >= 4) {  // ---------------------------------------- softmax / epilogue
-    const int q = warp & 3;          // TMEM lane quarter
-    const int r = q * 32 + lane;     // query row within the tile
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    uint32_t sfull_ph[2] = {0, 0};
-    uint32_t pv_seen = 0;  // PV count at the start of this item
+    // Two warps per TMEM lane quarter: hf = 0 takes key columns 0..63 (and O
+    // columns 0..63), hf = 1 columns 64..127.  Row max / row sum halves meet in
+    // a double-buffered smem exchange behind a 64-thread named barrier.
+    const int q = warp & 3;             // TMEM lane quarter
+    const int hf = (warp - 4) >> 2;     // column half
+    const int r = q * 32 + lane;        // query row within the tile
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + hf * 64;   // S columns
+    const uint32_t o_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + kColO + hf * 64;
+    const uint32_t p_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + kColP + hf * 32;
+    float* xch = reinterpret_cast<float*>(sm + kSmemXch);  // [2 parity][2 half][128 rows]
+    uint32_t xpar = 0;
+    auto exchange = [&](float v) {  // returns the partner half's value for row r
+      xch[(xpar * 2 + hf) * 128 + r] = v;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+      const float o = xch[(xpar * 2 + (hf ^ 1)) * 128 + r];
+      xpar ^= 1;
+      return o;
+    };
+    uint32_t sfull_ph = 0;  // per-S-buffer bits
+    uint32_t pv_seen = 0;   // PV count at the start of this item
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
       int qt, h, seq;
       decode_item(it, qt, h, seq);
       const int n = qt + 1;
-      float m_used = -FLT_MAX, l = 0.0f;
+      float m_used = -FLT_MAX, l = 0.0f;  // m_used in scaled log2 units; l over this half
       for (int j = 0; j < n; ++j) {
         const int b = j & 1;
-        bar_wait(&s_full[b], sfull_ph[b]);
-        sfull_ph[b] ^= 1;
+        bar_wait(&s_full[b], (sfull_ph >> b) & 1u);
+        if (lane == 0 && warp == 4) FA_T(5, tile_sm);
+        sfull_ph ^= 1u << b;
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        float s[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tld32(lane_base + b * 128 + c * 32, *reinterpret_cast<float(*)[32]>(&s[c * 32]));
+        float s[64];
+        tld32(lane_base + b * 128, *reinterpret_cast<float(*)[32]>(&s[0]));
+        tld32(lane_base + b * 128 + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) bar_arrive(&s_free[b]);
-        // scale, causal mask (diagonal tile only), row max
-        const bool diag = j == qt;
-        float mx = -FLT_MAX;
+        if (lane == 0 && warp == 4) FA_T(7, tile_sm);
+        // causal mask (diagonal tile only) and row max on the raw scores; the
+        // softmax scale folds into one FFMA per element below
+        float mx8[8];
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          float v = s[c] * scale_log2;
-          if (diag && c > r) v = -FLT_MAX;
-          s[c] = v;
-          mx = fmaxf(mx, v);
+        for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+        if (j == qt) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            if (hf * 64 + c > r) s[c] = -INFINITY;
+            mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
         }
-        // lazy rescale of the exponent base
+        const float pm = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        const float mx = scale_log2 * fmaxf(pm, exchange(pm));  // identical in both halves
+        if (lane == 0 && warp == 4) FA_T(8, tile_sm);
+        // lazy rescale of the exponent base (log2 units)
         float factor = 1.0f;
         const bool rescale = mx > m_used + kRescaleThresh;
         if (rescale) {
@@ -358,62 +470,60 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_used = mx;
         }
         l *= factor;
-        float sum = 0.0f;
-        // P buffer b was last read by PV_{j-2}
-        if (j >= 2)
-          while (*pv_count < pv_seen + static_cast<uint32_t>(j - 1)) {
-          }
-        uint8_t* pbuf = sm + kSmemP + b * kTile;
+        float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[32];  // P row half, packed bf16x2
 #pragma unroll
-        for (int c8 = 0; c8 < 16; ++c8) {
-          float p[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            p[e] = ex2(s[c8 * 8 + e] - m_used);
-            sum += p[e];
-          }
-          const int half = c8 >> 3, chunk = c8 & 7;
-          uint4 u;
-          u.x = bf2(p[0], p[1]);
-          u.y = bf2(p[2], p[3]);
-          u.z = bf2(p[4], p[5]);
-          u.w = bf2(p[6], p[7]);
-          *reinterpret_cast<uint4*>(pbuf + half * kHalf + r * 128 + ((chunk ^ (r & 7)) << 4)) = u;
+        for (int c2 = 0; c2 < 32; ++c2) {
+          // FA4-style split: the first kPolyPairs pairs use the FMA-pipe polynomial,
+          // the rest MUFU ex2 (the pipes run concurrently)
+          const float x0 = fmaf(s[2 * c2], scale_log2, -m_used), x1 = fmaf(s[2 * c2 + 1], scale_log2, -m_used);
+          const float p0 = c2 < kPolyPairs ? ex2_poly(x0) : ex2(x0);
+          const float p1 = c2 < kPolyPairs ? ex2_poly(x1) : ex2(x1);
+          sum8[(2 * c2) & 7] += p0;
+          sum8[(2 * c2 + 1) & 7] += p1;
+          pk[c2] = bf2(p0, p1);
         }
-        l += sum;
-        // rescale O (TMEM) when any row of this warp moved its base (not on tile 0)
-        if (j > 0 && __any_sync(0xffffffffu, rescale)) {
-          while (*pv_count < pv_seen + static_cast<uint32_t>(j)) {  // PV_{j-1} complete
-          }
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        l += ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
+        if (lane == 0 && warp == 4) FA_T(9, tile_sm);
+        // P buffer (j & 1) was last read by PV_{j-2}; O rescaling needs PV_{j-1} retired
+        const bool any_rescale = j > 0 && __any_sync(0xffffffffu, rescale);
+        const uint32_t need = any_rescale ? static_cast<uint32_t>(j) : (j >= 2 ? static_cast<uint32_t>(j - 1) : 0u);
+        while (ld_acquire(pv_count_addr) < pv_seen + need) {
+        }
+        if (lane == 0 && warp == 4) FA_T(10, tile_sm);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (any_rescale) {  // this half's 64 O columns
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < 2; ++c) {
             float o[32];
-            tld32(lane_base + 256 + c * 32, o);
+            tld32(o_base + c * 32, o);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[e] *= factor;
-            tst32(lane_base + 256 + c * 32, o);
+            tst32(o_base + c * 32, o);
           }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tst32u(p_base + (j & 1) * 64, pk);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) bar_arrive(&p_full[b]);
+        if (lane == 0) bar_arrive(p_full);
+        if (lane == 0 && warp == 4) FA_T(6, tile_sm);
+        ++tile_sm;
       }
       // ---- epilogue: wait for the item's last PV, O / l -> bf16 -> global
-      while (*pv_count < pv_seen + static_cast<uint32_t>(n)) {
+      const float l_all = l + exchange(l);
+      while (ld_acquire(pv_count_addr) < pv_seen + static_cast<uint32_t>(n)) {
       }
       pv_seen += n;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const float inv = l > 0.0f ? 1.0f / l : 0.0f;
+      const float inv = l_all > 0.0f ? 1.0f / l_all : 0.0f;
       __nv_bfloat16* orow = out + (static_cast<int64_t>(seq) * S + qt * BQ + r) * (static_cast<int64_t>(nq) * HD) +
-                            static_cast<int64_t>(h) * HD;
+                            static_cast<int64_t>(h) * HD + hf * 64;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         float o[32];
-        tld32(lane_base + 256 + c * 32, o);
+        tld32(o_base + c * 32, o);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int v = 0; v < 4; ++v) {

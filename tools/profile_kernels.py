@@ -1,6 +1,7 @@
 """Run each hot kernel once on its Llama-3-8B bench shape (for ncu captures):
   gemm (qkv 8192x6144x4096, gate_up+SiLU 8192x28672x4096), prefill attention
-  (8 x 1024 tokens, 32/8 heads), paged decode attention (512 x 4K), add_rmsnorm.
+  (8 x 1024 tokens, 32/8 heads), paged decode attention (512 x 4K), add_rmsnorm,
+  Qwen3 MoE expert FFN (dispatch, grouped gate_up / down, combine).
 Usage: ncu --set full -k regex:<kernel> python tools/profile_kernels.py [which]"""
 import os
 import sys
@@ -73,5 +74,40 @@ if which in ("all", "norm"):
           "attrs": {"custom_name": "add_rmsnorm", "params": {"eps": 1e-5}}}
     for _ in range(2):
         of.launch(op, [x, r, gm], [s_, y], T)
+if which in ("all", "moe"):
+    # Qwen3-30B-A3B expert FFN: 8192 tokens, 128 experts, top-8, H 2048, moe_inter 768
+    import json
+    E, k, Hm, MI = 128, 8, 2048, 768
+    ids = torch.argsort(torch.rand(T, E, device=dev), dim=1)[:, :k].contiguous()
+    x = torch.randn(T, Hm, device=dev).to(torch.bfloat16)
+    tens = [{"name": "x", "shape": [T, Hm], "dtype": "bf16", "role": "input"},
+            {"name": "ids", "shape": [T, k], "dtype": "i64", "role": "input"},
+            {"name": "wgu", "shape": [E, Hm, 2 * MI], "dtype": "bf16", "role": "weight", "batch": "replicated"},
+            {"name": "wd", "shape": [E, MI, Hm], "dtype": "bf16", "role": "weight", "batch": "replicated"},
+            {"name": "w", "shape": [T, k], "dtype": "f32", "role": "input"},
+            {"name": "xd", "shape": [T, k * Hm], "dtype": "bf16"},
+            {"name": "slot", "shape": [T, k], "dtype": "i64"},
+            {"name": "hd", "shape": [T, k * MI], "dtype": "bf16"},
+            {"name": "yd", "shape": [T, k * Hm], "dtype": "bf16"},
+            {"name": "y", "shape": [T, Hm], "dtype": "bf16", "role": "output"}]
+    prm = {"experts": E, "topk": k}
+    ops = [{"name": "dispatch", "kind": "Custom", "inputs": ["x", "ids"], "outputs": ["xd", "slot"],
+            "attrs": {"custom_name": "moe_dispatch", "params": prm}},
+           {"name": "gate_up", "kind": "Custom", "inputs": ["xd", "ids", "wgu"], "outputs": ["hd"],
+            "attrs": {"custom_name": "moe_gate_up", "params": prm}},
+           {"name": "down", "kind": "Custom", "inputs": ["hd", "ids", "wd"], "outputs": ["yd"],
+            "attrs": {"custom_name": "moe_down", "params": prm}},
+           {"name": "combine", "kind": "Custom", "inputs": ["yd", "slot", "w"], "outputs": ["y"],
+            "attrs": {"custom_name": "moe_combine", "params": prm}}]
+    g = of.build_graph(json.dumps({"tensors": tens, "operators": ops}))
+    s = of.Session(g, of.partition(g, []), {"lanes": 1})
+    bind = {"x": x, "ids": ids, "w": torch.full((T, k), 1.0 / k, device=dev),
+            "wgu": (torch.randn(E, Hm, 2 * MI, device=dev) / Hm ** 0.5).to(torch.bfloat16),
+            "wd": (torch.randn(E, MI, Hm, device=dev) / MI ** 0.5).to(torch.bfloat16),
+            "y": torch.empty(T, Hm, device=dev, dtype=torch.bfloat16)}
+    for n_, t_ in bind.items():
+        s.bind(n_, t_)
+    for _ in range(2):
+        s.run()
 torch.cuda.synchronize()
 print("done", which)
