@@ -146,6 +146,19 @@ typedef struct opf_sched_ctx opf_sched_ctx;
 opf_status opf_session_create(const opf_graph* g, const opf_plan* p, const char* config_json,
                               opf_comm* comm, opf_session** out);
 void opf_session_free(opf_session* s);
+
+/* Symmetric arena for peer-memory (expert-parallel) ops: every rank runs the
+ * same plans, so a tensor sits at the same arena offset on every rank.
+ * opf_session_arena_export allocates (at least min_bytes) and pins the arena
+ * (later plans must fit) and returns its CUDA IPC handle (NULL: skip);
+ * opf_session_arena_open maps all peers' handles ([world][64] bytes) into the
+ * session's communicator; opf_session_arena_link_local wires `world` sessions
+ * of ONE process (virtual ranks on one device) without IPC.  No reference
+ * counterpart: the reference's AllToAll is a single-process column
+ * permutation (/root/reference/proj/src/eval.cpp:71-80). */
+opf_status opf_session_arena_export(opf_session* s, int64_t min_bytes, uint8_t ipc_handle_out[64]);
+opf_status opf_session_arena_open(opf_session* s, const uint8_t* handles);
+opf_status opf_session_arena_link_local(opf_session* const* sessions, int32_t world, int64_t min_bytes);
 /* Bind an external tensor (GraphInput / Weight, or a GraphOutput destination)
  * to caller-owned device memory. */
 opf_status opf_session_bind(opf_session* s, const char* tensor, const opf_view* v);
@@ -153,6 +166,9 @@ opf_status opf_session_bind(opf_session* s, const char* tensor, const opf_view* 
  * ({"name":"sequential"|"split_overlap"|"dbo"|"fuse_norm_comm"|"nanoflow", ...}).
  * Record → Algorithm-1 plan → CUDA-graph capture on a cache miss, replay on a hit. */
 opf_status opf_session_run(opf_session* s, const char* strategy_json, void* stream);
+/* Plan, prepack and capture `strategy` for the bound row count without
+ * launching (virtual peer ranks on one device prepare every rank first). */
+opf_status opf_session_prepare(opf_session* s, const char* strategy, void* stream);
 /* User-programmable strategy: `schedule` is called with a scheduling context
  * on which it calls opf_sched_split / opf_sched_ready / opf_sched_execute. */
 typedef opf_status (*opf_schedule_fn)(opf_sched_ctx* ctx, void* user);

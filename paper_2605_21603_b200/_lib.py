@@ -81,6 +81,10 @@ _SIGS = {
     "opf_session_free": (None, [C.c_void_p]),
     "opf_session_bind": (C.c_int32, [C.c_void_p, C.c_char_p, C.POINTER(opf_view)]),
     "opf_session_run": (C.c_int32, [C.c_void_p, C.c_char_p, C.c_void_p]),
+    "opf_session_prepare": (C.c_int32, [C.c_void_p, C.c_char_p, C.c_void_p]),
+    "opf_session_arena_export": (C.c_int32, [C.c_void_p, C.c_int64, C.c_void_p]),
+    "opf_session_arena_open": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "opf_session_arena_link_local": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int64]),
     "opf_session_run_custom": (C.c_int32, [C.c_void_p, C.c_char_p, SCHEDULE_FN, C.c_void_p,
                                            C.c_void_p]),
     "opf_session_output": (C.c_int32, [C.c_void_p, C.c_char_p, C.POINTER(opf_view)]),

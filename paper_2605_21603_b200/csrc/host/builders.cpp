@@ -124,6 +124,8 @@ GraphDescription llama_graph(const LlamaShape& s) {
           "llama: tokens must be a multiple of seq_len");
   require(s.experts == 0 || (s.tp == 1 && s.topk >= 1 && s.topk <= s.experts), Errc::ConfigError,
           "moe: experts need tp == 1 and 1 <= topk <= experts");
+  require(s.ep >= 1 && s.ep <= 8 && (s.experts == 0 ? s.ep == 1 : s.experts % s.ep == 0), Errc::ConfigError,
+          "moe: ep must be 1..8 and divide experts");
   DescWriter w(s.dtype);
   const int64_t T = s.tokens, H = s.hidden, hd = s.head_dim;
   const int64_t nq = s.heads / s.tp, nkv = s.kv_heads / s.tp, I = s.inter / s.tp;
@@ -158,10 +160,10 @@ GraphDescription llama_graph(const LlamaShape& s) {
     const std::string wo = w.weight(p + ".o.w", {nq * hd, H});
     const std::string g2 = w.weight(p + ".mlp_norm.w", {H});
     const bool moe = s.experts > 0;
-    const int64_t E = s.experts, K = s.topk, MI = s.moe_inter;
-    const std::string wgu = moe ? w.weight(p + ".experts.gate_up.w", {E, H, 2 * MI})
+    const int64_t E = s.experts, K = s.topk, MI = s.moe_inter, EP = s.ep, El = moe ? E / EP : 0;
+    const std::string wgu = moe ? w.weight(p + ".experts.gate_up.w", {El, H, 2 * MI})
                                 : w.weight(p + ".gate_up.w", {H, 2 * I});
-    const std::string wd = moe ? w.weight(p + ".experts.down.w", {E, MI, H}) : w.weight(p + ".down.w", {I, H});
+    const std::string wd = moe ? w.weight(p + ".experts.down.w", {El, MI, H}) : w.weight(p + ".down.w", {I, H});
     if (s.decode) {
       const int64_t pages = s.num_pages ? s.num_pages : T * max_pages;
       kc = w.weight(p + ".k_cache", {pages, s.page_size, nkv, hd});
@@ -220,12 +222,8 @@ GraphDescription llama_graph(const LlamaShape& s) {
                                        TensorRole::kIntermediate, Dtype::kI64);
       const std::string wts = w.tensor(p + ".topk_w", {T, K}, BatchSemantics::kBatched,
                                        TensorRole::kIntermediate, Dtype::kF32);
-      const std::string xd = w.act(p + ".dispatched", {T, K * H});
-      const std::string slot = w.tensor(p + ".slot", {T, K}, BatchSemantics::kBatched,
-                                        TensorRole::kIntermediate, Dtype::kI64);
-      const std::string hd_ = w.act(p + ".expert_act", {T, K * MI});
-      const std::string yd = w.act(p + ".expert_out", {T, K * H});
-      const std::vector<std::pair<std::string, double>> mp = {{"experts", double(E)}, {"topk", double(K)}};
+      const std::vector<std::pair<std::string, double>> mp = {
+          {"experts", double(E)}, {"topk", double(K)}, {"ep", double(EP)}};
       auto params = [&](std::initializer_list<std::pair<const std::string, double>> extra) {
         std::map<std::string, double> m(mp.begin(), mp.end());
         for (const auto& kv : extra) m[kv.first] = kv.second;
@@ -236,18 +234,45 @@ GraphDescription llama_graph(const LlamaShape& s) {
       w.custom(p + ".topk", "moe_topk", {logits}, {ids, wts}, p + ".moe.topk", ResourceClass::kMemory,
                CostParams{2.0, E * 2.0 / 6.5e6})
           .attrs.params = params({{"renorm", 1.0}});
-      w.custom(p + ".dispatch", "moe_dispatch", {h2, ids}, {xd, slot}, p + ".moe.dispatch",
-               ResourceClass::kNetwork, CostParams{5.0, K * H * 4.0 / 6.5e6})
-          .attrs.params = params({});
-      w.custom(p + ".experts_gate_up", "moe_gate_up", {xd, ids, wgu}, {hd_}, p + ".moe.experts",
-               ResourceClass::kCompute, CostParams{2.0, K * 2.0 * H * 2 * MI / 1.4e9})
-          .attrs.params = params({});
-      w.custom(p + ".experts_down", "moe_down", {hd_, ids, wd}, {yd}, p + ".moe.experts",
-               ResourceClass::kCompute, CostParams{2.0, K * 2.0 * MI * H / 1.4e9})
-          .attrs.params = params({});
-      w.custom(p + ".combine", "moe_combine", {yd, slot, wts}, {dn}, p + ".moe.combine",
-               ResourceClass::kNetwork, CostParams{5.0, K * H * 2.0 / 6.5e6})
-          .attrs.params = params({});
+      const CostParams a2a{5.0, K * H * 4.0 / (EP > 1 ? 0.8e6 : 6.5e6)};
+      if (EP == 1) {
+        const std::string xd = w.act(p + ".dispatched", {T, K * H});
+        const std::string slot = w.tensor(p + ".slot", {T, K}, BatchSemantics::kBatched,
+                                          TensorRole::kIntermediate, Dtype::kI64);
+        const std::string hd_ = w.act(p + ".expert_act", {T, K * MI});
+        const std::string yd = w.act(p + ".expert_out", {T, K * H});
+        w.custom(p + ".dispatch", "moe_dispatch", {h2, ids}, {xd, slot}, p + ".moe.dispatch",
+                 ResourceClass::kNetwork, a2a)
+            .attrs.params = params({});
+        w.custom(p + ".experts_gate_up", "moe_gate_up", {xd, ids, wgu}, {hd_}, p + ".moe.experts",
+                 ResourceClass::kCompute, CostParams{2.0, K * 2.0 * H * 2 * MI / 1.4e9})
+            .attrs.params = params({});
+        w.custom(p + ".experts_down", "moe_down", {hd_, ids, wd}, {yd}, p + ".moe.experts",
+                 ResourceClass::kCompute, CostParams{2.0, K * 2.0 * MI * H / 1.4e9})
+            .attrs.params = params({});
+        w.custom(p + ".combine", "moe_combine", {yd, slot, wts}, {dn}, p + ".moe.combine",
+                 ResourceClass::kNetwork, CostParams{5.0, K * H * 2.0 / 6.5e6})
+            .attrs.params = params({});
+      } else {
+        // expert parallel: rows travel to the owner rank's arena and back
+        const std::string xr = w.act(p + ".dispatched", {T, EP * K * H});
+        const std::string rinfo = w.tensor(p + ".recv_info", {T, EP * K + El}, BatchSemantics::kBatched,
+                                           TensorRole::kIntermediate, Dtype::kI64);
+        const std::string hr = w.act(p + ".expert_act", {T, EP * K * MI});
+        const std::string yr = w.act(p + ".expert_out", {T, EP * K * H});
+        w.custom(p + ".dispatch", "moe_ep_dispatch", {h2, ids}, {xr, rinfo}, p + ".moe.dispatch",
+                 ResourceClass::kNetwork, a2a)
+            .attrs.params = params({});
+        w.custom(p + ".experts_gate_up", "moe_gate_up", {xr, rinfo, wgu}, {hr}, p + ".moe.experts",
+                 ResourceClass::kCompute, CostParams{2.0, K * 2.0 * H * 2 * MI / 1.4e9})
+            .attrs.params = params({});
+        w.custom(p + ".experts_down", "moe_down", {hr, rinfo, wd}, {yr}, p + ".moe.experts",
+                 ResourceClass::kCompute, CostParams{2.0, K * 2.0 * MI * H / 1.4e9})
+            .attrs.params = params({});
+        w.custom(p + ".combine", "moe_ep_combine", {yr, rinfo, wts, ids}, {dn}, p + ".moe.combine",
+                 ResourceClass::kNetwork, a2a)
+            .attrs.params = params({});
+      }
     } else {
       const std::string gu = w.act(p + ".gu", {T, 2 * I});
       const std::string a = w.act(p + ".act", {T, I});
@@ -375,6 +400,7 @@ std::string build_json(const std::string& name, const std::string& params_json) 
     s.experts = geti(p, "experts", s.experts);
     s.topk = geti(p, "topk", s.topk);
     s.moe_inter = geti(p, "moe_inter", s.moe_inter);
+    s.ep = geti(p, "ep", s.ep);
     s.qk_norm = geti(p, "qk_norm", s.qk_norm ? 1 : 0) != 0;
     if (dtv) s.dtype = dt;
     return description_to_json(llama_graph(s));

@@ -344,6 +344,7 @@ void opf_comm_free(opf_comm* c) {
   if (!c) return;
   if (c->nccl) nccl().CommDestroy(c->nccl);
   for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  for (void* p : c->opened_arenas) cudaIpcCloseMemHandle(p);
   if (c->window_base) cudaFree(c->window_base);
   delete c;
 }
@@ -406,6 +407,51 @@ opf_status opf_session_create(const opf_graph* g, const opf_plan* p, const char*
 
 void opf_session_free(opf_session* s) { delete s; }
 
+opf_status opf_session_arena_export(opf_session* s, int64_t min_bytes, uint8_t ipc_handle_out[64]) {
+  return guard([&] {
+    need(s, "session");
+    void* base = s->s->export_arena(min_bytes);
+    if (ipc_handle_out) {
+      cudaIpcMemHandle_t h;
+      OPF_CUDA(cudaIpcGetMemHandle(&h, base));
+      std::memcpy(ipc_handle_out, &h, sizeof(h));
+    }
+  });
+}
+
+opf_status opf_session_arena_open(opf_session* s, const uint8_t* handles) {
+  return guard([&] {
+    need(s, "session");
+    need(handles, "handles");
+    opf_comm* c = s->s->comm();
+    require(c != nullptr, Errc::ConfigError, "session has no communicator");
+    std::vector<void*> bases(c->world, nullptr);
+    for (int p = 0; p < c->world; ++p) {
+      if (p == c->rank) {
+        bases[p] = s->s->export_arena(0);
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + p * sizeof(cudaIpcMemHandle_t), sizeof(h));
+      OPF_CUDA(cudaIpcOpenMemHandle(&bases[p], h, cudaIpcMemLazyEnablePeerAccess));
+      c->opened_arenas.push_back(bases[p]);
+    }
+    s->s->set_peer_arenas(bases);
+  });
+}
+
+opf_status opf_session_arena_link_local(opf_session* const* sessions, int32_t world, int64_t min_bytes) {
+  return guard([&] {
+    need(sessions, "sessions");
+    std::vector<void*> bases;
+    for (int r = 0; r < world; ++r) {
+      need(sessions[r], "session");
+      bases.push_back(sessions[r]->s->export_arena(min_bytes));
+    }
+    for (int r = 0; r < world; ++r) sessions[r]->s->set_peer_arenas(bases);
+  });
+}
+
 opf_status opf_session_bind(opf_session* s, const char* tensor, const opf_view* v) {
   return guard([&] {
     need(s, "session");
@@ -421,6 +467,15 @@ opf_status opf_session_run(opf_session* s, const char* strategy, void* stream) {
     auto cs = s->s->choose(spec, static_cast<cudaStream_t>(stream));
     auto strat = make_strategy(cs);
     s->s->run(*strat, "builtin:" + cs, static_cast<cudaStream_t>(stream));
+  });
+}
+
+opf_status opf_session_prepare(opf_session* s, const char* strategy, void* stream) {
+  return guard([&] {
+    need(s, "session");
+    const std::string spec = strategy ? strategy : "{}";
+    auto strat = make_strategy(spec);
+    s->s->prepare(*strat, "builtin:" + spec, static_cast<cudaStream_t>(stream));
   });
 }
 

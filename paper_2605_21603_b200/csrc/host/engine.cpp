@@ -8,6 +8,7 @@
 #include <functional>
 #include <numeric>
 
+#include "opflow/comm.hpp"
 #include "opflow/json.hpp"
 
 namespace opflow {
@@ -220,12 +221,32 @@ void Session::warm_aux(const CompiledPlan& cp) {
 
 void Session::ensure_arena(int64_t bytes) {
   if (bytes <= arena_bytes_) return;
+  require(!arena_pinned_, Errc::ConfigError,
+          "plan needs a " + std::to_string(bytes) + "-byte arena but the arena is peer-mapped at " +
+              std::to_string(arena_bytes_) + " bytes (export a larger arena before mapping peers)");
   if (arena_) {
     OPF_CUDA(cudaDeviceSynchronize());
     OPF_CUDA(cudaFree(arena_));
   }
   OPF_CUDA(cudaMalloc(&arena_, bytes));
   arena_bytes_ = bytes;
+}
+
+void* Session::export_arena(int64_t bytes) {
+  require(!dry_, Errc::ConfigError, "dry sessions have no arena");
+  require(comm_ != nullptr, Errc::ConfigError, "peer arena needs a communicator");
+  ensure_arena(std::max<int64_t>(bytes, 1));
+  arena_pinned_ = true;
+  return arena_;
+}
+
+void Session::set_peer_arenas(const std::vector<void*>& bases) {
+  require(comm_ != nullptr && static_cast<int>(bases.size()) == comm_->world, Errc::ConfigError,
+          "peer arenas: one base per rank");
+  require(arena_pinned_ && bases[comm_->rank] == arena_, Errc::ConfigError, "export the arena first");
+  comm_->arena_base = arena_;
+  comm_->arena_bytes = static_cast<size_t>(arena_bytes_);
+  comm_->peer_arena = bases;
 }
 
 std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const std::string& key,
@@ -304,6 +325,7 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
     return v;
   };
 
+  int32_t last_comm = -1;
   for (int32_t di = 0; di < nd; ++di) {
     const Dispatch& d = ds[di];
     PlannedDispatch pd;
@@ -353,6 +375,16 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
                 "tensor '" + m.name + "' ubatch " + std::to_string(u) + " already reclaimed");
         deps.insert(inst[t][u].producer);
       }
+    }
+    // Communicating dispatches form one global chain, identical on every rank:
+    // two collectives (NCCL, or peer-window kernels sharing the staging window and
+    // flags) must never run concurrently on different lanes.
+    bool comm_dispatch = false;
+    if (comm_ && comm_->world > 1)
+      for (int32_t op : ops) comm_dispatch = comm_dispatch || g_.ops[op].resource_class == ResourceClass::kNetwork;
+    if (comm_dispatch) {
+      if (last_comm >= 0) deps.insert(last_comm);
+      last_comm = di;
     }
     // vector clock of this dispatch
     std::vector<int32_t>& my = vc[di];
@@ -838,17 +870,23 @@ std::string Session::choose(const std::string& spec, cudaStream_t stream) {
 }
 
 void Session::run(Scheduler& strat, const std::string& key_in, cudaStream_t stream) {
-  require(!dry_, Errc::EngineStopped, "dry session cannot execute");
-  CompiledPlan* cp = lookup_or_build(strat, key_in);
+  CompiledPlan* cp = prepare(strat, key_in, stream);
   last_ = cp;
-  ensure_packed_for(*cp, stream);
-  ensure_arena(cp->arena_bytes);
-  warm_aux(*cp);
   if (!cfg_.cuda_graph) {
     launch_plan(*cp, stream, false);
     OPF_CUDA(cudaGetLastError());
     return;
   }
+  OPF_CUDA(cudaGraphLaunch(cp->exec, stream));
+}
+
+CompiledPlan* Session::prepare(Scheduler& strat, const std::string& key_in, cudaStream_t stream) {
+  require(!dry_, Errc::EngineStopped, "dry session cannot execute");
+  CompiledPlan* cp = lookup_or_build(strat, key_in);
+  ensure_packed_for(*cp, stream);
+  ensure_arena(cp->arena_bytes);
+  warm_aux(*cp);
+  if (!cfg_.cuda_graph) return cp;
   if (!cp->exec || cp->arena_base_at_capture != arena_) {
     if (cp->exec) {
       OPF_CUDA(cudaGraphExecDestroy(cp->exec));
@@ -875,7 +913,7 @@ void Session::run(Scheduler& strat, const std::string& key_in, cudaStream_t stre
     OPF_CUDA(cudaStreamDestroy(cap));
     cp->arena_base_at_capture = arena_;
   }
-  OPF_CUDA(cudaGraphLaunch(cp->exec, stream));
+  return cp;
 }
 
 opf_view Session::output(const std::string& name) {

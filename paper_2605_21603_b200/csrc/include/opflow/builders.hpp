@@ -52,6 +52,7 @@ struct LlamaShape {
   int64_t experts = 0;
   int64_t topk = 8;
   int64_t moe_inter = 768;
+  int64_t ep = 1;  // expert parallelism: this rank holds experts / ep experts' weights
 };
 
 GraphDescription llama_graph(const LlamaShape& s);

@@ -29,6 +29,11 @@ struct opf_comm {
   size_t window_bytes = 0;
   std::vector<void*> opened;        // IPC-opened peer windows (closed on free)
   bool virtual_rank = false;        // one-device test rank (no NCCL)
+  // Symmetric session arenas (expert-parallel ops write peers' tensors directly)
+  void* arena_base = nullptr;       // my arena
+  size_t arena_bytes = 0;
+  std::vector<void*> peer_arena;    // [world] (mine included)
+  std::vector<void*> opened_arenas; // IPC-opened peer arenas (closed on free)
 };
 
 namespace opflow {

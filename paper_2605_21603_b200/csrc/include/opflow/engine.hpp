@@ -213,6 +213,11 @@ class Session {
   // rows, and return its spec; any other spec is returned unchanged.
   std::string choose(const std::string& spec, cudaStream_t stream);
   void run(Scheduler& strat, const std::string& key, cudaStream_t stream);
+  // Everything run() does except the launch: plan (cached), prepack weights,
+  // size the arena, capture the CUDA graph.  Peer-memory ranks sharing one
+  // device prepare all ranks before launching any (no allocation may then
+  // synchronise the device while a peer's barrier kernel spins).
+  CompiledPlan* prepare(Scheduler& strat, const std::string& key, cudaStream_t stream);
   opf_view output(const std::string& tensor);
   std::string stats_json() const;
   std::string schedule_json() const;
@@ -221,6 +226,15 @@ class Session {
   const Graph& graph() const { return g_; }
   const PartitionPlan& plan() const { return p_; }
   int64_t rows() const;
+
+  // Symmetric arena for peer-memory ops (expert-parallel dispatch / combine):
+  // every rank compiles the same plans, so a tensor lives at the same arena
+  // offset on every rank.  export_arena() allocates at least `bytes` and pins
+  // the arena (later plans must fit); set_peer_arenas() hands all ranks' bases
+  // (mine included) to the communicator.
+  void* export_arena(int64_t bytes);
+  void set_peer_arenas(const std::vector<void*>& bases);
+  opf_comm* comm() const { return comm_; }
 
  private:
   std::unique_ptr<CompiledPlan> compile(const SchedContext& ctx, const std::string& key,
@@ -244,6 +258,7 @@ class Session {
   bool prepack_dirty_ = true;
   void* arena_ = nullptr;
   int64_t arena_bytes_ = 0;
+  bool arena_pinned_ = false;  // peer-mapped: never reallocated
   std::map<std::string, std::unique_ptr<CompiledPlan>> cache_;
   std::map<std::pair<uint64_t, int64_t>, void*> perms_;
   CompiledPlan* last_ = nullptr;

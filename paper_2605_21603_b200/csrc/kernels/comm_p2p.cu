@@ -22,52 +22,17 @@
 
 #include "opflow/comm.hpp"
 #include "opflow/device.hpp"
+#include "opflow/p2p.cuh"
 
 namespace opflow {
 
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kMaxWorld = 8;
-constexpr int kMaxCtas = 1024;
-constexpr int64_t kSpinLimit = 1ll << 24;  // ~seconds: error flag instead of a hung GPU
 
-struct PeerPtrs {
-  const __nv_bfloat16* buf[kMaxWorld];  // staging rows of each rank
-  uint32_t* flags[kMaxWorld];           // flag arrays of each rank [kMaxCtas][kMaxWorld]
-};
-
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ bool cta_barrier(const PeerPtrs& pp, uint32_t* my_epoch, int world, int rank,
-                            uint32_t* err) {
-  __syncthreads();
-  __shared__ uint32_t ok;
-  if (threadIdx.x == 0) {
-    ok = 1;
-    const uint32_t e = ++my_epoch[blockIdx.x];
-    __threadfence_system();
-    for (int p = 0; p < world; ++p) st_release(pp.flags[p] + blockIdx.x * kMaxWorld + rank, e);
-    for (int p = 0; p < world; ++p) {
-      int64_t spins = 0;
-      while (ld_acquire(pp.flags[rank] + blockIdx.x * kMaxWorld + p) < e) {
-        if (++spins > kSpinLimit) {
-          atomicExch(err, 1u);
-          ok = 0;
-          break;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  return ok != 0;
+__device__ __forceinline__ bool cta_barrier(const PeerPtrs& pp, uint32_t* my_epoch, int world, int rank,
+                                            uint32_t* err) {
+  return slot_barrier(pp, my_epoch, blockIdx.x, world, rank, err);
 }
 
 __global__ void __launch_bounds__(kThreads) ar_add_rmsnorm_p2p_kernel(
@@ -100,7 +65,7 @@ __global__ void __launch_bounds__(kThreads) ar_add_rmsnorm_p2p_kernel(
         }
       }
       for (int p = 0; p < world; ++p) {
-        const uint4 u = reinterpret_cast<const uint4*>(pp.buf[p] + r * H)[c];
+        const uint4 u = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(pp.buf[p]) + r * H)[c];
         const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -150,7 +115,7 @@ __global__ void __launch_bounds__(kThreads) allreduce_p2p_kernel(
     for (int64_t c = threadIdx.x; c < n8; c += kThreads) {
       float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int p = 0; p < world; ++p) {
-        const uint4 u = reinterpret_cast<const uint4*>(pp.buf[p] + r * H)[c];
+        const uint4 u = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(pp.buf[p]) + r * H)[c];
         const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -168,12 +133,6 @@ __global__ void __launch_bounds__(kThreads) allreduce_p2p_kernel(
   cta_barrier(pp, my_epoch, world, rank, err);
 }
 
-size_t window_layout(size_t stage_bytes, size_t* flags_off, size_t* epoch_off) {
-  const size_t s = (stage_bytes + 255) / 256 * 256;
-  *flags_off = s;
-  *epoch_off = s + sizeof(uint32_t) * kMaxCtas * kMaxWorld;
-  return *epoch_off + sizeof(uint32_t) * kMaxCtas + sizeof(uint32_t) /*error flag*/;
-}
 
 }  // namespace
 
@@ -248,12 +207,12 @@ bool ar_add_rmsnorm_p2p(const opf_comm* c, const opf_view& o, const opf_view& x,
   window_layout(c->peer_bytes, &fo, &eo);
   PeerPtrs pp{};
   for (int p = 0; p < c->world; ++p) {
-    pp.buf[p] = static_cast<const __nv_bfloat16*>(c->peer_buf[p]);
+    pp.buf[p] = c->peer_buf[p];
     pp.flags[p] = c->peer_flag[p];
   }
   char* base = static_cast<char*>(c->window_base);
   int grid = max_ctas > 0 ? max_ctas : num_sms();
-  grid = static_cast<int>(std::min<int64_t>(std::min(grid, kMaxCtas), rows));
+  grid = static_cast<int>(std::min<int64_t>(std::min(grid, kBarrierSlot), rows));
   ar_add_rmsnorm_p2p_kernel<<<std::max(grid, 1), kThreads, H * sizeof(float), s>>>(
       pp, c->world, c->rank, vptr<__nv_bfloat16>(o), reinterpret_cast<__nv_bfloat16*>(base),
       reinterpret_cast<uint32_t*>(base + eo), vptr<__nv_bfloat16>(x), vptr<__nv_bfloat16>(g),
@@ -271,12 +230,12 @@ bool allreduce_p2p(const opf_comm* c, const opf_view& in, opf_view& out, int64_t
   window_layout(c->peer_bytes, &fo, &eo);
   PeerPtrs pp{};
   for (int p = 0; p < c->world; ++p) {
-    pp.buf[p] = static_cast<const __nv_bfloat16*>(c->peer_buf[p]);
+    pp.buf[p] = c->peer_buf[p];
     pp.flags[p] = c->peer_flag[p];
   }
   char* base = static_cast<char*>(c->window_base);
   int grid = max_ctas > 0 ? max_ctas : num_sms();
-  grid = static_cast<int>(std::min<int64_t>(std::min(grid, kMaxCtas), rows));
+  grid = static_cast<int>(std::min<int64_t>(std::min(grid, kBarrierSlot), rows));
   allreduce_p2p_kernel<<<std::max(grid, 1), kThreads, 0, s>>>(
       pp, c->world, c->rank, vptr<__nv_bfloat16>(in), reinterpret_cast<__nv_bfloat16*>(base),
       reinterpret_cast<uint32_t*>(base + eo), vptr<__nv_bfloat16>(out), rows, H,

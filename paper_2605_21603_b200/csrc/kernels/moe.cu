@@ -27,6 +27,7 @@
 #include <cfloat>
 
 #include "opflow/device.hpp"
+#include "opflow/p2p.cuh"
 
 namespace opflow {
 
@@ -129,7 +130,8 @@ __global__ void __launch_bounds__(256) route_hist_kernel(const int64_t* __restri
 // One CTA: base[c][e] = off[e] + sum_{c' < c} cnt[c'][e]  (in place over cnt),
 // and (optionally) the grouped-GEMM tile table.
 __global__ void __launch_bounds__(1024) route_scan_kernel(int32_t* __restrict__ cnt, int chunks, int E,
-                                                          int32_t* __restrict__ gtab, int tile_m) {
+                                                          int32_t* __restrict__ gtab, int tile_m,
+                                                          int32_t* __restrict__ tot_out, int32_t* __restrict__ off_out) {
   pdl_wait();
   __shared__ int32_t tot[kMaxE], off[kMaxE + 1], toff[kMaxE + 1];
   const int e = threadIdx.x;
@@ -157,6 +159,8 @@ __global__ void __launch_bounds__(1024) route_scan_kernel(int32_t* __restrict__ 
   __syncthreads();
   if (e < E) {
     const int32_t o = off[e];
+    if (tot_out) tot_out[e] = tot[e];
+    if (off_out) off_out[e] = o;
     for (int c = 0; c < chunks; ++c) cnt[static_cast<int64_t>(c) * E + e] += o;
     if (gtab) {
       const int32_t end = o + tot[e];
@@ -243,6 +247,152 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
   }
 }
 
+// ---------------------------------------------------------------- expert parallel
+// W ranks, rank r owns experts [r*El, (r+1)*El).  Every rank runs the same
+// plan, so a tensor sits at the same arena offset everywhere: peers write the
+// dispatched rows straight into the owner's xr tensor (and results straight
+// back into the source's yc tensor) over NVLink.  Receive layout on the owner:
+// rows sorted by (local expert, source rank, source slot order); rinfo =
+// [El per-local-expert row counts | per-row source code (rank * T*k + slot)].
+struct PeerArena {
+  char* base[kMaxWorld];
+};
+
+// counts all-gather through the window + the offsets every rank derives from it
+__global__ void __launch_bounds__(1024) ep_exchange_kernel(PeerPtrs pp, uint32_t* epochs, uint32_t* err, int W,
+                                                           int rank, int E, int El,
+                                                           const int32_t* __restrict__ tot,
+                                                           int32_t* __restrict__ send_off,
+                                                           int64_t* __restrict__ rinfo_head) {
+  pdl_wait();
+  if (!slot_barrier(pp, epochs, kBarrierSlot, W, rank, err)) return;  // all ranks reached the dispatch
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    for (int p = 0; p < W; ++p) static_cast<int32_t*>(const_cast<void*>(pp.buf[p]))[rank * E + e] = tot[e];
+  __threadfence_system();
+  if (!slot_barrier(pp, epochs, kBarrierSlot, W, rank, err)) return;  // count matrix complete
+  const int32_t* M = static_cast<const int32_t*>(pp.buf[rank]);         // [W][E]
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int o = e / El, el = e % El;
+    int32_t acc = 0;
+    for (int e2 = o * El; e2 < o * El + el; ++e2)
+      for (int src = 0; src < W; ++src) acc += M[src * E + e2];
+    for (int src = 0; src < rank; ++src) acc += M[src * E + e];
+    send_off[e] = acc;
+  }
+  for (int el = threadIdx.x; el < El; el += blockDim.x) {
+    int32_t r = 0;
+    for (int src = 0; src < W; ++src) r += M[src * E + rank * El + el];
+    rinfo_head[el] = r;
+  }
+  pdl_trigger();
+}
+
+// one warp per local slot: row x[s / k] -> owner's xr, source code -> owner's rinfo
+__global__ void __launch_bounds__(256) ep_send_kernel(PeerArena pa, int64_t xr_off, int64_t rinfo_off,
+                                                      const __nv_bfloat16* __restrict__ x,
+                                                      const int64_t* __restrict__ ids,
+                                                      const int64_t* __restrict__ slot_local,
+                                                      const int32_t* __restrict__ off_local,
+                                                      const int32_t* __restrict__ send_off, int64_t n, int k,
+                                                      int64_t H, int E, int El, int rank) {
+  pdl_wait();
+  const int lane = threadIdx.x % 32;
+  for (int64_t s = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; s < n;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    const int64_t e = ids[s];
+    if (!valid_id(e, E)) continue;
+    const int o = static_cast<int>(e / El);
+    const int64_t dest = send_off[e] + (slot_local[s] - off_local[e]);
+    const uint4* src = reinterpret_cast<const uint4*>(x + (s / k) * H);
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(pa.base[o] + xr_off) + dest * H);
+    for (int64_t i = lane; i < H / 8; i += 32) dst[i] = src[i];
+    if (lane == 0) reinterpret_cast<int64_t*>(pa.base[o] + rinfo_off)[El + dest] = static_cast<int64_t>(rank) * n + s;
+  }
+  __threadfence_system();
+}
+
+__global__ void ep_barrier_kernel(PeerPtrs pp, uint32_t* epochs, uint32_t* err, int W, int rank) {
+  pdl_wait();
+  slot_barrier(pp, epochs, kBarrierSlot, W, rank, err);
+  pdl_trigger();
+}
+
+// one warp per received row: expert output row -> the source rank's yc[slot]
+__global__ void __launch_bounds__(256) ep_return_kernel(PeerArena pa, int64_t yc_off,
+                                                        const __nv_bfloat16* __restrict__ yr,
+                                                        const int64_t* __restrict__ rinfo, int El, int64_t n,
+                                                        int64_t H) {
+  pdl_wait();
+  __shared__ int64_t n_recv;
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int el = 0; el < El; ++el) t += rinfo[el];
+    n_recv = t;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x % 32;
+  for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; i < n_recv;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    const int64_t code = rinfo[El + i];
+    const int p = static_cast<int>(code / n);
+    const int64_t s = code % n;
+    const uint4* src = reinterpret_cast<const uint4*>(yr + i * H);
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(pa.base[p] + yc_off) + s * H);
+    for (int64_t c = lane; c < H / 8; c += 32) dst[c] = src[c];
+  }
+  __threadfence_system();
+}
+
+// y[t] = sum_j w[t,j] * yc[t*k + j]  (valid ids only, j ascending)
+__global__ void __launch_bounds__(256) combine_slots_kernel(const __nv_bfloat16* __restrict__ yc,
+                                                            const int64_t* __restrict__ ids,
+                                                            const float* __restrict__ w, int k, int E, int64_t H,
+                                                            __nv_bfloat16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t t = blockIdx.x;
+  for (int64_t c = threadIdx.x; c < H / 8; c += blockDim.x) {
+    float acc[8] = {};
+    for (int j = 0; j < k; ++j) {
+      if (!valid_id(ids[t * k + j], E)) continue;
+      const float wj = w[t * k + j];
+      const uint4 u = *reinterpret_cast<const uint4*>(yc + (t * k + j) * H + c * 8);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h2[i]);
+        acc[2 * i] += wj * f.x;
+        acc[2 * i + 1] += wj * f.y;
+      }
+    }
+    uint4 o;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o2[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+    *reinterpret_cast<uint4*>(y + t * H + c * 8) = o;
+  }
+}
+
+// grouped-GEMM tile table from per-local-expert row counts (EP receive side)
+__global__ void tiles_from_counts_kernel(const int64_t* __restrict__ counts, int El, int32_t* __restrict__ gtab,
+                                         int tile_m) {
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    int32_t row = 0, t = 0;
+    for (int el = 0; el < El; ++el) {
+      const int32_t c = static_cast<int32_t>(counts[el]);
+      for (int32_t r = 0; r < c; r += tile_m, ++t) {
+        gtab[1 + 3 * t] = row + r;
+        gtab[2 + 3 * t] = row + c;
+        gtab[3 + 3 * t] = el;
+      }
+      row += c;
+    }
+    gtab[0] = t;
+  }
+  pdl_trigger();
+}
+
 // ---------------------------------------------------------------- host ops
 int64_t chunks_of(int64_t n) { return (n + kChunk - 1) / kChunk; }
 int64_t max_tiles(int64_t n, int E) { return n / 128 + E + 1; }
@@ -252,11 +402,12 @@ int topk_param(const opf_op_ctx& c) { return static_cast<int>(ctx_param(c, "topk
 int experts_param(const opf_op_ctx& c) { return static_cast<int>(ctx_param(c, "experts", 128)); }
 
 // route: histogram + scan (+ tile table); returns the per-chunk bases in ws
-void route_plan(const int64_t* ids, int64_t n, int E, char* ws, int32_t* gtab, cudaStream_t s) {
+void route_plan(const int64_t* ids, int64_t n, int E, char* ws, int32_t* gtab, cudaStream_t s,
+                int32_t* tot = nullptr, int32_t* off = nullptr) {
   auto* cnt = reinterpret_cast<int32_t*>(ws);
   const int64_t C = chunks_of(n);
   if (C > 0) launch_pdl(route_hist_kernel, dim3(static_cast<unsigned>(C)), dim3(256), 0, s, ids, n, E, cnt);
-  launch_pdl(route_scan_kernel, dim3(1), dim3(1024), 0, s, cnt, static_cast<int>(C), E, gtab, 128);
+  launch_pdl(route_scan_kernel, dim3(1), dim3(1024), 0, s, cnt, static_cast<int>(C), E, gtab, 128, tot, off);
 }
 
 opf_status op_moe_topk(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out, int32_t n_out,
@@ -328,31 +479,55 @@ opf_status op_moe_dispatch(const opf_op_ctx* c, const opf_view* in, int32_t n_in
   return launch_status("moe_dispatch");
 }
 
-// shared body of the two grouped expert GEMMs
+int ep_param(const opf_op_ctx& c) { return static_cast<int>(ctx_param(c, "ep", 1)); }
+
+size_t ws_grouped_any(const opf_op_ctx& c, const opf_view* in, int n_in, const opf_view* out, int n_out,
+                      int64_t rows) {
+  const int ep = ep_param(c);
+  if (ep <= 1) return ws_grouped(c, in, n_in, out, n_out, rows);
+  const int64_t n = rows * topk_param(c) * ep;
+  return align256(static_cast<size_t>(1 + 3 * max_tiles(n, experts_param(c) / ep)) * 4) + 256;
+}
+
+// shared body of the two grouped expert GEMMs.  ep == 1: (act, ids, w[E,K,N]),
+// tile table from a routing pass over ids.  ep > 1: (act = received rows,
+// rinfo, w = this rank's [E/ep, K, N] shard), tile table from rinfo's counts.
 opf_status grouped(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out, int32_t n_out,
                    int64_t rows, void* stream, bool gate_up) {
   const char* who = gate_up ? "moe_gate_up" : "moe_down";
-  if (n_in != 3 || n_out != 1) return op_error(Errc::ShapeMismatch, std::string(who) + " takes (act, ids, w) -> out");
-  const int k = topk_param(*c), E = experts_param(*c);
-  // w: [E, K, N] reference layout (per-expert [K,N] MatMul weight)
-  if (in[2].rank != 3 || in[2].shape[0] != E || in[0].dtype != OPF_BF16 || in[2].dtype != OPF_BF16 ||
-      out[0].dtype != OPF_BF16 || view_row_elems(in[1]) != k)
-    return op_error(Errc::ShapeMismatch, std::string(who) + ": w must be [E, K, N] bf16, ids [T, k]");
+  if (n_in != 3 || n_out != 1) return op_error(Errc::ShapeMismatch, std::string(who) + " takes (act, ids|rinfo, w) -> out");
+  const int k = topk_param(*c), ep = ep_param(*c), E = experts_param(*c);
+  if (ep < 1 || E % ep) return op_error(Errc::ConfigError, std::string(who) + ": experts % ep");
+  const int El = E / ep;  // experts whose weights this rank holds
+  // w: [El, K, N] reference layout (per-expert [K,N] MatMul weight)
+  const int64_t route_w = ep == 1 ? k : static_cast<int64_t>(ep) * k + El;
+  if (in[2].rank != 3 || in[2].shape[0] != El || in[0].dtype != OPF_BF16 || in[2].dtype != OPF_BF16 ||
+      out[0].dtype != OPF_BF16 || view_row_elems(in[1]) != route_w || in[1].dtype != OPF_I64)
+    return op_error(Errc::ShapeMismatch, std::string(who) + ": w must be [experts/ep, K, N] bf16, ids [T, k] "
+                                                            "(ep 1) or rinfo [T, ep*k + experts/ep] (ep > 1)");
   const int64_t K = in[2].shape[1], N = in[2].shape[2];
   const int64_t n_out_cols = gate_up ? N / 2 : N;
-  if (view_row_elems(in[0]) != k * K || view_row_elems(out[0]) != k * n_out_cols)
+  const int64_t slots = static_cast<int64_t>(k) * ep;  // row capacity per token
+  if (view_row_elems(in[0]) != slots * K || view_row_elems(out[0]) != slots * n_out_cols)
     return op_error(Errc::ShapeMismatch, std::string(who) + ": activation widths");
   if (rows == 0) return 0;
   const void* packed = c->aux ? c->aux : (ctx_param(*c, "packed", 0.0) != 0.0 ? view_ptr(in[2]) : nullptr);
   if (!packed)
     return op_error(Errc::ConfigError, std::string(who) + ": expert weights not packed (run through a Session, "
                                                           "or pass packed [E,N,K] weights with params.packed=1)");
-  if (opf_status e = need_ws(c, ws_grouped(*c, in, n_in, out, n_out, rows), who)) return e;
+  if (opf_status e = need_ws(c, ws_grouped_any(*c, in, n_in, out, n_out, rows), who)) return e;
   auto s = static_cast<cudaStream_t>(stream);
-  const int64_t n = rows * k;
+  const int64_t n = rows * slots;
   char* ws = static_cast<char*>(c->workspace);
-  auto* gtab = reinterpret_cast<int32_t*>(ws + align256(static_cast<size_t>(chunks_of(n)) * E * 4));
-  route_plan(vptr<int64_t>(in[1]), n, E, ws, gtab, s);
+  int32_t* gtab;
+  if (ep == 1) {
+    gtab = reinterpret_cast<int32_t*>(ws + align256(static_cast<size_t>(chunks_of(n)) * E * 4));
+    route_plan(vptr<int64_t>(in[1]), n, E, ws, gtab, s);
+  } else {
+    gtab = reinterpret_cast<int32_t*>(ws);
+    launch_pdl(tiles_from_counts_kernel, dim3(1), dim3(32), 0, s, static_cast<const int64_t*>(vptr<int64_t>(in[1])),
+               El, gtab, 128);
+  }
   GemmArgs g{};
   g.a = view_ptr(in[0]);
   g.bt = packed;
@@ -364,8 +539,132 @@ opf_status grouped(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_vi
   g.ldc = n_out_cols;
   g.max_ctas = c->max_ctas;
   g.epi = gate_up ? 1 : 0;
-  gemm_bf16_grouped(g, gtab, max_tiles(n, E), N, E, s);
+  gemm_bf16_grouped(g, gtab, max_tiles(n, El), N, El, s);
   return launch_status(who);
+}
+
+// ---- expert-parallel dispatch / combine (peer-arena all-to-all)
+struct EpCtx {
+  WindowView w;
+  PeerArena pa{};
+  int W = 1, rank = 0;
+};
+opf_status ep_ctx(const opf_op_ctx* c, const char* who, EpCtx* x, std::initializer_list<const opf_view*> arena_views) {
+  const opf_comm* cm = static_cast<const opf_comm*>(c->comm);
+  const int ep = ep_param(*c);
+  if (!cm || cm->world != ep || ep > kMaxWorld)
+    return op_error(Errc::ConfigError, std::string(who) + ": needs a communicator with world == params.ep (<= 8)");
+  if (!window_view(cm, &x->w))
+    return op_error(Errc::ConfigError, std::string(who) + ": communicator has no peer window");
+  if (cm->peer_arena.size() != static_cast<size_t>(ep) || !cm->arena_base)
+    return op_error(Errc::ConfigError, std::string(who) + ": peer arenas not mapped (opf_session_arena_open / _link_local)");
+  const char* base = static_cast<const char*>(cm->arena_base);
+  for (const opf_view* v : arena_views) {
+    const char* p = view_ptr(*v);
+    if (p < base || p >= base + cm->arena_bytes)
+      return op_error(Errc::ConfigError, std::string(who) + ": peer-written tensors must live in the session arena");
+  }
+  for (int r = 0; r < ep; ++r) x->pa.base[r] = static_cast<char*>(cm->peer_arena[r]);
+  x->W = ep;
+  x->rank = cm->rank;
+  return 0;
+}
+
+size_t ws_ep_dispatch(const opf_op_ctx& c, const opf_view*, int, const opf_view*, int, int64_t rows) {
+  const int64_t n = rows * topk_param(c);
+  const int E = experts_param(c);
+  return align256(static_cast<size_t>(chunks_of(n)) * E * 4) + align256(static_cast<size_t>(n) * 8) +
+         3 * align256(static_cast<size_t>(E) * 4) + 256;
+}
+
+opf_status op_moe_ep_dispatch(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out,
+                              int32_t n_out, int64_t rows, void* stream) {
+  if (n_in != 2 || n_out != 2)
+    return op_error(Errc::ShapeMismatch, "moe_ep_dispatch takes (x, ids) -> (xr, rinfo)");
+  const int k = topk_param(*c), E = experts_param(*c), ep = ep_param(*c);
+  if (ep < 2 || E % ep || E > kMaxE) return op_error(Errc::ConfigError, "moe_ep_dispatch: ep >= 2 dividing experts");
+  const int El = E / ep;
+  const int64_t H = view_row_elems(in[0]);
+  if (in[0].dtype != OPF_BF16 || out[0].dtype != OPF_BF16 || H % 8 || view_row_elems(in[1]) != k ||
+      view_row_elems(out[0]) != static_cast<int64_t>(ep) * k * H || out[1].dtype != OPF_I64 ||
+      view_row_elems(out[1]) != static_cast<int64_t>(ep) * k + El)
+    return op_error(Errc::ShapeMismatch,
+                    "moe_ep_dispatch: x [T,H] bf16, ids [T,k] -> xr [T, ep*k*H] bf16, rinfo [T, ep*k + experts/ep] i64");
+  EpCtx x;
+  if (opf_status e = ep_ctx(c, "moe_ep_dispatch", &x, {&out[0], &out[1]})) return e;
+  if (x.w.stage_bytes < static_cast<size_t>(ep) * E * 4)
+    return op_error(Errc::ConfigError, "moe_ep_dispatch: peer window smaller than the count matrix");
+  if (opf_status e = need_ws(c, ws_ep_dispatch(*c, in, n_in, out, n_out, rows), "moe_ep_dispatch")) return e;
+  auto s = static_cast<cudaStream_t>(stream);
+  const int64_t n = rows * k;
+  char* ws = static_cast<char*>(c->workspace);
+  auto* cnt = reinterpret_cast<int32_t*>(ws);
+  auto* slot_local = reinterpret_cast<int64_t*>(ws + align256(static_cast<size_t>(chunks_of(n)) * E * 4));
+  auto* tot = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(slot_local) + align256(static_cast<size_t>(n) * 8));
+  auto* off = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(tot) + align256(static_cast<size_t>(E) * 4));
+  auto* send_off = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(off) + align256(static_cast<size_t>(E) * 4));
+  const int64_t* ids = vptr<int64_t>(in[1]);
+  if (n > 0) {
+    route_plan(ids, n, E, ws, nullptr, s, tot, off);
+    route_assign_kernel<<<static_cast<unsigned>(chunks_of(n)), 32, 0, s>>>(ids, n, E, cnt, slot_local);
+  } else {
+    OPF_CUDA(cudaMemsetAsync(tot, 0, E * 4, s));
+  }
+  launch_pdl(ep_exchange_kernel, dim3(1), dim3(1024), 0, s, x.w.pp, x.w.epochs, x.w.err, ep, x.rank, E, El,
+             static_cast<const int32_t*>(tot), send_off, vptr<int64_t>(out[1]));
+  const char* base = static_cast<const char*>(static_cast<const opf_comm*>(c->comm)->arena_base);
+  const int64_t xr_off = view_ptr(out[0]) - base, rinfo_off = view_ptr(out[1]) - base;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n * 32 + 255) / 256, num_sms() * 8LL)));
+  launch_pdl(ep_send_kernel, dim3(grid), dim3(256), 0, s, x.pa, xr_off, rinfo_off,
+             static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[0])), ids,
+             static_cast<const int64_t*>(slot_local), static_cast<const int32_t*>(off),
+             static_cast<const int32_t*>(send_off), n, k, H, E, El, x.rank);
+  launch_pdl(ep_barrier_kernel, dim3(1), dim3(32), 0, s, x.w.pp, x.w.epochs, x.w.err, ep, x.rank);
+  return launch_status("moe_ep_dispatch");
+}
+
+// The returned rows land in the combine's workspace (planned inside the arena,
+// so it sits at the same offset on every rank and lives exactly as long as the
+// combine: peers write it only between the two barriers).
+size_t ws_ep_combine(const opf_op_ctx& c, const opf_view*, int, const opf_view* out, int, int64_t rows) {
+  return align256(static_cast<size_t>(rows) * topk_param(c) * view_row_elems(out[0]) * 2) + 256;
+}
+
+opf_status op_moe_ep_combine(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out,
+                             int32_t n_out, int64_t rows, void* stream) {
+  if (n_in != 4 || n_out != 1)
+    return op_error(Errc::ShapeMismatch, "moe_ep_combine takes (yr, rinfo, w, ids) -> y");
+  const int k = topk_param(*c), E = experts_param(*c), ep = ep_param(*c);
+  if (ep < 2 || E % ep) return op_error(Errc::ConfigError, "moe_ep_combine: ep >= 2 dividing experts");
+  const int El = E / ep;
+  const int64_t H = view_row_elems(out[0]);
+  if (in[0].dtype != OPF_BF16 || out[0].dtype != OPF_BF16 || H % 8 ||
+      view_row_elems(in[0]) != static_cast<int64_t>(ep) * k * H ||
+      view_row_elems(in[1]) != static_cast<int64_t>(ep) * k + El || in[2].dtype != OPF_F32 ||
+      view_row_elems(in[2]) != k || view_row_elems(in[3]) != k)
+    return op_error(Errc::ShapeMismatch, "moe_ep_combine: yr [T, ep*k*H], rinfo, w [T,k] f32, ids [T,k] -> y [T,H]");
+  if (opf_status e = need_ws(c, ws_ep_combine(*c, in, n_in, out, n_out, rows), "moe_ep_combine")) return e;
+  opf_view yc = out[0];
+  yc.base = c->workspace;
+  yc.elem_offset = 0;
+  EpCtx x;
+  if (opf_status e = ep_ctx(c, "moe_ep_combine", &x, {&yc})) return e;
+  auto s = static_cast<cudaStream_t>(stream);
+  const int64_t n = rows * k;
+  const int64_t yc_off = static_cast<const char*>(c->workspace) -
+                         static_cast<const char*>(static_cast<const opf_comm*>(c->comm)->arena_base);
+  launch_pdl(ep_barrier_kernel, dim3(1), dim3(32), 0, s, x.w.pp, x.w.epochs, x.w.err, ep, x.rank);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n * ep * 32 + 255) / 256, num_sms() * 8LL)));
+  launch_pdl(ep_return_kernel, dim3(grid), dim3(256), 0, s, x.pa, yc_off,
+             static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[0])),
+             static_cast<const int64_t*>(vptr<int64_t>(in[1])), El, n, H);
+  launch_pdl(ep_barrier_kernel, dim3(1), dim3(32), 0, s, x.w.pp, x.w.epochs, x.w.err, ep, x.rank);
+  if (rows > 0)
+    launch_pdl(combine_slots_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), 0, s,
+               static_cast<const __nv_bfloat16*>(c->workspace),
+               static_cast<const int64_t*>(vptr<int64_t>(in[3])), static_cast<const float*>(vptr<float>(in[2])), k, E,
+               H, vptr<__nv_bfloat16>(out[0]));
+  return launch_status("moe_ep_combine");
 }
 
 opf_status op_moe_gate_up(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out, int32_t n_out,
@@ -399,9 +698,11 @@ opf_status op_moe_combine(const opf_op_ctx* c, const opf_view* in, int32_t n_in,
 void register_moe_ops(OpRegistry& r) {
   r.add({"moe_topk", op_moe_topk, ResourceClass::kMemory, 1, 2, {}});
   r.add({"moe_dispatch", op_moe_dispatch, ResourceClass::kNetwork, 2, 2, ws_dispatch});
-  r.add({"moe_gate_up", op_moe_gate_up, ResourceClass::kCompute, 3, 1, ws_grouped, 2, 2});
-  r.add({"moe_down", op_moe_down, ResourceClass::kCompute, 3, 1, ws_grouped, 2, 3});
+  r.add({"moe_gate_up", op_moe_gate_up, ResourceClass::kCompute, 3, 1, ws_grouped_any, 2, 2});
+  r.add({"moe_down", op_moe_down, ResourceClass::kCompute, 3, 1, ws_grouped_any, 2, 3});
   r.add({"moe_combine", op_moe_combine, ResourceClass::kNetwork, 3, 1, {}});
+  r.add({"moe_ep_dispatch", op_moe_ep_dispatch, ResourceClass::kNetwork, 2, 2, ws_ep_dispatch});
+  r.add({"moe_ep_combine", op_moe_ep_combine, ResourceClass::kNetwork, 4, 1, ws_ep_combine});
 }
 
 }  // namespace opflow

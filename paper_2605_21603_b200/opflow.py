@@ -585,6 +585,30 @@ class Session:
         spec = json.dumps(strategy if strategy is not None else {"name": "sequential"})
         check(lib().opf_session_run(self._h, spec.encode(), s))
 
+    def prepare(self, strategy: Any = None, stream=None) -> None:
+        """Plan + prepack + capture without launching (virtual peer ranks on one
+        device prepare every rank before any rank launches)."""
+        s = stream.cuda_stream if stream is not None and hasattr(stream, "cuda_stream") else stream
+        spec = json.dumps(strategy if strategy is not None else {"name": "sequential"})
+        check(lib().opf_session_prepare(self._h, spec.encode(), s))
+
+    def enable_peer_arena(self, min_bytes: int = 0) -> None:
+        """Symmetric arena for expert-parallel ops (one process per GPU): export
+        my arena's CUDA IPC handle, all-gather over torch.distributed, map peers."""
+        import torch.distributed as dist
+        h = (C.c_uint8 * 64)()
+        check(lib().opf_session_arena_export(self._h, min_bytes, h))
+        allh = [None] * self._comm.world
+        dist.all_gather_object(allh, bytes(h))
+        flat = (C.c_uint8 * (64 * self._comm.world))(*b"".join(allh))
+        check(lib().opf_session_arena_open(self._h, flat))
+
+    @staticmethod
+    def link_virtual(sessions: Sequence["Session"], min_bytes: int) -> None:
+        """Wire the arenas of `world` virtual-rank sessions sharing one device."""
+        arr = (C.c_void_p * len(sessions))(*[s_._h for s_ in sessions])
+        check(lib().opf_session_arena_link_local(arr, len(sessions), min_bytes))
+
     def stats(self) -> dict:
         p = C.c_void_p()
         check(lib().opf_session_stats(self._h, C.byref(p)))
