@@ -291,10 +291,10 @@ def run_ours(args):
         torch.cuda.empty_cache()
         decode = run_decode(of, torch, dev, args, tp, comm, rank, world, stream)
     moe = None
-    if not args.no_moe and tp == 1:
+    if not args.no_moe and args.tokens % (world * args.seq_len) == 0:
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
-        moe = run_moe(of, torch, dev, args, rank, world, stream)
+        moe = run_moe(of, torch, dev, args, rank, world, stream, comm)
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(args, T, S, tp)
         line = {
@@ -454,24 +454,31 @@ def time_op(of, torch, dev, stream, fn, ins, outs, params, rows, reps=20):
     return e0.elapsed_time(e1) / reps
 
 
-def run_moe(of, torch, dev, args, rank, world, stream):
+def run_moe(of, torch, dev, args, rank, world, stream, comm=None):
     """BASELINE configs[4]: Qwen3-30B-A3B-shaped MoE layer (q/k-norm GQA
     attention + 128-expert top-8 FFN), 8192 tokens (8 x 1024), dual-batch
     overlap vs sequential on one GPU (EP=1: dispatch/combine are local
     permutations at the all-to-all sites).  Roofline: the grouped tcgen05
     expert GEMMs (tensor) and dispatch/combine (HBM), timed alone."""
-    T, S, L = args.tokens, args.seq_len, args.moe_layers
+    S, L = args.seq_len, args.moe_layers
+    T = args.tokens // world  # EP=N: the job's tokens are spread over the ranks (C5: 8192 at EP=8)
     Q = QWEN3
-    desc = of.qwen3_moe_graph(layers=L, tokens=T, seq_len=S, dtype="bf16", **Q)
+    desc = of.qwen3_moe_graph(layers=L, tokens=T, seq_len=S, dtype="bf16", ep=world, **Q)
     R = of.PartitionRule
     rules = [R.by_module("layer*.attn"), R.by_module("layer*.moe.dispatch"),
              R.by_module("layer*.moe.experts"), R.by_module("layer*.moe.combine")]
-    g, plan, sess, bufs = build_session(of, desc, rules, dev, None, seed=4321 + rank)
+    g, plan, sess, bufs = build_session(of, desc, rules, dev, comm, seed=4321 + rank)
     pos = (torch.arange(T, device=dev) % S).to(torch.int64)
     bufs["positions"] = pos
     sess.bind("positions", pos)
     cands = {"sequential": {"name": "sequential"}, "dbo": {"name": "dbo", "align": S},
              "nanoflow_u2": {"name": "split_overlap", "n_microbatches": 2, "align": S, "lane_mode": "ubatch"}}
+    if world > 1:
+        # peer window (count exchange + barriers) and symmetric arena sized for every candidate plan
+        comm.enable_window(1 << 16)
+        need = max(of.dry_run(g, plan, spec, rows=T, config={"lanes": 3, "world": world})[1]["last"]["plan_arena_bytes"]
+                   for spec in cands.values())
+        sess.enable_peer_arena(need)
     res = {k: time_steps(torch, lambda s=s: sess.run(s, stream), args.steps, args.warmup, stream, world)
            for k, s in cands.items()}
     best = min((k for k in res if k != "sequential"), key=lambda k: res[k])
@@ -512,10 +519,12 @@ def run_moe(of, torch, dev, args, rank, world, stream):
                "hbm_frac": round(b_disp / ms_disp / 1e6 / PEAKS["hbm_gbs"], 4)},
               {"op": "moe_combine", "ms": round(ms_cb, 4), "gbs": round(b_comb / ms_cb / 1e6, 1),
                "hbm_frac": round(b_comb / ms_cb / 1e6 / PEAKS["hbm_gbs"], 4)}]
+    Tj = T * world
     return {"workload": f"qwen3-30b-a3b-shaped MoE layer x{L} (q/k-norm GQA attention + {E}-expert top-{k} "
-                        f"FFN, moe_inter {MI}), {T} tokens ({T // S} seqs x {S}), EP=1",
-            "tokens_per_s": round(T / (res[best] / 1e3), 1), "strategy": best,
-            "sequential_tokens_per_s": round(T / (res["sequential"] / 1e3), 1),
+                        f"FFN, moe_inter {MI}), {Tj} tokens ({Tj // S} seqs x {S}), EP={world}"
+                        + (" (peer-memory all-to-all)" if world > 1 else " (local dispatch/combine)"),
+            "tokens_per_s": round(Tj / (res[best] / 1e3), 1), "strategy": best,
+            "sequential_tokens_per_s": round(Tj / (res["sequential"] / 1e3), 1),
             "speedup_vs_sequential": round(res["sequential"] / res[best], 4),
             "strategies_ms": {k_: round(v, 3) for k_, v in res.items()},
             "launches_per_step": launches,

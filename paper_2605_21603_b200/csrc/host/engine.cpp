@@ -380,7 +380,8 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
     // two collectives (NCCL, or peer-window kernels sharing the staging window and
     // flags) must never run concurrently on different lanes.
     bool comm_dispatch = false;
-    if (comm_ && comm_->world > 1)
+    const int world = cfg_.world > 0 ? cfg_.world : (comm_ ? comm_->world : 1);
+    if (world > 1)
       for (int32_t op : ops) comm_dispatch = comm_dispatch || g_.ops[op].resource_class == ResourceClass::kNetwork;
     if (comm_dispatch) {
       if (last_comm >= 0) deps.insert(last_comm);

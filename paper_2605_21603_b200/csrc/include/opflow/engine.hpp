@@ -144,6 +144,7 @@ struct SessionConfig {
   int device = 0;
   int gemm_sm_budget = 0;     // max CTAs for tensor-core GEMMs on lane 0 when overlapping
   std::vector<int> lane_sm_budget;  // per-lane SM budget defaults (strategy may override)
+  int world = 0;                    // dry sessions: communicator size to plan for (0 = the comm's)
 };
 
 struct PlannedView {

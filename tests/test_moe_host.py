@@ -83,3 +83,23 @@ def test_oracle_topk_ties_prefer_lower_index():
     ids, w = oracle.moe_topk(lg, 2, renorm=False)
     p = np.exp(lg[0] - 3.0)
     np.testing.assert_allclose(w[0], [1 / p.sum(), 1 / p.sum()], rtol=1e-6)
+
+
+def test_collectives_form_one_chain_when_planned_for_a_world():
+    """With world > 1 every communicating (network-class) dispatch must be
+    ordered after the previous one — identical order on every rank, never two
+    collectives in flight on different lanes (they share NCCL / the peer window)."""
+    from paper_2605_21603_b200.racecheck import happens_before
+    g = of.build_graph(of.qwen3_moe_graph(**dict(SMALL, ep=4)))
+    p = of.partition(g, DBO_RULES)
+    for world, chained in ((4, True), (1, False)):
+        sched, stats = of.dry_run(g, p, {"name": "dbo", "align": 128}, config={"lanes": 3, "world": world})
+        assert stats["last"]["copied_elements"] == 0 and not find_races(sched)
+        labels = {s.id: s.label for s in p.subgraphs}
+        net = [d["id"] for d in sched["dispatches"]
+               if any(labels[sg].endswith((".moe.dispatch", ".moe.combine")) for sg in d["subgraphs"])]
+        assert len(net) == 8  # 2 layers x (dispatch, combine) x 2 micro-batches
+        before = happens_before(sched)  # bitmask of predecessors per dispatch
+        ordered = all(before[b] >> a & 1 for a, b in zip(net, net[1:]))
+        if chained:
+            assert ordered
