@@ -374,7 +374,11 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
     desc = of.llama_decode_graph(layers=L, tokens=B, ctx_len=ctx, page_size=page, tp=tp, dtype="bf16",
                                  **LLAMA)
     g = of.build_graph(desc)
-    rules = [of.PartitionRule.by_func("AllReduce"), of.PartitionRule.by_func("add_rmsnorm")] if tp > 1 else []
+    # attention gets its own subgraphs (NanoFlow: memory-bound attention on one
+    # lane, the compute-bound GEMM fillers between attentions on the other)
+    rules = [of.PartitionRule.by_func("attn_decode")]
+    if tp > 1:
+        rules += [of.PartitionRule.by_func("AllReduce"), of.PartitionRule.by_func("add_rmsnorm")]
     sess = of.Session(g, of.partition(g, rules), {"lanes": 3, "device": dev.index}, comm)
     gen = torch.Generator(device=dev).manual_seed(99 + rank)
     keep = {}
@@ -408,11 +412,13 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
     cands = {"sequential": {"name": "sequential"},
              "nanoflow_u2": {"name": "split_overlap", "n_microbatches": 2, "lane_mode": "ubatch"},
              "nanoflow_class": {"name": "split_overlap", "n_microbatches": 2}}
-    # NanoFlow SM partitioning: GEMMs (compute lane 0) on G SMs, paged attention
-    # and the memory-bound ops (lane 1) on the remaining SMs, concurrently.
-    for gsm in (args.sm_sweep or []):
+    # NanoFlow SM partitioning: the GEMM fillers (compute lane 0) on G SMs, the
+    # persistent paged attention (memory lane 1) on the other 148 - G SMs,
+    # nano-batch A's attention concurrent with nano-batch B's GEMMs.
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    for gsm in (args.sm_sweep if args.sm_sweep is not None else [24, 40, 56, 72]):
         cands[f"nanoflow_class_sm{gsm}"] = {"name": "split_overlap", "n_microbatches": 2,
-                                            "lane_sm_budget": [gsm, 148 - gsm, 0]}
+                                            "lane_sm_budget": [gsm, nsm - gsm, 0]}
     res = {k: time_steps(torch, lambda s=s: sess.run(s, stream), args.steps, args.warmup, stream, world)
            for k, s in cands.items()}
     best = min((k for k in res if k != "sequential"), key=lambda k: res[k])

@@ -115,6 +115,9 @@ opf_status opf_has_op(const char* name, int32_t* present);
 opf_status opf_launch(const char* op_json, const opf_view* in, int32_t n_in, opf_view* out,
                       int32_t n_out, int64_t rows, void* stream);
 opf_status opf_view_rows(const opf_view* v, int64_t row_off, int64_t nrows, opf_view* out);
+/* K splits the tcgen05 GEMM takes for an (m, n, k) MatMul on max_ctas SMs
+ * (0 = whole GPU) when the engine provides its workspace; 1 = no split. */
+int32_t opf_gemm_splits(int64_t m, int64_t n, int64_t k, int32_t max_ctas);
 /* opf_launch with a communicator (TP collectives / fused comm ops) and an SM budget. */
 typedef struct opf_comm opf_comm;
 opf_status opf_launch_comm(const char* op_json, const opf_view* in, int32_t n_in, opf_view* out,

@@ -11,7 +11,8 @@ import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libopflow_b200.so"
+# OPF_LIB overrides the library (A/B timing of a variant build, tools/build_ab.py)
+LIB_PATH = Path(os.environ["OPF_LIB"]) if os.environ.get("OPF_LIB") else _PKG / "libopflow_b200.so"
 
 ERRC = [
     "CycleDetected", "UnknownTensor", "ShapeMismatch", "DuplicateId", "MissingBinding",
@@ -65,6 +66,7 @@ _SIGS = {
     "opf_has_op": (C.c_int32, [C.c_char_p, C.POINTER(C.c_int32)]),
     "opf_launch": (C.c_int32, [C.c_char_p, C.POINTER(opf_view), C.c_int32, C.POINTER(opf_view),
                                C.c_int32, C.c_int64, C.c_void_p]),
+    "opf_gemm_splits": (C.c_int32, [C.c_int64, C.c_int64, C.c_int64, C.c_int32]),
     "opf_view_rows": (C.c_int32, [C.POINTER(opf_view), C.c_int64, C.c_int64, C.POINTER(opf_view)]),
     "opf_comm_unique_id": (C.c_int32, [C.POINTER(C.c_uint8)]),
     "opf_comm_init": (C.c_int32, [C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32,

@@ -227,6 +227,14 @@ opf_status opf_has_op(const char* name, int32_t* present) {
   return guard([&] { *present = OpRegistry::global().find(name) != nullptr; });
 }
 
+int32_t opf_gemm_splits(int64_t m, int64_t n, int64_t k, int32_t max_ctas) {
+  try {
+    return opflow::gemm_splitk_splits(m, n, k, max_ctas);
+  } catch (...) {
+    return 1;
+  }
+}
+
 opf_status opf_launch(const char* op_json, const opf_view* in, int32_t n_in, opf_view* out,
                       int32_t n_out, int64_t rows, void* stream) {
   opf_status st = 0;

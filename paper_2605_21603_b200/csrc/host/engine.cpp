@@ -610,6 +610,7 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
       c.kind = static_cast<int32_t>(l.kind);
       c.world_size = l.attrs.world_size;
       c.comm = comm_;
+      c.max_ctas = l.max_ctas;
       std::vector<opf_view> iv, ov;
       for (const auto& v : l.in) iv.push_back(make_view(nullptr, v.elem_offset, v.dtype, v.shape, v.batched));
       for (const auto& v : l.out) ov.push_back(make_view(nullptr, v.elem_offset, v.dtype, v.shape, v.batched));

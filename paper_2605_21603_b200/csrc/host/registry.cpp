@@ -95,7 +95,15 @@ ncclDataType_t nccl_type(int32_t dt) {
 
 }  // namespace
 
-size_t kind_workspace(const opf_op_ctx&, const opf_view*, int, const opf_view*, int, int64_t) {
+size_t kind_workspace(const opf_op_ctx& c, const opf_view* in, int n_in, const opf_view* out, int n_out,
+                      int64_t rows) {
+  // bf16 MatMul on the tcgen05 path: split-K partials for under-filled grids
+  if (static_cast<OperatorKind>(c.kind) == OperatorKind::kMatMul && n_in == 2 && n_out >= 1 &&
+      in[0].dtype == OPF_BF16) {
+    const int epi = static_cast<int>(ctx_param(c, "epi", 0.0));
+    const int64_t N = out[0].shape[1] * (epi == 1 ? 2 : 1);
+    return gemm_splitk_workspace(rows, N, in[0].shape[1], c.max_ctas);
+  }
   return 0;
 }
 
@@ -130,6 +138,8 @@ opf_status launch_kind(const opf_op_ctx& c, const opf_view* in, int n_in, opf_vi
           g.ldc = out[0].shape[1];
           g.max_ctas = c.max_ctas;
           g.epi = epi;
+          g.ws = c.workspace;
+          g.ws_bytes = c.workspace_bytes;
           if (c.aux) {  // pre-packed [N,K] weight -> tcgen05 path
             g.bt = c.aux;
             gemm_bf16_tc(g, s);

@@ -126,8 +126,14 @@ struct GemmArgs {
   int max_ctas;    // 0 = all SMs
   bool b_kn;       // simt path only: B given as [K,N] row-major instead of [N,K]
   int epi;         // 0 plain; 1 SiLU-mul (Bt packed by k_pack_gate_up, C is [M, N/2])
+  void* ws;        // split-K workspace (gemm_splitk_workspace bytes), nullptr = no split
+  size_t ws_bytes;
 };
 void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s);
+// K splits the 2-CTA kernel uses for an (m, n, k) launch on `max_ctas` SMs
+// (1 = none) and the workspace they need (fp32 partials + tile semaphores).
+int gemm_splitk_splits(int64_t m, int64_t n, int64_t k, int max_ctas);
+size_t gemm_splitk_workspace(int64_t m, int64_t n, int64_t k, int max_ctas);
 // Grouped per-expert GEMM (MoE): gtab = device tile table [n, (row0, row_end, expert) x n],
 // bt = [n_groups * group_n, K]; g.m bounds the rows of a / c, g.n is unused.
 void gemm_bf16_grouped(const GemmArgs& g, const int32_t* gtab, int64_t max_mtiles, int64_t group_n,

@@ -191,13 +191,14 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t m_blocks, int64_t
 //   EPI 0: plain, 256 output columns at nb*256.
 //   EPI 1: SiLU-mul, the weight was packed so tile columns [0,128) are gate and
 //          [128,256) the matching up columns; 128 outputs at nb*128.
-template <int EPI>
+template <int EPI, int TN = BN>
 __device__ __forceinline__ void store_tile(const CUtensorMap* map_c, uint32_t tmem_col0,
                                            uint8_t* const (&stg)[2], int& buf, int lane, int64_t nb,
-                                           int64_t row0, int64_t M) {
-  constexpr int kChunks = EPI == 1 ? 2 : BN / 64;
+                                           int64_t row0, int64_t M, int first = 0, int step = 1) {
+  // EPI 1 needs TN = 256 (gate | up halves of 128); chunks are 64 output columns
+  constexpr int kChunks = EPI == 1 ? 2 : TN / 64;
 #pragma unroll 1
-  for (int chunk = 0; chunk < kChunks; ++chunk) {
+  for (int chunk = first; chunk < kChunks; chunk += step) {
     uint32_t v0[32], v1[32];
     const uint32_t taddr = tmem_col0 + static_cast<uint32_t>(chunk * 64);
     tmem_ld32(taddr, v0);
@@ -234,7 +235,7 @@ __device__ __forceinline__ void store_tile(const CUtensorMap* map_c, uint32_t tm
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0 && row0 < M) {
-      const int64_t col = EPI == 1 ? nb * (BN / 2) + chunk * 64 : nb * BN + chunk * 64;
+      const int64_t col = EPI == 1 ? nb * (TN / 2) + chunk * 64 : nb * TN + chunk * 64;
       tma_store_2d(map_c, sbuf, static_cast<int32_t>(col), static_cast<int32_t>(row0));
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
@@ -432,6 +433,147 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
 }
 
+// ------------------------------------------------------------------ split-K (2-CTA, TN = 256)
+// Under-filled grids (decode / TP-sharded shapes: M = 256..512 rows, or few N
+// tiles) split the K loop over S work units per output tile so every SM
+// streams weights.  Each epilogue warp owns a fixed region of the 256x256 tile
+// (CTA rank r, lane quarter, 4 pieces of 32 accumulator columns): it writes its
+// fp32 partial to the workspace, bumps the region's semaphore, and the warp
+// that arrives last sums the S partials in split order (its own from TMEM) —
+// deterministic whatever the arrival order — applies the epilogue and stores.
+constexpr int kRegionFloats = 32 * 128;  // 32 rows x 4 pieces x 32 columns
+
+// accumulator column of piece p (0..3) of this warp's region
+template <int EPI>
+__device__ __forceinline__ uint32_t splitk_piece_col(int half, int p) {
+  if constexpr (EPI == 1) return static_cast<uint32_t>((p >> 1) * 128 + half * 64 + (p & 1) * 32);
+  return static_cast<uint32_t>(((p >> 1) * 2 + half) * 64 + (p & 1) * 32);
+}
+
+// acc = sum over splits j = 0..S-1 (in order) of piece p of a region, read
+// from the workspace two splits at a time (16 x 16-byte loads in flight)
+__device__ __forceinline__ void ld_piece(float (&t)[32], const float4* src) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 x = __ldcg(src + q * 32);
+    t[4 * q] = x.x;
+    t[4 * q + 1] = x.y;
+    t[4 * q + 2] = x.z;
+    t[4 * q + 3] = x.w;
+  }
+}
+__device__ __forceinline__ void splitk_sum_piece(float (&acc)[32], const float4* __restrict__ regions,
+                                                 int64_t split_stride, int S, int p, int lane) {
+  const float4* src = regions + p * 8 * 32 + lane;
+  ld_piece(acc, src);  // split 0 (0 + p0 == p0 exactly)
+  int j = 1;
+  for (; j + 1 < S; j += 2) {
+    float t0[32], t1[32];
+    ld_piece(t0, src + j * split_stride);
+    ld_piece(t1, src + (j + 1) * split_stride);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = (acc[i] + t0[i]) + t1[i];
+  }
+  if (j < S) {
+    float t0[32];
+    ld_piece(t0, src + j * split_stride);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] += t0[i];
+  }
+}
+
+// bf16-pack 32 columns of this lane's row into half h (16-byte chunks 4h..4h+3)
+// of the 64-column swizzled staging buffer
+__device__ __forceinline__ void stage_half(uint8_t* sbuf, const float (&v)[32], int h, int lane) {
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    const int j = 4 * h + jj;
+    uint4 q;
+    q.x = pack_bf16(__float_as_uint(v[8 * jj]), __float_as_uint(v[8 * jj + 1]));
+    q.y = pack_bf16(__float_as_uint(v[8 * jj + 2]), __float_as_uint(v[8 * jj + 3]));
+    q.z = pack_bf16(__float_as_uint(v[8 * jj + 4]), __float_as_uint(v[8 * jj + 5]));
+    q.w = pack_bf16(__float_as_uint(v[8 * jj + 6]), __float_as_uint(v[8 * jj + 7]));
+    *reinterpret_cast<uint4*>(sbuf + lane * 128 + ((j ^ (lane & 7)) * 16)) = q;
+  }
+}
+__device__ __forceinline__ uint8_t* stage_begin(uint8_t* const (&stg)[2], int buf, int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  __syncwarp();
+  return stg[buf];
+}
+__device__ __forceinline__ void stage_commit(const CUtensorMap* map_c, uint8_t* sbuf, int& buf, int lane,
+                                             int64_t col, int64_t row0, int64_t M) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0 && row0 < M) {
+    tma_store_2d(map_c, sbuf, static_cast<int32_t>(col), static_cast<int32_t>(row0));
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  buf ^= 1;
+}
+
+// One epilogue warp's share of split `mine` of tile `tile`.  The accumulator
+// is released (release_acc) as soon as the partial is in the workspace, so
+// the last arriver's fixup overlaps the next unit's MMAs.
+template <int EPI, typename Release>
+__device__ __forceinline__ void store_tile_splitk(const CUtensorMap* map_c, uint32_t tcol, uint8_t* const (&stg)[2],
+                                                  int& buf, int lane, int64_t nb, int64_t row0, int64_t M,
+                                                  int half, int region, int64_t tile, int mine, int S,
+                                                  float4* __restrict__ ws, int* __restrict__ sem,
+                                                  Release release_acc) {
+  const int64_t split_stride = 16LL * kRegionFloats / 4;  // float4s between splits of one region
+  float4* regions = ws + (tile * S * 16 + region) * (kRegionFloats / 4);
+  float4* my = regions + mine * split_stride;
+  // 1. partial -> workspace (coalesced: a warp store covers 512 contiguous bytes)
+#pragma unroll 1
+  for (int p = 0; p < 4; ++p) {
+    uint32_t v[32];
+    tmem_ld32(tcol + splitk_piece_col<EPI>(half, p), v);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      __stcg(my + p * 8 * 32 + q * 32 + lane,
+             make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                         __uint_as_float(v[4 * q + 3])));
+  }
+  release_acc();
+  __threadfence();
+  __syncwarp();
+  int old = 0;
+  int* sm = sem + tile * 16 + region;
+  if (lane == 0) old = atomicAdd(sm, 1);
+  old = __shfl_sync(0xffffffffu, old, 0);
+  if (old != S - 1) return;
+  // 2. last arriver: sum the S partials in split order, epilogue, store
+  __threadfence();
+  if (lane == 0) *sm = 0;  // self-cleaning for the next launch on this workspace
+  if constexpr (EPI == 1) {
+    uint8_t* sbuf = stage_begin(stg, buf, lane);
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      float g[32], u[32];
+      splitk_sum_piece(g, regions, split_stride, S, h, lane);
+      splitk_sum_piece(u, regions, split_stride, S, 2 + h, lane);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) g[i] = g[i] / (1.0f + __expf(-g[i])) * u[i];
+      stage_half(sbuf, g, h, lane);
+    }
+    stage_commit(map_c, sbuf, buf, lane, nb * 128 + half * 64, row0, M);
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint8_t* sbuf = stage_begin(stg, buf, lane);
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        float v[32];
+        splitk_sum_piece(v, regions, split_stride, S, 2 * c + h, lane);
+        stage_half(sbuf, v, h, lane);
+      }
+      stage_commit(map_c, sbuf, buf, lane, nb * 256 + (2 * c + half) * 64, row0, M);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ 2-CTA (cta_group::2) path
 // A CTA pair (cluster of 2 on one TPC) owns a 256x256 output tile.  Each CTA
 // TMA-loads its own 128 A rows and 128 of the 256 B rows per 64-deep k-block
@@ -441,11 +583,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Full barriers live in the leader (TMA complete_tx from both CTAs lands
 // there); smem-slot and accumulator-ready commits multicast to both CTAs;
 // both CTAs' epilogue warps release the accumulator on the leader's barrier.
-constexpr int kStages2 = 6;
-constexpr uint32_t kStageBytes2 = kABytes + kBBytes / 2;  // 32 KB
-constexpr uint32_t kSmemBytes2 = 1024 + kStages2 * kStageBytes2 + kEpiWarps * 2 * kEpiBytes + 256;
-constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(256 >> 3) << 17) |
-                             (static_cast<uint32_t>(256 >> 4) << 24);
+//
+// Tile width TN in {256, 192, 128} (OPF_GEMM_TN; 256 by default).  Epilogue
+// warps: 4 (one per TMEM lane quarter, 6-stage ring) for whole-K tiles; the
+// split-K variant uses 8 (warp w reads lane quarter w % 4 and the 64-column
+// chunks (w - 2) / 4, +2: 16 independent regions per tile for the partial
+// fixup) with a 5-stage ring.  8 warps did not speed up the whole-K epilogue
+// on short-K shapes (A/B in profiles/r01_gemm_ab_r0_vs_new.jsonl), so the
+// lighter 4-warp / 6-stage configuration stays there.
+template <int TN, bool SPLIT>
+struct Tc2Cfg {
+  static constexpr int kEpiW = SPLIT ? 8 : 4;
+  static constexpr int kThreads = 64 + kEpiW * 32;
+  static constexpr uint32_t kStageBytes = kABytes + (TN / 2) * BK * 2;
+  static constexpr uint32_t kFixed = 1024 + kEpiW * 2 * kEpiBytes + 512;
+  static constexpr int kStages = ((232448 - kFixed) / kStageBytes) > 6 ? 6 : (232448 - kFixed) / kStageBytes;
+  static constexpr uint32_t kSmemBytes = kFixed + kStages * kStageBytes;
+  static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(TN >> 3) << 17) |
+                                     (static_cast<uint32_t>(256 >> 4) << 24);
+};
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clear the CTA-rank bit: address the pair leader
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -464,12 +620,13 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
       : "memory");
 }
-__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                              uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kIdesc2), "r"(acc));
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
   asm volatile(
@@ -483,15 +640,19 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
                : "memory");
 }
 
-template <int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+template <int EPI, int TN, bool SPLIT = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                    const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K) {
+                    const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K, int splits,
+                    float4* __restrict__ ws, int* __restrict__ sem) {
+  using C = Tc2Cfg<TN, SPLIT>;
+  constexpr int kStages2 = C::kStages;
+  constexpr uint32_t kStageBytes2 = C::kStageBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;
   uint8_t* epi_base = smem + kStages2 * kStageBytes2;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + kEpiWarps * 2 * kEpiBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + C::kEpiW * 2 * kEpiBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages2;
   uint64_t* tfull = bars + 2 * kStages2;
@@ -501,9 +662,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int64_t m_blocks = (M + 2 * BM - 1) / (2 * BM), n_blocks = (N + BN - 1) / BN;
+  const int64_t m_blocks = (M + 2 * BM - 1) / (2 * BM), n_blocks = (N + TN - 1) / TN;
   const int64_t tiles = m_blocks * n_blocks;
   const int k_blocks = static_cast<int>((K + BK - 1) / BK);
+  const int64_t units = tiles * splits;  // unit u = split (u % splits) of tile (u / splits)
   const int64_t cluster = blockIdx.x / 2, n_clusters = gridDim.x / 2;
 
   if (warp == 0) {
@@ -522,7 +684,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < kAccStages; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * kEpiWarps);
+      mbar_init(&tempty[a], 2 * C::kEpiW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -537,12 +699,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = cluster; t < tiles; t += n_clusters) {
+      for (int64_t u = cluster; u < units; u += n_clusters) {
+        const int64_t t = u / splits;
+        const int sp = static_cast<int>(u % splits);
         int64_t mb, nb;
         tile_coords(t, m_blocks, n_blocks, mb, nb);
         const int32_t m0 = static_cast<int32_t>(mb * 2 * BM + rank * BM);
-        const int32_t n0 = static_cast<int32_t>(nb * BN + rank * (BN / 2));
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        const int32_t n0 = static_cast<int32_t>(nb * TN + rank * (TN / 2));
+        const int kb0 = sp * k_blocks / splits, kb1 = (sp + 1) * k_blocks / splits;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = stage_base + stage * kStageBytes2;
           if (leader) mbar_expect_tx(&full[stage], 2 * kStageBytes2);
@@ -561,19 +726,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int64_t t = cluster; t < tiles; t += n_clusters) {
+      for (int64_t u = cluster; u < units; u += n_clusters) {
+        const int sp = static_cast<int>(u % splits);
+        const int kb0 = sp * k_blocks / splits, kb1 = (sp + 1) * k_blocks / splits;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * TN);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = smem_u32(stage_base + stage * kStageBytes2);
           const uint32_t sb = sa + kABytes;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_f16_pair(d_tmem, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32),
-                          (kb | k) != 0);
+            umma_f16_pair(d_tmem, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32), C::kIdesc,
+                          (kb != kb0 || k != 0) ? 1u : 0u);
           umma_commit_pair(&empty[stage]);
           if (++stage == kStages2) {
             stage = 0;
@@ -590,23 +757,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else {  // ---------------- epilogue warps (both CTAs)
     const int ew = warp - 2;
     const int quarter = warp % 4;
+    const int half = C::kEpiW == 8 ? ew / 4 : 0;  // column chunks half, half + step, ...
+    constexpr int kStep = C::kEpiW == 8 ? 2 : 1;
     uint8_t* stg[2] = {epi_base + (ew * 2) * kEpiBytes, epi_base + (ew * 2 + 1) * kEpiBytes};
     int acc = 0;
     uint32_t acc_phase = 0;
     int buf = 0;
-    for (int64_t t = cluster; t < tiles; t += n_clusters) {
+    for (int64_t u = cluster; u < units; u += n_clusters) {
+      const int64_t t = u / splits;
       int64_t mb, nb;
       tile_coords(t, m_blocks, n_blocks, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t row0 = mb * 2 * BM + rank * BM + quarter * 32;
-      store_tile<EPI>(&map_c,
-                      tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                          static_cast<uint32_t>(acc * BN),
-                      stg, buf, lane, nb, row0, M);
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+      const uint32_t tcol = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * TN);
+      auto release = [&]() {  // accumulator fully read: hand it back to the MMA warp
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+      };
+      if constexpr (SPLIT && TN == 256) {
+        store_tile_splitk<EPI>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, static_cast<int>(rank) * 8 + ew, t,
+                               static_cast<int>(u % splits), splits, ws, sem, release);
+      } else {
+        store_tile<EPI, TN>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, kStep);
+        release();
+      }
       if (++acc == kAccStages) {
         acc = 0;
         acc_phase ^= 1;
@@ -668,10 +844,18 @@ void gemm_bf16_tc_init() {
                                   static_cast<int>(kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemBytes)));
-    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSmemBytes2)));
-    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSmemBytes2)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<192, false>::kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<128, false>::kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<256, true>::kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<256, true>::kSmemBytes)));
   });
 }
 
@@ -681,6 +865,43 @@ void gemm_bf16_simt(const GemmArgs& g, cudaStream_t s) {
                                         static_cast<const __nv_bfloat16*>(g.bt),
                                         static_cast<__nv_bfloat16*>(g.c), g.m, g.n, g.k, g.lda,
                                         g.ldc, g.b_kn);
+}
+
+// K splits for a 2-CTA launch.  Split only when every split of every tile
+// fits in ONE round of clusters (measured on B200: in multi-round grids the
+// partial write + fixup is paid by every unit and loses, e.g. 8192x768x4096
+// 49 -> 67 us at S = 3), each split keeps >= 16 k-blocks, and the split saves
+// >= 32 k-block steps (~9 us) against a ~10 us fixed prologue / drain / fixup
+// cost (profiles/r01_gemm_splitk_ab.json).  Largest such S <= 8.
+int gemm_splitk_splits(int64_t m, int64_t n, int64_t k, int max_ctas) {
+  if (m <= BM) return 1;
+  static const int forced = [] {
+    const char* e = std::getenv("OPF_GEMM_SPLITK");
+    return e ? std::atoi(e) : -1;
+  }();
+  static const int tn_forced = [] {
+    const char* e = std::getenv("OPF_GEMM_TN");
+    return e ? std::atoi(e) : 256;
+  }();
+  if (tn_forced == 192 || tn_forced == 128) return 1;
+  int grid = num_sms();
+  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  const int64_t clusters = std::max(grid / 2, 1);
+  const int64_t tiles = ((m + 2 * BM - 1) / (2 * BM)) * ((n + 255) / 256);
+  const int64_t kb = (k + BK - 1) / BK;
+  if (forced >= 1) return static_cast<int>(std::min<int64_t>(forced, std::max<int64_t>(kb, 1)));
+  int best = 1;
+  for (int S = 2; S <= 8; ++S)
+    if (tiles * S <= clusters && kb / S >= 16 && kb - kb / S >= 32) best = S;
+  return best;
+}
+
+size_t gemm_splitk_workspace(int64_t m, int64_t n, int64_t k, int max_ctas) {
+  const int S = gemm_splitk_splits(m, n, k, max_ctas);
+  if (S <= 1) return 0;
+  const int64_t tiles = ((m + 2 * BM - 1) / (2 * BM)) * ((n + 255) / 256);
+  return static_cast<size_t>(tiles * S * 16 * kRegionFloats) * sizeof(float) +
+         static_cast<size_t>(tiles * 16) * sizeof(int);
 }
 
 void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
@@ -705,15 +926,57 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
   int grid = num_sms();
   if (g.max_ctas > 0 && g.max_ctas < grid) grid = g.max_ctas;
   if (pair) {
-    const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN / 2);
-    const int64_t tiles = ((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n + BN - 1) / BN);
-    int clusters = grid / 2;
-    if (tiles < clusters) clusters = static_cast<int>(tiles);
-    const unsigned blocks = 2u * static_cast<unsigned>(std::max(clusters, 1));
-    if (g.epi == 1)
-      launch_pdl(gemm_tc2_kernel<1>, dim3(blocks), dim3(kThreads), kSmemBytes2, s, ma, mb, mc, g.m, g.n, g.k);
+    const int64_t mt = (g.m + 2 * BM - 1) / (2 * BM);
+    const int cmax = std::max(grid / 2, 1);
+    // Tile width: 256 unless OPF_GEMM_TN forces 192 / 128.  Narrower tiles
+    // quantise better onto 74 clusters (e.g. N = 768: 96 -> 128 tiles) but
+    // measured slower per FLOP on B200 (more L2 -> SMEM bytes per MAC), so the
+    // rounds x width model alone picks them wrongly (profiles/r01_gemm_sweep*.json).
+    int tn = 256;
+    if (g.epi == 0) {
+      static const int forced = [] {
+        const char* e = std::getenv("OPF_GEMM_TN");
+        const int v = e ? std::atoi(e) : 0;
+        return (v == 192 || v == 128) ? v : 256;
+      }();
+      tn = forced;
+    }
+    const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, static_cast<uint32_t>(tn / 2));
+    const int64_t tiles = mt * ((g.n + tn - 1) / tn);
+    int splits = tn == 256 ? gemm_splitk_splits(g.m, g.n, g.k, g.max_ctas) : 1;
+    float4* ws = nullptr;
+    int* sem = nullptr;
+    if (splits > 1) {
+      const size_t need = gemm_splitk_workspace(g.m, g.n, g.k, g.max_ctas);
+      if (g.ws == nullptr || g.ws_bytes < need || (reinterpret_cast<uintptr_t>(g.ws) % 16) != 0) {
+        splits = 1;  // direct launches without an engine workspace
+      } else {
+        ws = static_cast<float4*>(g.ws);
+        sem = reinterpret_cast<int*>(static_cast<char*>(g.ws) + need - static_cast<size_t>(tiles * 16) * sizeof(int));
+        // semaphores start at zero (the last arriver re-zeroes its own)
+        OPF_CUDA(cudaMemsetAsync(sem, 0, static_cast<size_t>(tiles * 16) * sizeof(int), s));
+      }
+    }
+    const int clusters = static_cast<int>(std::min<int64_t>(tiles * splits, cmax));
+    const dim3 blocks(2u * static_cast<unsigned>(std::max(clusters, 1)));
+    if (splits > 1 && g.epi == 1)
+      launch_pdl(gemm_tc2_kernel<1, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
+                 g.m, g.n, g.k, splits, ws, sem);
+    else if (splits > 1)
+      launch_pdl(gemm_tc2_kernel<0, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
+                 g.m, g.n, g.k, splits, ws, sem);
+    else if (g.epi == 1)
+      launch_pdl(gemm_tc2_kernel<1, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
+                 g.n, g.k, splits, ws, sem);
+    else if (tn == 256)
+      launch_pdl(gemm_tc2_kernel<0, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
+                 g.n, g.k, splits, ws, sem);
+    else if (tn == 192)
+      launch_pdl(gemm_tc2_kernel<0, 192>, blocks, dim3(Tc2Cfg<192, false>::kThreads), Tc2Cfg<192, false>::kSmemBytes, s, ma, mb, mc, g.m,
+                 g.n, g.k, 1, ws, sem);
     else
-      launch_pdl(gemm_tc2_kernel<0>, dim3(blocks), dim3(kThreads), kSmemBytes2, s, ma, mb, mc, g.m, g.n, g.k);
+      launch_pdl(gemm_tc2_kernel<0, 128>, blocks, dim3(Tc2Cfg<128, false>::kThreads), Tc2Cfg<128, false>::kSmemBytes, s, ma, mb, mc, g.m,
+                 g.n, g.k, 1, ws, sem);
     return;
   }
   const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN);

@@ -210,7 +210,8 @@ def test_llama_decode_bf16(cuda):
 
 
 @pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 512, 1024), (300, 520, 200), (1, 256, 64),
-                                   (2048, 6144, 4096), (8192, 4096, 512), (77, 3000, 1032)])
+                                   (2048, 6144, 4096), (8192, 4096, 512), (77, 3000, 1032),
+                                   (8192, 768, 4096), (8192, 3584, 512), (8192, 712, 256), (1000, 712, 256)])
 def test_gemm_tcgen05_vs_torch(cuda, m, n, k):
     import torch
     g = torch.Generator(device="cuda").manual_seed(m * 7 + n)
@@ -285,3 +286,73 @@ def test_prefill_attention_tensor_core(cuda, S, nq, nkv, seqs):
     torch.cuda.synchronize()
     assert rel_err(out.float().cpu().numpy(), want) < 1e-2
     assert rel_err(out2.float().cpu().numpy(), want) < 1e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tn", [192, 128])
+def test_gemm_tile_width_variants(tn):
+    """The 2-CTA kernel's narrower tile widths (OPF_GEMM_TN, read once per
+    process) stay correct: ragged N, short and long K."""
+    import subprocess
+    import sys
+    code = (
+        "import torch,json,sys; sys.path.insert(0, '.');"
+        "from paper_2605_21603_b200 import opflow as of\n"
+        "for (m,n,k) in [(8192,768,4096),(4096,712,256),(1000,3584,512)]:\n"
+        "  g=torch.Generator(device='cuda').manual_seed(m+n)\n"
+        "  a=(torch.rand(m,k,device='cuda',generator=g)*2-1).to(torch.bfloat16)\n"
+        "  w=((torch.rand(k,n,device='cuda',generator=g)*2-1)/k**0.5).to(torch.bfloat16)\n"
+        "  d=json.dumps({'tensors':[{'name':'a','shape':[m,k],'dtype':'bf16','role':'input'},"
+        "{'name':'w','shape':[k,n],'batch':'replicated','dtype':'bf16','role':'weight'},"
+        "{'name':'c','shape':[m,n],'dtype':'bf16','role':'output'}],'operators':[{'name':'mm','kind':'MatMul',"
+        "'inputs':['a','w'],'outputs':['c']}]})\n"
+        "  gr=of.build_graph(d); s=of.Session(gr, of.partition(gr, []), {'lanes':1})\n"
+        "  c=torch.empty(m,n,dtype=torch.bfloat16,device='cuda'); s.bind('a',a); s.bind('w',w); s.bind('c',c); s.run()\n"
+        "  torch.cuda.synchronize(); want=a.float()@w.float()\n"
+        "  e=((c.float()-want).norm()/want.norm()).item(); assert e<1e-2,(m,n,k,e)\n"
+        "print('ok')\n")
+    import os
+    env = dict(os.environ, OPF_GEMM_TN=str(tn))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,k,silu", [(256, 6144, 4096, False), (256, 4096, 14336, False),
+                                        (512, 4096, 14336, False), (512, 4096, 4096, True),
+                                        (384, 1000, 8192, False)])
+def test_gemm_splitk_deterministic(cuda, m, n, k, silu):
+    """Under-filled grids take the split-K path (engine workspace): results
+    match torch fp32 and are bit-identical across replays (split-order sums)."""
+    import torch
+    from paper_2605_21603_b200 import _lib
+    splits = _lib.lib().opf_gemm_splits(m, n, k, 0)
+    assert splits > 1, (m, n, k, splits)
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    a = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w = ((torch.rand(k, n, device="cuda", generator=g) * 2 - 1) / k ** 0.5).to(torch.bfloat16)
+    nout = n // 2 if silu else n
+    tens = [{"name": "a", "shape": [m, k], "dtype": "bf16", "role": "input"},
+            {"name": "w", "shape": [k, n], "batch": "replicated", "dtype": "bf16", "role": "weight"},
+            {"name": "c", "shape": [m, nout], "dtype": "bf16", "role": "output"}]
+    ops = [{"name": "mm", "kind": "MatMul", "inputs": ["a", "w"], "outputs": ["gu" if silu else "c"]}]
+    if silu:
+        tens.append({"name": "gu", "shape": [m, n], "dtype": "bf16"})
+        ops.append({"name": "act", "kind": "Custom", "inputs": ["gu"], "outputs": ["c"],
+                    "attrs": {"custom_name": "silu_mul"}})
+    gr = of.build_graph(json.dumps({"tensors": tens, "operators": ops}))
+    sess = of.Session(gr, of.partition(gr, []), {"lanes": 1})
+    c = torch.empty(m, nout, dtype=torch.bfloat16, device="cuda")
+    sess.bind("a", a), sess.bind("w", w), sess.bind("c", c)
+    sess.run()
+    torch.cuda.synchronize()
+    first = c.clone()
+    for _ in range(3):
+        sess.run()
+    torch.cuda.synchronize()
+    assert torch.equal(first, c)
+    h = a.float() @ w.float()
+    want = (torch.nn.functional.silu(h[:, : n // 2]) * h[:, n // 2:]) if silu else h
+    err = ((c.float() - want).norm() / want.norm()).item()
+    assert err < 1e-2, err

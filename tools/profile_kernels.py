@@ -43,6 +43,8 @@ if which in ("all", "gemm"):
     gemm(T, H, 6144)
 if which == "proj":  # the four Llama-3-8B projections at TP=1 (bench roofline shapes)
     gemm(T, H, 6144), gemm(T, H, 4096), gemm(T, H, 28672), gemm(T, 14336, H)
+if which == "splitk":  # decode nano-batch down projection (S = 4 split-K) and decode O
+    gemm(256, 14336, H), gemm(512, 4096, 6144)
 if which == "proj_tp8":  # per-rank shapes at TP=8
     gemm(T, H, 768), gemm(T, 512, H), gemm(T, H, 3584), gemm(T, 1792, H)
 if which in ("all", "gemm_silu"):
