@@ -411,7 +411,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t tcol = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN);
       if constexpr (GROUPED) {
-        store_tile_direct<EPI>(tcol, c_out, ldc, gtab[1 + 3 * mb] + quarter * 32 + lane, gtab[2 + 3 * mb], nb);
+        // whole 32-row slabs inside the expert segment go out by TMA; only the
+        // slab straddling the segment end (rows past it belong to the next
+        // expert's tile) is stored row by row
+        const int64_t r0 = gtab[1 + 3 * mb] + quarter * 32, r_end = gtab[2 + 3 * mb];
+        if (r0 + 32 <= r_end)
+          store_tile<EPI>(&map_c, tcol, stg, buf, lane, nb, r0, M);
+        else
+          store_tile_direct<EPI>(tcol, c_out, ldc, r0 + lane, r_end, nb);
       } else {
         store_tile<EPI>(&map_c, tcol, stg, buf, lane, nb, mb * BM + quarter * 32, M);
       }
@@ -1006,11 +1013,12 @@ void gemm_bf16_grouped(const GemmArgs& g, const int32_t* gtab, int64_t max_mtile
   const int64_t tiles = max_mtiles * (group_n / BN);
   if (tiles < grid) grid = static_cast<int>(std::max<int64_t>(tiles, 1));
   auto* c = static_cast<__nv_bfloat16*>(g.c);
+  const CUtensorMap mc = make_map(g.c, g.epi == 1 ? group_n / 2 : group_n, g.m, g.ldc, 64, 32);
   if (g.epi == 1)
-    launch_pdl(gemm_tc_kernel<1, true>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, ma, g.m, group_n, g.k,
+    launch_pdl(gemm_tc_kernel<1, true>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, group_n, g.k,
                gtab, c, g.ldc);
   else
-    launch_pdl(gemm_tc_kernel<0, true>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, ma, g.m, group_n, g.k,
+    launch_pdl(gemm_tc_kernel<0, true>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, group_n, g.k,
                gtab, c, g.ldc);
 }
 

@@ -33,7 +33,7 @@ namespace opflow {
 
 namespace {
 
-constexpr int kChunk = 1024;  // slots per routing chunk
+constexpr int kChunk = 256;  // slots per routing chunk (one hist CTA / one assign warp each)
 constexpr int kMaxE = 1024;
 
 __device__ __forceinline__ bool valid_id(int64_t e, int E) { return e >= 0 && e < E; }
@@ -128,47 +128,83 @@ __global__ void __launch_bounds__(256) route_hist_kernel(const int64_t* __restri
 }
 
 // One CTA: base[c][e] = off[e] + sum_{c' < c} cnt[c'][e]  (in place over cnt),
-// and (optionally) the grouped-GEMM tile table.
+// and (optionally) the grouped-GEMM tile table.  Thread (part p, expert e)
+// owns a contiguous range of chunks of column e (P = 1024 / E parts): range
+// sums -> per-part prefixes -> a block-wide scan over experts (totals and
+// tile counts) -> the range rewritten as running bases.  Loads are batched 8
+// deep so the latency of the column walk is paid C / (8 P) times, not C.
 __global__ void __launch_bounds__(1024) route_scan_kernel(int32_t* __restrict__ cnt, int chunks, int E,
                                                           int32_t* __restrict__ gtab, int tile_m,
                                                           int32_t* __restrict__ tot_out, int32_t* __restrict__ off_out) {
   pdl_wait();
-  __shared__ int32_t tot[kMaxE], off[kMaxE + 1], toff[kMaxE + 1];
-  const int e = threadIdx.x;
-  int32_t run = 0;
-  if (e < E)
-    for (int c = 0; c < chunks; ++c) {
-      const int32_t v = cnt[static_cast<int64_t>(c) * E + e];
-      cnt[static_cast<int64_t>(c) * E + e] = run;
-      run += v;
-    }
-  if (e < E) tot[e] = run;
+  __shared__ int32_t psum[1024], sc[kMaxE], st[kMaxE];
+  const int tid = threadIdx.x;
+  const int P = E >= 1024 ? 1 : 1024 / E;
+  const int e = tid % E, p = tid / E;
+  const bool act = tid < P * E;
+  const int c0 = act ? static_cast<int>(static_cast<int64_t>(p) * chunks / P) : 0;
+  const int c1 = act ? static_cast<int>(static_cast<int64_t>(p + 1) * chunks / P) : 0;
+  int32_t sum = 0;
+  for (int c = c0; c < c1; c += 8) {
+    int32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = c + i < c1 ? cnt[static_cast<int64_t>(c + i) * E + e] : 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sum += v[i];
+  }
+  if (act) psum[tid] = sum;
   __syncthreads();
-  if (e == 0) {
-    int32_t a = 0, b = 0;
-    for (int i = 0; i < E; ++i) {
-      off[i] = a;
-      toff[i] = b;
-      a += tot[i];
-      b += (tot[i] + tile_m - 1) / tile_m;
+  if (act && p == 0) {  // exclusive prefix over this expert's parts; totals
+    int32_t r = 0;
+    for (int q = 0; q < P; ++q) {
+      const int32_t t = psum[q * E + e];
+      psum[q * E + e] = r;
+      r += t;
     }
-    off[E] = a;
-    toff[E] = b;
-    if (gtab) gtab[0] = b;
+    sc[e] = r;
+    st[e] = (r + tile_m - 1) / tile_m;
   }
   __syncthreads();
-  if (e < E) {
-    const int32_t o = off[e];
-    if (tot_out) tot_out[e] = tot[e];
-    if (off_out) off_out[e] = o;
-    for (int c = 0; c < chunks; ++c) cnt[static_cast<int64_t>(c) * E + e] += o;
-    if (gtab) {
-      const int32_t end = o + tot[e];
-      int32_t* g = gtab + 1 + 3 * toff[e];
-      for (int32_t r = o, i = 0; r < end; r += tile_m, ++i) {
-        g[3 * i] = r;
-        g[3 * i + 1] = end;
-        g[3 * i + 2] = e;
+  for (int d = 1; d < E; d <<= 1) {  // inclusive scan over experts (rows, tiles)
+    int32_t a = 0, b = 0;
+    if (tid < E && tid >= d) {
+      a = sc[tid - d];
+      b = st[tid - d];
+    }
+    __syncthreads();
+    if (tid < E && tid >= d) {
+      sc[tid] += a;
+      st[tid] += b;
+    }
+    __syncthreads();
+  }
+  if (gtab && tid == 0) gtab[0] = st[E - 1];
+  if (act) {
+    const int32_t off = e ? sc[e - 1] : 0;
+    int32_t run = off + psum[tid];
+    for (int c = c0; c < c1; c += 8) {
+      int32_t v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = c + i < c1 ? cnt[static_cast<int64_t>(c + i) * E + e] : 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (c + i < c1) {
+          cnt[static_cast<int64_t>(c + i) * E + e] = run;
+          run += v[i];
+        }
+    }
+    if (p == 0) {
+      const int32_t tot = sc[e] - off;
+      if (tot_out) tot_out[e] = tot;
+      if (off_out) off_out[e] = off;
+      if (gtab) {
+        const int32_t end = off + tot;
+        int32_t* g = gtab + 1 + 3 * (e ? st[e - 1] : 0);
+        for (int32_t r = off, i = 0; r < end; r += tile_m, ++i) {
+          g[3 * i] = r;
+          g[3 * i + 1] = end;
+          g[3 * i + 2] = e;
+        }
       }
     }
   }
