@@ -197,11 +197,16 @@ def time_candidates(torch, sess, cands, steps, warmup, stream, world, rounds=3, 
     import statistics
     first = next(iter(cands.values()))
     if soak_s > 0:
+        # a fixed step count agreed by all ranks (collectives must match)
+        sess.run(first, stream)
+        torch.cuda.synchronize()
         t0 = time.time()
-        while time.time() - t0 < soak_s:
-            for _ in range(4):
-                sess.run(first, stream)
-            torch.cuda.synchronize()
+        sess.run(first, stream)
+        torch.cuda.synchronize()
+        one = allreduce_max(time.time() - t0, world)
+        for _ in range(max(1, min(2000, int(soak_s / max(one, 1e-4))))):
+            sess.run(first, stream)
+        torch.cuda.synchronize()
     per = {k: [] for k in cands}
     for _ in range(rounds):
         for k, spec in cands.items():

@@ -122,6 +122,8 @@ def lib() -> C.CDLL:
                 f"g.build()'` (no CPU fallback exists for the device path)")
         _lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | C.RTLD_GLOBAL)
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("OPF_LIB") and not hasattr(_lib, name):
+                continue  # an older A/B variant build may predate a symbol
             fn = getattr(_lib, name)
             fn.restype = res
             fn.argtypes = args

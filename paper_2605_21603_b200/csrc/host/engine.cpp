@@ -517,9 +517,9 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
       pd.launches.push_back(std::move(l));
     } else {
       // Epilogue fusion (per-subgraph compilation): a bf16
-      // MatMul whose output feeds only a silu_mul of the same dispatch runs as
-      // ONE tcgen05 GEMM with the SiLU-mul epilogue; its [T, 2I] output never
-      // touches HBM.
+      // MatMul whose output feeds only a silu_mul (or a rope) of the same
+      // dispatch runs as ONE tcgen05 GEMM with the SiLU-mul (RoPE) epilogue;
+      // the un-activated [T, 2I] (un-rotated qkv) never touches HBM.
       std::map<int32_t, int32_t> fused_act;  // matmul op -> silu_mul op
       std::set<int32_t> skip;
       if (cfg_.fuse) {
@@ -535,7 +535,13 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
               std::find(b_out.begin(), b_out.end(), t) != b_out.end())
             continue;
           const OperatorNode& act = g_.ops[cons[0]];
-          if (act.kind != OperatorKind::kCustom || act.attrs.custom_name != "silu_mul") continue;
+          if (act.kind != OperatorKind::kCustom) continue;
+          const bool silu = act.attrs.custom_name == "silu_mul";
+          // RoPE epilogue: 128-wide heads tiling N (two per 256-column tile)
+          const auto hd = act.attrs.params.find("head_dim");
+          const bool rope = act.attrs.custom_name == "rope" && act.inputs.size() == 2 && act.inputs[0] == t &&
+                            hd != act.attrs.params.end() && hd->second == 128.0;
+          if (!silu && !rope) continue;
           fused_act[op] = cons[0];
           skip.insert(cons[0]);
         }
@@ -553,18 +559,22 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
             scratch.push_back(blk);
             view_of[a_out] = arena_view(blk, a_out, 0, nrows);
           }
+          const bool rope = act.attrs.custom_name == "rope";
           PlannedLaunch l;
           l.op = op;
           l.kind = OperatorKind::kMatMul;
           l.attrs = node.attrs;
-          l.attrs.params["epi"] = 1.0;
+          if (rope)
+            for (const auto& kv : act.attrs.params) l.attrs.params[kv.first] = kv.second;
+          l.attrs.params["epi"] = rope ? 2.0 : 1.0;
           l.name = node.name + "+" + act.name;
           l.rows = nrows;
           l.in.push_back(view_of.at(node.inputs[0]));
           l.in.push_back(weight_view(node.inputs[1], node));
+          if (rope) l.in.push_back(view_of.at(act.inputs[1]));  // positions
           l.out.push_back(view_of.at(a_out));
           l.prepacked = node.inputs[1];
-          l.prepack_mode = 1;
+          l.prepack_mode = rope ? 0 : 1;
           pd.launches.push_back(std::move(l));
           continue;
         }

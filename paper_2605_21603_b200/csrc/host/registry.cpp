@@ -7,6 +7,8 @@
 #include "opflow/nccl_api.hpp"
 #include "opflow/device.hpp"
 
+#include <cmath>
+
 namespace opflow {
 
 bool allreduce_p2p(const opf_comm* c, const opf_view& in, opf_view& out, int64_t rows, int max_ctas,
@@ -98,9 +100,10 @@ ncclDataType_t nccl_type(int32_t dt) {
 size_t kind_workspace(const opf_op_ctx& c, const opf_view* in, int n_in, const opf_view* out, int n_out,
                       int64_t rows) {
   // bf16 MatMul on the tcgen05 path: split-K partials for under-filled grids
-  if (static_cast<OperatorKind>(c.kind) == OperatorKind::kMatMul && n_in == 2 && n_out >= 1 &&
+  if (static_cast<OperatorKind>(c.kind) == OperatorKind::kMatMul && n_in >= 2 && n_out >= 1 &&
       in[0].dtype == OPF_BF16) {
     const int epi = static_cast<int>(ctx_param(c, "epi", 0.0));
+    if (epi == 2) return 0;  // RoPE epilogue runs unsplit
     const int64_t N = out[0].shape[1] * (epi == 1 ? 2 : 1);
     return gemm_splitk_workspace(rows, N, in[0].shape[1], c.max_ctas);
   }
@@ -119,14 +122,15 @@ opf_status launch_kind(const opf_op_ctx& c, const opf_view* in, int n_in, opf_vi
   try {
     switch (kind) {
       case OperatorKind::kMatMul: {
-        if (n_in != 2) return op_error(Errc::ShapeMismatch, "MatMul takes 2 inputs");
+        const int epi = static_cast<int>(ctx_param(c, "epi", 0.0));  // 1: fused SiLU-mul, 2: fused RoPE
+        if (n_in != (epi == 2 ? 3 : 2))
+          return op_error(Errc::ShapeMismatch, epi == 2 ? "MatMul+RoPE takes (x, w, positions)" : "MatMul takes 2 inputs");
         const int64_t K = in[0].shape[1];
-        const int epi = static_cast<int>(ctx_param(c, "epi", 0.0));  // 1: fused SiLU-mul
         const int64_t N = out[0].shape[1] * (epi == 1 ? 2 : 1);
         if (in[1].shape[0] != K || in[1].shape[1] != N)
           return op_error(Errc::ShapeMismatch, "MatMul weight must be [K,N]");
-        if (epi == 1 && (dt != Dtype::kBF16 || !c.aux))
-          return op_error(Errc::ShapeMismatch, "SiLU-mul epilogue needs the packed bf16 weight");
+        if (epi >= 1 && (dt != Dtype::kBF16 || !c.aux))
+          return op_error(Errc::ShapeMismatch, "fused epilogues need the packed bf16 weight");
         if (dt == Dtype::kBF16) {
           GemmArgs g{};
           g.a = view_ptr(in[0]);
@@ -140,6 +144,16 @@ opf_status launch_kind(const opf_op_ctx& c, const opf_view* in, int n_in, opf_vi
           g.epi = epi;
           g.ws = c.workspace;
           g.ws_bytes = c.workspace_bytes;
+          if (epi == 2) {  // RoPE epilogue: rotate-half on q/k heads (params of the fused rope op)
+            const int nq = static_cast<int>(ctx_param(c, "heads", 1));
+            const int nkv = static_cast<int>(ctx_param(c, "kv_heads", 1));
+            if (static_cast<int>(ctx_param(c, "head_dim", 128)) != 128 || N != static_cast<int64_t>(nq + 2 * nkv) * 128)
+              return op_error(Errc::ShapeMismatch, "RoPE epilogue needs head_dim 128 and N = (heads + 2 kv_heads) * 128");
+            if (in[2].dtype != OPF_I64) return op_error(Errc::ShapeMismatch, "RoPE positions must be i64");
+            g.pos = vptr<const int64_t>(in[2]);
+            g.rot_heads = nq + nkv;
+            g.log2_theta = static_cast<float>(std::log2(ctx_param(c, "theta", 10000.0)));
+          }
           if (c.aux) {  // pre-packed [N,K] weight -> tcgen05 path
             g.bt = c.aux;
             gemm_bf16_tc(g, s);

@@ -125,7 +125,11 @@ struct GemmArgs {
   int64_t m, n, k, lda, ldc;
   int max_ctas;    // 0 = all SMs
   bool b_kn;       // simt path only: B given as [K,N] row-major instead of [N,K]
-  int epi;         // 0 plain; 1 SiLU-mul (Bt packed by k_pack_gate_up, C is [M, N/2])
+  int epi;         // 0 plain; 1 SiLU-mul (Bt packed by k_pack_gate_up, C is [M, N/2]);
+                   // 2 rotate-half RoPE on 128-wide q/k heads (C = rope(A B^T))
+  const int64_t* pos;  // epi 2: per-row positions
+  int rot_heads;       // epi 2: heads [0, rot_heads) rotated, the rest copied
+  float log2_theta;    // epi 2
   void* ws;        // split-K workspace (gemm_splitk_workspace bytes), nullptr = no split
   size_t ws_bytes;
 };

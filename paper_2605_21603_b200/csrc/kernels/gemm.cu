@@ -73,6 +73,12 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const __nv_bfloat16* __r
 
 // ------------------------------------------------------------------ tcgen05 path
 constexpr int BM = 128, BN = 256, BK = 64;
+// EPI 2 (RoPE epilogue): a 256-column tile holds two 128-wide heads.
+struct RopeArgs {
+  const int64_t* pos;
+  int rot_heads;
+  float log2_theta;
+};
 constexpr int kStages = 4;
 constexpr int kAccStages = 2;
 constexpr int kEpiWarps = 4;
@@ -191,10 +197,18 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t m_blocks, int64_t
 //   EPI 0: plain, 256 output columns at nb*256.
 //   EPI 1: SiLU-mul, the weight was packed so tile columns [0,128) are gate and
 //          [128,256) the matching up columns; 128 outputs at nb*128.
+__device__ void store_tile_rope(const CUtensorMap* map_c, uint32_t tmem_col0, uint8_t* const (&stg)[2], int lane,
+                                int64_t nb, int64_t row0, int64_t M, const RopeArgs& rope);
+
 template <int EPI, int TN = BN>
 __device__ __forceinline__ void store_tile(const CUtensorMap* map_c, uint32_t tmem_col0,
                                            uint8_t* const (&stg)[2], int& buf, int lane, int64_t nb,
-                                           int64_t row0, int64_t M, int first = 0, int step = 1) {
+                                           int64_t row0, int64_t M, int first = 0, int step = 1,
+                                           const RopeArgs* rope = nullptr) {
+  if constexpr (EPI == 2) {
+    store_tile_rope(map_c, tmem_col0, stg, lane, nb, row0, M, *rope);
+    return;
+  }
   // EPI 1 needs TN = 256 (gate | up halves of 128); chunks are 64 output columns
   constexpr int kChunks = EPI == 1 ? 2 : TN / 64;
 #pragma unroll 1
@@ -291,7 +305,8 @@ template <int EPI, bool GROUPED = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K,
-                   const int32_t* __restrict__ gtab, __nv_bfloat16* __restrict__ c_out, int64_t ldc) {
+                   const int32_t* __restrict__ gtab, __nv_bfloat16* __restrict__ c_out, int64_t ldc,
+                   RopeArgs rope) {
   // GROUPED: gtab = [n_tiles, (row0, row_end, expert) x n_tiles]; N is the per-expert
   // width, expert e's B rows start at e * N; M bounds the A rows.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -420,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         else
           store_tile_direct<EPI>(tcol, c_out, ldc, r0 + lane, r_end, nb);
       } else {
-        store_tile<EPI>(&map_c, tcol, stg, buf, lane, nb, mb * BM + quarter * 32, M);
+        store_tile<EPI>(&map_c, tcol, stg, buf, lane, nb, mb * BM + quarter * 32, M, 0, 1, &rope);
       }
       // accumulator fully read: hand it back to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -517,6 +532,61 @@ __device__ __forceinline__ void stage_commit(const CUtensorMap* map_c, uint8_t* 
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
   buf ^= 1;
+}
+
+// RoPE epilogue (EPI 2, TN = 256): this warp's 32 rows of the two 128-wide
+// heads of the tile.  Rotate-half on q/k heads (global head < rot_heads):
+//   out[d] = a cos - b sin, out[d + 64] = b cos + a sin,  a = x[d], b = x[d + 64],
+//   angle = pos * theta^(-d / 64)  (HF / the rope op in llama_ops.cu),
+// applied to the fp32 accumulator before the bf16 rounding; v heads copied.
+// Both staging buffers hold one head (dims 0-63 | 64-127).
+__device__ void store_tile_rope(const CUtensorMap* map_c, uint32_t tmem_col0, uint8_t* const (&stg)[2], int lane,
+                                int64_t nb, int64_t row0, int64_t M, const RopeArgs& rope) {
+  const int64_t row = row0 + lane;
+  const float p = row < M ? static_cast<float>(rope.pos[row]) : 0.0f;
+#pragma unroll 1
+  for (int hh = 0; hh < 2; ++hh) {
+    const bool rot = nb * 2 + hh < rope.rot_heads;
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
+#pragma unroll 1
+    for (int j = 0; j < 2; ++j) {
+      uint32_t a[32], b[32];
+      tmem_ld32(tmem_col0 + static_cast<uint32_t>(hh * 128 + j * 32), a);
+      tmem_ld32(tmem_col0 + static_cast<uint32_t>(hh * 128 + 64 + j * 32), b);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      float ra[32], rb[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float x = __uint_as_float(a[i]), y = __uint_as_float(b[i]);
+        if (rot) {
+          // angle reduced to [-pi, pi] (two-constant Cody-Waite), then the MUFU
+          // sin/cos (abs err ~2^-21 there; the bf16 output rounds at 2^-8)
+          const float inv_freq = exp2f(-2.0f * static_cast<float>(j * 32 + i) / 128.0f * rope.log2_theta);
+          const float ang = p * inv_freq;
+          const float q = rintf(ang * 0.15915494309189535f);
+          const float r = fmaf(-q, 6.28318548202514648f, fmaf(-q, -1.7484556e-07f, ang));
+          float sn, cs;
+          __sincosf(r, &sn, &cs);
+          ra[i] = x * cs - y * sn;
+          rb[i] = y * cs + x * sn;
+        } else {
+          ra[i] = x;
+          rb[i] = y;
+        }
+      }
+      stage_half(stg[0], ra, j, lane);
+      stage_half(stg[1], rb, j, lane);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0 && row0 < M) {
+      const int32_t col = static_cast<int32_t>(nb * 256 + hh * 128);
+      tma_store_2d(map_c, stg[0], col, static_cast<int32_t>(row0));
+      tma_store_2d(map_c, stg[1], col + 64, static_cast<int32_t>(row0));
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
 }
 
 // One epilogue warp's share of split `mine` of tile `tile`.  The accumulator
@@ -651,7 +721,7 @@ template <int EPI, int TN, bool SPLIT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K, int splits,
-                    float4* __restrict__ ws, int* __restrict__ sem) {
+                    float4* __restrict__ ws, int* __restrict__ sem, RopeArgs rope) {
   using C = Tc2Cfg<TN, SPLIT>;
   constexpr int kStages2 = C::kStages;
   constexpr uint32_t kStageBytes2 = C::kStageBytes;
@@ -787,7 +857,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
         store_tile_splitk<EPI>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, static_cast<int>(rank) * 8 + ew, t,
                                static_cast<int>(u % splits), splits, ws, sem, release);
       } else {
-        store_tile<EPI, TN>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, kStep);
+        store_tile<EPI, TN>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, kStep, &rope);
         release();
       }
       if (++acc == kAccStages) {
@@ -847,6 +917,10 @@ void gemm_bf16_tc_init() {
                                   static_cast<int>(kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -918,7 +992,9 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
            reinterpret_cast<uintptr_t>(g.c)) % 16 == 0,
           Errc::ShapeMismatch, "tcgen05 GEMM needs 16-byte aligned base pointers");
   require(g.epi == 0 || g.n % BN == 0, Errc::ShapeMismatch,
-          "SiLU-mul epilogue needs N (= 2 x inter) to be a multiple of 256");
+          "SiLU-mul / RoPE epilogues need N to be a multiple of 256");
+  require(g.epi != 2 || g.pos != nullptr, Errc::ShapeMismatch, "RoPE epilogue needs positions");
+  const RopeArgs rope{g.pos, g.rot_heads, g.log2_theta};
   gemm_bf16_tc_init();
   static const int mode = [] {  // OPF_GEMM=1sm|2sm|auto
     const char* e = std::getenv("OPF_GEMM");
@@ -950,7 +1026,7 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     }
     const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, static_cast<uint32_t>(tn / 2));
     const int64_t tiles = mt * ((g.n + tn - 1) / tn);
-    int splits = tn == 256 ? gemm_splitk_splits(g.m, g.n, g.k, g.max_ctas) : 1;
+    int splits = tn == 256 && g.epi != 2 ? gemm_splitk_splits(g.m, g.n, g.k, g.max_ctas) : 1;
     float4* ws = nullptr;
     int* sem = nullptr;
     if (splits > 1) {
@@ -968,33 +1044,39 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     const dim3 blocks(2u * static_cast<unsigned>(std::max(clusters, 1)));
     if (splits > 1 && g.epi == 1)
       launch_pdl(gemm_tc2_kernel<1, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
-                 g.m, g.n, g.k, splits, ws, sem);
+                 g.m, g.n, g.k, splits, ws, sem, rope);
     else if (splits > 1)
       launch_pdl(gemm_tc2_kernel<0, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
-                 g.m, g.n, g.k, splits, ws, sem);
+                 g.m, g.n, g.k, splits, ws, sem, rope);
+    else if (g.epi == 2)
+      launch_pdl(gemm_tc2_kernel<2, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb,
+                 mc, g.m, g.n, g.k, 1, ws, sem, rope);
     else if (g.epi == 1)
       launch_pdl(gemm_tc2_kernel<1, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, splits, ws, sem);
+                 g.n, g.k, splits, ws, sem, rope);
     else if (tn == 256)
       launch_pdl(gemm_tc2_kernel<0, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, splits, ws, sem);
+                 g.n, g.k, splits, ws, sem, rope);
     else if (tn == 192)
       launch_pdl(gemm_tc2_kernel<0, 192>, blocks, dim3(Tc2Cfg<192, false>::kThreads), Tc2Cfg<192, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, 1, ws, sem);
+                 g.n, g.k, 1, ws, sem, rope);
     else
       launch_pdl(gemm_tc2_kernel<0, 128>, blocks, dim3(Tc2Cfg<128, false>::kThreads), Tc2Cfg<128, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, 1, ws, sem);
+                 g.n, g.k, 1, ws, sem, rope);
     return;
   }
   const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN);
   const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN);
   if (tiles < grid) grid = static_cast<int>(tiles);
-  if (g.epi == 1)
+  if (g.epi == 2)
+    launch_pdl(gemm_tc_kernel<2>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, g.n, g.k,
+               static_cast<const int32_t*>(nullptr), static_cast<__nv_bfloat16*>(nullptr), int64_t{0}, rope);
+  else if (g.epi == 1)
     launch_pdl(gemm_tc_kernel<1>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, g.n, g.k,
-               static_cast<const int32_t*>(nullptr), static_cast<__nv_bfloat16*>(nullptr), int64_t{0});
+               static_cast<const int32_t*>(nullptr), static_cast<__nv_bfloat16*>(nullptr), int64_t{0}, rope);
   else
     launch_pdl(gemm_tc_kernel<0>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, g.n, g.k,
-               static_cast<const int32_t*>(nullptr), static_cast<__nv_bfloat16*>(nullptr), int64_t{0});
+               static_cast<const int32_t*>(nullptr), static_cast<__nv_bfloat16*>(nullptr), int64_t{0}, rope);
 }
 
 // Grouped (per-expert) GEMM: rows of `a` are expert-sorted segments, gtab the
@@ -1016,10 +1098,10 @@ void gemm_bf16_grouped(const GemmArgs& g, const int32_t* gtab, int64_t max_mtile
   const CUtensorMap mc = make_map(g.c, g.epi == 1 ? group_n / 2 : group_n, g.m, g.ldc, 64, 32);
   if (g.epi == 1)
     launch_pdl(gemm_tc_kernel<1, true>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, group_n, g.k,
-               gtab, c, g.ldc);
+               gtab, c, g.ldc, RopeArgs{});
   else
     launch_pdl(gemm_tc_kernel<0, true>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, group_n, g.k,
-               gtab, c, g.ldc);
+               gtab, c, g.ldc, RopeArgs{});
 }
 
 // [K, 2I] gate|up weight -> K-major [2I, K] with gate/up interleaved in 128-row

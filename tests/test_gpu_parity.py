@@ -356,3 +356,51 @@ def test_gemm_splitk_deterministic(cuda, m, n, k, silu):
     want = (torch.nn.functional.silu(h[:, : n // 2]) * h[:, n // 2:]) if silu else h
     err = ((c.float() - want).norm() / want.norm()).item()
     assert err < 1e-2, err
+
+
+def _rope_ref(x, pos, nq, nkv, theta=10000.0):
+    """HF rotate-half on the q/k heads of [T, (nq+2nkv)*128] fp32 (v copied)."""
+    import torch
+    T = x.shape[0]
+    h = x.view(T, nq + 2 * nkv, 128).clone()
+    inv = theta ** (-torch.arange(0, 64, device=x.device, dtype=torch.float32) / 64.0)
+    ang = pos.float()[:, None] * inv[None, :]
+    c, s = torch.cos(ang)[:, None, :], torch.sin(ang)[:, None, :]
+    a, b = h[:, : nq + nkv, :64].clone(), h[:, : nq + nkv, 64:].clone()
+    h[:, : nq + nkv, :64] = a * c - b * s
+    h[:, : nq + nkv, 64:] = b * c + a * s
+    return h.view(T, -1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,nq,nkv", [(8192, 4, 1), (512, 32, 8), (100, 8, 2), (1024, 2, 1)])
+def test_gemm_rope_epilogue_fused(cuda, m, nq, nkv):
+    """MatMul -> rope in one dispatch runs as ONE tcgen05 GEMM with the RoPE
+    epilogue (q/k heads rotated on the fp32 accumulator, v heads copied);
+    matches torch fp32 rope(a @ w)."""
+    import torch
+    K, N = 512, (nq + 2 * nkv) * 128
+    g = torch.Generator(device="cuda").manual_seed(m + nq)
+    a = (torch.rand(m, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w = ((torch.rand(K, N, device="cuda", generator=g) * 2 - 1) / K ** 0.5).to(torch.bfloat16)
+    pos = (torch.arange(m, device="cuda") % 700).to(torch.int64)
+    tens = [{"name": "a", "shape": [m, K], "dtype": "bf16", "role": "input"},
+            {"name": "pos", "shape": [m], "dtype": "i64", "role": "input"},
+            {"name": "w", "shape": [K, N], "batch": "replicated", "dtype": "bf16", "role": "weight"},
+            {"name": "qkv", "shape": [m, N], "dtype": "bf16"},
+            {"name": "c", "shape": [m, N], "dtype": "bf16", "role": "output"}]
+    ops = [{"name": "qkv_proj", "kind": "MatMul", "inputs": ["a", "w"], "outputs": ["qkv"]},
+           {"name": "rope", "kind": "Custom", "inputs": ["qkv", "pos"], "outputs": ["c"],
+            "attrs": {"custom_name": "rope", "params": {"heads": nq, "kv_heads": nkv, "head_dim": 128,
+                                                        "theta": 10000.0}}}]
+    gr = of.build_graph(json.dumps({"tensors": tens, "operators": ops}))
+    sess = of.Session(gr, of.partition(gr, []), {"lanes": 1})
+    c = torch.empty(m, N, dtype=torch.bfloat16, device="cuda")
+    sess.bind("a", a), sess.bind("w", w), sess.bind("pos", pos), sess.bind("c", c)
+    sess.run()
+    torch.cuda.synchronize()
+    names = [l["name"] for d in sess.schedule()["dispatches"] for l in d["launches"]]
+    assert names == ["qkv_proj+rope"], names
+    want = _rope_ref(a.float() @ w.float(), pos, nq, nkv)
+    err = ((c.float() - want).norm() / want.norm()).item()
+    assert err < 1e-2, err
