@@ -317,18 +317,57 @@ def run_ours(args):
     stats = sess.stats()
     launches = stats["last"]["launches"]
 
-    # ---- e2e through the C-ABI with host buffers (pinned), copies in the timed region
-    xh = torch.empty(T, LLAMA["hidden"], dtype=torch.bfloat16, pin_memory=True)
-    xh.copy_(bufs["x"].cpu())
-    oh = torch.empty(T, LLAMA["hidden"], dtype=torch.bfloat16, pin_memory=True)
+    # ---- e2e through the public Session API with pinned HOST buffers: every
+    # step copies its input H2D and its output D2H inside the timed region.
+    # Two sessions (shared weights, own activation arenas) alternate so that
+    # step i+1's H2D and step i-1's D2H ride the copy engines while step i
+    # computes (a serving loop's double buffering).
     spec = cands[best]
+    H = LLAMA["hidden"]
+    x2 = [bufs["x"], torch.empty_like(bufs["x"])]
+    o2 = [bufs[out_name], torch.empty_like(bufs[out_name])]
+    sess_b = of.Session(g, plan, {"lanes": 3, "device": dev.index}, comm)
+    for t in g.description["tensors"]:
+        if t["role"] == "weight":
+            sess_b.bind(t["name"], bufs[t["name"]])
+    sess_b.bind("x", x2[1]), sess_b.bind(out_name, o2[1]), sess_b.bind("positions", pos)
+    sessions = [sess, sess_b]
+    xh = [torch.empty(T, H, dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
+    oh = [torch.empty(T, H, dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
+    for h in xh:
+        h.copy_(bufs["x"].cpu())
+    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    comp_done = [torch.cuda.Event(), torch.cuda.Event()]
+    in_ready = [torch.cuda.Event(), torch.cuda.Event()]
 
-    def e2e_step():
-        bufs["x"].copy_(xh, non_blocking=True)
-        sess.run(spec, stream)
-        oh.copy_(bufs[out_name], non_blocking=True)
+    def e2e_steps(n, first):
+        for i in range(first, first + n):
+            b = i % 2
+            h2d.wait_event(comp_done[b])          # step i-2 finished reading this buffer
+            with torch.cuda.stream(h2d):
+                x2[b].copy_(xh[b], non_blocking=True)
+            in_ready[b].record(h2d)
+            stream.wait_event(in_ready[b])
+            sessions[b].run(spec, stream)
+            comp_done[b].record(stream)
+            d2h.wait_event(comp_done[b])
+            with torch.cuda.stream(d2h):
+                oh[b].copy_(o2[b], non_blocking=True)
+        fin = torch.cuda.Event()
+        fin.record(d2h)
+        stream.wait_event(fin)
 
-    e2e_ms = time_steps(torch, e2e_step, args.steps, args.warmup, stream, world)
+    e2e_steps(args.warmup, 0)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h2d.wait_event(e0)
+    e2e_steps(args.steps, args.warmup)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = allreduce_max(e0.elapsed_time(e1) / args.steps, world)
+    del sess_b
     e2e_val = tokens_job / (e2e_ms / 1e3)
 
     # ---- roofline of the dominant kernel (tcgen05 GEMM), per-rank shapes
@@ -383,8 +422,9 @@ def run_ours(args):
                 "ms_per_step": round(auto_ms, 3), "chosen": auto_pick,
                 "speedup_vs_sequential": round(seq_ms / auto_ms, 4)},
             "e2e": {"value": round(e2e_val, 1), "unit": "tokens/s",
-                    "h2d_bytes_per_step": int(xh.numel() * 2),
-                    "d2h_bytes_per_step": int(oh.numel() * 2)},
+                    "h2d_bytes_per_step": int(xh[0].numel() * 2),
+                    "d2h_bytes_per_step": int(oh[0].numel() * 2),
+                    "pipelining": "two sessions alternate; step i+1 H2D and step i-1 D2H overlap step i"},
             "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05, bf16)",
                          "achieved": round(achieved, 1),
                          "peak": PEAKS["bf16_tflops"], "unit": "TFLOP/s",
