@@ -140,6 +140,9 @@ int gemm_splitk_splits(int64_t m, int64_t n, int64_t k, int max_ctas);
 size_t gemm_splitk_workspace(int64_t m, int64_t n, int64_t k, int max_ctas);
 // Grouped per-expert GEMM (MoE): gtab = device tile table [n, (row0, row_end, expert) x n],
 // bt = [n_groups * group_n, K]; g.m bounds the rows of a / c, g.n is unused.
+// rows per grouped-GEMM tile (128: 1-SM, default; 256: 2-CTA pairs, OPF_MOE_TILE=256);
+// the routing kernels build the tile table with the same height
+int moe_tile_m();
 void gemm_bf16_grouped(const GemmArgs& g, const int32_t* gtab, int64_t max_mtiles, int64_t group_n,
                        int64_t n_groups, cudaStream_t s);
 void k_pack_gate_up(const void* src, void* dst, int64_t K, int64_t I, cudaStream_t s);

@@ -717,11 +717,17 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
                : "memory");
 }
 
-template <int EPI, int TN, bool SPLIT = false>
+// GROUPED (MoE experts, TN = 256, unsplit): gtab = [n_tiles, (row0, row_end,
+// expert) x n_tiles] with 256-row tiles; N is the per-expert width, expert e's
+// B rows start at e * N; rows of a tile past row_end belong to the next
+// expert's tile (computed, never stored).
+template <int EPI, int TN, bool SPLIT = false, bool GROUPED = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K, int splits,
-                    float4* __restrict__ ws, int* __restrict__ sem, RopeArgs rope) {
+                    float4* __restrict__ ws, int* __restrict__ sem, RopeArgs rope,
+                    const int32_t* __restrict__ gtab = nullptr, __nv_bfloat16* __restrict__ c_out = nullptr,
+                    int64_t ldc = 0) {
   using C = Tc2Cfg<TN, SPLIT>;
   constexpr int kStages2 = C::kStages;
   constexpr uint32_t kStageBytes2 = C::kStageBytes;
@@ -739,10 +745,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int64_t m_blocks = (M + 2 * BM - 1) / (2 * BM), n_blocks = (N + TN - 1) / TN;
-  const int64_t tiles = m_blocks * n_blocks;
+  int64_t m_blocks = (M + 2 * BM - 1) / (2 * BM);
+  const int64_t n_blocks = (N + TN - 1) / TN;
   const int k_blocks = static_cast<int>((K + BK - 1) / BK);
-  const int64_t units = tiles * splits;  // unit u = split (u % splits) of tile (u / splits)
   const int64_t cluster = blockIdx.x / 2, n_clusters = gridDim.x / 2;
 
   if (warp == 0) {
@@ -771,6 +776,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();     // inputs of the previous kernel on this stream are visible from here
   pdl_trigger();  // persistent grid: let the next kernel stage its prologue on freed SMs
+  if constexpr (GROUPED) m_blocks = *reinterpret_cast<const volatile int32_t*>(gtab);  // routing kernel output
+  const int64_t tiles = m_blocks * n_blocks;
+  const int64_t units = tiles * splits;  // unit u = split (u % splits) of tile (u / splits)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
@@ -781,8 +789,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
         const int sp = static_cast<int>(u % splits);
         int64_t mb, nb;
         tile_coords(t, m_blocks, n_blocks, mb, nb);
-        const int32_t m0 = static_cast<int32_t>(mb * 2 * BM + rank * BM);
-        const int32_t n0 = static_cast<int32_t>(nb * TN + rank * (TN / 2));
+        int32_t m0 = static_cast<int32_t>(mb * 2 * BM + rank * BM);
+        int32_t n0 = static_cast<int32_t>(nb * TN + rank * (TN / 2));
+        if constexpr (GROUPED) {
+          m0 = gtab[1 + 3 * mb] + static_cast<int32_t>(rank * BM);
+          n0 += static_cast<int32_t>(gtab[3 + 3 * mb] * N);
+        }
         const int kb0 = sp * k_blocks / splits, kb1 = (sp + 1) * k_blocks / splits;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -846,14 +858,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
       tile_coords(t, m_blocks, n_blocks, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int64_t row0 = mb * 2 * BM + rank * BM + quarter * 32;
+      int64_t row0 = mb * 2 * BM + rank * BM + quarter * 32;
+      int64_t row_end = M;
+      if constexpr (GROUPED) {
+        row0 = gtab[1 + 3 * mb] + rank * BM + quarter * 32;
+        row_end = gtab[2 + 3 * mb];
+      }
       const uint32_t tcol = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * TN);
       auto release = [&]() {  // accumulator fully read: hand it back to the MMA warp
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive_leader(&tempty[acc]);
       };
-      if constexpr (SPLIT && TN == 256) {
+      if constexpr (GROUPED) {
+        // whole 32-row slabs inside the expert segment by TMA; the straddling slab row by row
+        if (row0 + 32 <= row_end)
+          store_tile<EPI, TN>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, kStep, &rope);
+        else
+          store_tile_direct<EPI>(tcol, c_out, ldc, row0 + lane, row_end, nb);
+        release();
+      } else if constexpr (SPLIT && TN == 256) {
         store_tile_splitk<EPI>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, static_cast<int>(rank) * 8 + ew, t,
                                static_cast<int>(u % splits), splits, ws, sem, release);
       } else {
@@ -921,6 +945,10 @@ void gemm_bf16_tc_init() {
                                   static_cast<int>(kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 256, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1, 256, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -985,6 +1013,9 @@ size_t gemm_splitk_workspace(int64_t m, int64_t n, int64_t k, int max_ctas) {
          static_cast<size_t>(tiles * 16) * sizeof(int);
 }
 
+constexpr const int32_t* kNoGtab = nullptr;
+constexpr __nv_bfloat16* kNoOut = nullptr;
+
 void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
   require(g.k % 8 == 0 && g.lda % 8 == 0 && g.ldc % 8 == 0, Errc::ShapeMismatch,
           "tcgen05 GEMM needs 16-byte aligned rows (K, lda, ldc multiples of 8)");
@@ -1044,25 +1075,25 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     const dim3 blocks(2u * static_cast<unsigned>(std::max(clusters, 1)));
     if (splits > 1 && g.epi == 1)
       launch_pdl(gemm_tc2_kernel<1, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
-                 g.m, g.n, g.k, splits, ws, sem, rope);
+                 g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
     else if (splits > 1)
       launch_pdl(gemm_tc2_kernel<0, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
-                 g.m, g.n, g.k, splits, ws, sem, rope);
+                 g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
     else if (g.epi == 2)
       launch_pdl(gemm_tc2_kernel<2, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb,
-                 mc, g.m, g.n, g.k, 1, ws, sem, rope);
+                 mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
     else if (g.epi == 1)
       launch_pdl(gemm_tc2_kernel<1, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, splits, ws, sem, rope);
+                 g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
     else if (tn == 256)
       launch_pdl(gemm_tc2_kernel<0, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, splits, ws, sem, rope);
+                 g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
     else if (tn == 192)
       launch_pdl(gemm_tc2_kernel<0, 192>, blocks, dim3(Tc2Cfg<192, false>::kThreads), Tc2Cfg<192, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, 1, ws, sem, rope);
+                 g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
     else
       launch_pdl(gemm_tc2_kernel<0, 128>, blocks, dim3(Tc2Cfg<128, false>::kThreads), Tc2Cfg<128, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, 1, ws, sem, rope);
+                 g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
     return;
   }
   const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN);
@@ -1083,19 +1114,43 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
 // device tile table built by the routing kernel, bt = [E * group_n, K] packed
 // expert weights.  max_mtiles bounds the tile count (grid sizing happens on the
 // host; the actual count is read on the device, so the launch is capturable).
+int moe_tile_m() {
+  static const int t = [] {  // OPF_MOE_TILE=256 selects the 2-CTA grouped kernel (measured no faster:
+                             // tile waste at ~512 rows/expert offsets the pair efficiency)
+    const char* e = std::getenv("OPF_MOE_TILE");
+    return e && std::atoi(e) == 256 ? 256 : 128;
+  }();
+  return t;
+}
+
 void gemm_bf16_grouped(const GemmArgs& g, const int32_t* gtab, int64_t max_mtiles, int64_t group_n,
                        int64_t n_groups, cudaStream_t s) {
   require(g.k % 8 == 0 && g.lda % 8 == 0 && g.ldc % 8 == 0 && group_n % BN == 0, Errc::ShapeMismatch,
           "grouped GEMM needs K, lda, ldc multiples of 8 and a per-expert N multiple of 256");
   gemm_bf16_tc_init();
+  auto* c = static_cast<__nv_bfloat16*>(g.c);
   const CUtensorMap ma = make_map(g.a, g.k, g.m, g.lda, BK, BM);
-  const CUtensorMap mb = make_map(g.bt, g.k, group_n * n_groups, g.k, BK, BN);
+  const CUtensorMap mc = make_map(g.c, g.epi == 1 ? group_n / 2 : group_n, g.m, g.ldc, 64, 32);
   int grid = num_sms();
   if (g.max_ctas > 0 && g.max_ctas < grid) grid = g.max_ctas;
   const int64_t tiles = max_mtiles * (group_n / BN);
+  if (moe_tile_m() == 256) {
+    // 2-CTA pairs on 256-row expert tiles (tile table built with tile_m = 256)
+    const CUtensorMap mb = make_map(g.bt, g.k, group_n * n_groups, g.k, BK, BN / 2);
+    const int clusters = static_cast<int>(std::max<int64_t>(std::min<int64_t>(tiles, std::max(grid / 2, 1)), 1));
+    const dim3 blocks(2u * static_cast<unsigned>(clusters));
+    if (g.epi == 1)
+      launch_pdl(gemm_tc2_kernel<1, 256, false, true>, blocks, dim3(Tc2Cfg<256, false>::kThreads),
+                 Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m, group_n, g.k, 1, static_cast<float4*>(nullptr),
+                 static_cast<int*>(nullptr), RopeArgs{}, gtab, c, g.ldc);
+    else
+      launch_pdl(gemm_tc2_kernel<0, 256, false, true>, blocks, dim3(Tc2Cfg<256, false>::kThreads),
+                 Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m, group_n, g.k, 1, static_cast<float4*>(nullptr),
+                 static_cast<int*>(nullptr), RopeArgs{}, gtab, c, g.ldc);
+    return;
+  }
+  const CUtensorMap mb = make_map(g.bt, g.k, group_n * n_groups, g.k, BK, BN);
   if (tiles < grid) grid = static_cast<int>(std::max<int64_t>(tiles, 1));
-  auto* c = static_cast<__nv_bfloat16*>(g.c);
-  const CUtensorMap mc = make_map(g.c, g.epi == 1 ? group_n / 2 : group_n, g.m, g.ldc, 64, 32);
   if (g.epi == 1)
     launch_pdl(gemm_tc_kernel<1, true>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, group_n, g.k,
                gtab, c, g.ldc, RopeArgs{});

@@ -431,7 +431,7 @@ __global__ void tiles_from_counts_kernel(const int64_t* __restrict__ counts, int
 
 // ---------------------------------------------------------------- host ops
 int64_t chunks_of(int64_t n) { return (n + kChunk - 1) / kChunk; }
-int64_t max_tiles(int64_t n, int E) { return n / 128 + E + 1; }
+int64_t max_tiles(int64_t n, int E) { return n / moe_tile_m() + E + 1; }
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 int topk_param(const opf_op_ctx& c) { return static_cast<int>(ctx_param(c, "topk", 8)); }
@@ -443,7 +443,7 @@ void route_plan(const int64_t* ids, int64_t n, int E, char* ws, int32_t* gtab, c
   auto* cnt = reinterpret_cast<int32_t*>(ws);
   const int64_t C = chunks_of(n);
   if (C > 0) launch_pdl(route_hist_kernel, dim3(static_cast<unsigned>(C)), dim3(256), 0, s, ids, n, E, cnt);
-  launch_pdl(route_scan_kernel, dim3(1), dim3(1024), 0, s, cnt, static_cast<int>(C), E, gtab, 128, tot, off);
+  launch_pdl(route_scan_kernel, dim3(1), dim3(1024), 0, s, cnt, static_cast<int>(C), E, gtab, moe_tile_m(), tot, off);
 }
 
 opf_status op_moe_topk(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out, int32_t n_out,
@@ -562,7 +562,7 @@ opf_status grouped(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_vi
   } else {
     gtab = reinterpret_cast<int32_t*>(ws);
     launch_pdl(tiles_from_counts_kernel, dim3(1), dim3(32), 0, s, static_cast<const int64_t*>(vptr<int64_t>(in[1])),
-               El, gtab, 128);
+               El, gtab, moe_tile_m());
   }
   GemmArgs g{};
   g.a = view_ptr(in[0]);

@@ -92,3 +92,34 @@ def test_prefill_tcgen05_capped_ctas(cuda):
         of.launch(op, [t], [out], S * seqs, max_ctas=cap)
         torch.cuda.synchronize()
         assert rel_err(out.float().cpu().numpy(), want) < 1e-2, cap
+
+
+@pytest.mark.parametrize("max_ctas", [1, 3, 148])
+def test_decode_tma_ring_wraps_across_items(cuda, max_ctas):
+    """TMA-ring decode: a CTA streams many (sequence, kv head) items through one
+    23-slot ring (wrapping many times, items of 0..45 pages, empty contexts),
+    merging each item while the producer prefetches the next."""
+    import torch
+    rng = np.random.default_rng(max_ctas)
+    B, nq, nkv, hd, page, max_pages = 40, 32, 8, 128, 16, 45
+    ctx = rng.integers(0, max_pages * page, size=B).astype(np.int64)
+    ctx[:3] = [0, 1, max_pages * page]
+    pages = B * max_pages
+    kc = rng.uniform(-1, 1, (pages, page, nkv, hd)).astype(np.float32)
+    vc = rng.uniform(-1, 1, (pages, page, nkv, hd)).astype(np.float32)
+    table = rng.permutation(pages).reshape(B, max_pages).astype(np.int64)
+    qkv = rng.uniform(-1, 1, (B, (nq + 2 * nkv) * hd)).astype(np.float32)
+    tb = lambda a: torch.from_numpy(a).cuda().to(torch.bfloat16)
+    t_qkv, t_k, t_v = tb(qkv), tb(kc), tb(vc)
+    want = oracle.attn_decode(t_qkv.float().cpu().numpy(), t_k.float().cpu().numpy(),
+                              t_v.float().cpu().numpy(), table, ctx, nq, nkv, hd, page)
+    out = torch.empty(B, nq * hd, dtype=torch.bfloat16, device="cuda")
+    op = {"name": "d", "kind": "Custom", "inputs": [], "outputs": [],
+          "attrs": {"custom_name": "attn_decode",
+                    "params": {"heads": nq, "kv_heads": nkv, "head_dim": hd, "page_size": page}}}
+    of.launch(op, [t_qkv, t_k, t_v, torch.from_numpy(table).cuda(), torch.from_numpy(ctx).cuda()], [out], B,
+              max_ctas=max_ctas)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for b in range(B):
+        assert rel_err(got[b], want[b]) < 1e-2, (b, ctx[b], rel_err(got[b], want[b]))

@@ -16,8 +16,11 @@ extra = sys.argv[4:]
 tmp = ROOT / "paper_2605_21603_b200" / "_build" / "ab"
 tmp.mkdir(parents=True, exist_ok=True)
 src = tmp / Path(rel).name
-src.write_text(subprocess.run(["git", "-C", str(ROOT), "show", f"{rev}:paper_2605_21603_b200/csrc/{rel}"],
-                              capture_output=True, text=True, check=True).stdout)
+if rev.startswith("file:"):  # a patched copy of the source instead of a git revision
+    src.write_text(Path(rev[5:]).read_text())
+else:
+    src.write_text(subprocess.run(["git", "-C", str(ROOT), "show", f"{rev}:paper_2605_21603_b200/csrc/{rel}"],
+                                  capture_output=True, text=True, check=True).stdout)
 B.build()
 objs = []
 for o in sorted(B.OBJ.glob("*.o")):
