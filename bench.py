@@ -543,6 +543,9 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
             "roofline": {"bound": "hbm", "kernel": "decode_t_kernel<12,2> (paged attention; tokens on MMA M, GQA group on N; 12 warps x 2-page cp.async rings)",
                          "achieved": round(achieved, 1), "peak": PEAKS["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / PEAKS["hbm_gbs"], 4), "ms_per_launch": round(attn_ms, 4),
+                         "read_peak_gbs": 7443.2, "frac_of_read_peak": round(achieved / 7443.2, 4),
+                         "read_peak_source": "measured pure-read probe, profiles/r01_hbm_read_probe.txt "
+                                             "(peak above is the driver's read+write copy figure)",
                          "algorithmic_bytes_per_launch": kv_bytes}}
 
 
