@@ -293,7 +293,12 @@ def attn_prefill(qkv, heads, kv_heads, head_dim, seq_len):
     return out
 
 
-def attn_decode(qkv, kc, vc, table, ctx_len, heads, kv_heads, head_dim, page_size):
+def attn_decode(qkv, kc, vc, table, ctx_len, heads, kv_heads, head_dim, page_size, kv_layout=0):
+    """kv_layout 0: pages [page, kv_heads, head_dim] (NHD, the reference / vLLM
+    layout); 1: pages [kv_heads, page, head_dim] (HND), read as NHD."""
+    if kv_layout == 1:
+        kc = np.ascontiguousarray(np.swapaxes(kc, 1, 2))
+        vc = np.ascontiguousarray(np.swapaxes(vc, 1, 2))
     B = qkv.shape[0]
     out = np.zeros((B, heads * head_dim), dtype=np.float32)
     grp = heads // kv_heads
@@ -414,7 +419,7 @@ def evaluate(desc_json: str, rows: int, bindings: Dict[str, np.ndarray],
                 r = [moe_combine(x[0], x[1], x[2])]
             elif fn == "attn_decode":
                 r = [attn_decode(x[0], x[1], x[2], x[3], x[4], int(p["heads"]), int(p["kv_heads"]),
-                                 int(p["head_dim"]), int(p.get("page_size", 16)))]
+                                 int(p["head_dim"]), int(p.get("page_size", 16)), int(p.get("kv_layout", 0)))]
             else:
                 raise KeyError(f"no oracle for custom op '{fn}'")
         for n, v in zip(o["outputs"], r):

@@ -166,8 +166,10 @@ GraphDescription llama_graph(const LlamaShape& s) {
     const std::string wd = moe ? w.weight(p + ".experts.down.w", {El, MI, H}) : w.weight(p + ".down.w", {I, H});
     if (s.decode) {
       const int64_t pages = s.num_pages ? s.num_pages : T * max_pages;
-      kc = w.weight(p + ".k_cache", {pages, s.page_size, nkv, hd});
-      vc = w.weight(p + ".v_cache", {pages, s.page_size, nkv, hd});
+      const std::vector<int64_t> cshape = s.kv_layout == 1 ? std::vector<int64_t>{pages, nkv, s.page_size, hd}
+                                                           : std::vector<int64_t>{pages, s.page_size, nkv, hd};
+      kc = w.weight(p + ".k_cache", cshape);
+      vc = w.weight(p + ".v_cache", cshape);
     }
     const std::string qkv = w.act(p + ".qkv", {T, nqkv});
     const std::string qkvr = w.act(p + ".qkv_rot", {T, nqkv});
@@ -195,7 +197,8 @@ GraphDescription llama_graph(const LlamaShape& s) {
       w.custom(p + ".attn", "attn_decode", {qkvr, kc, vc, table, pos}, {ctx}, p + ".attn.core",
                ResourceClass::kMemory, mem_cost)
           .attrs.params = {{"heads", double(nq)}, {"kv_heads", double(nkv)},
-                           {"head_dim", double(hd)}, {"page_size", double(s.page_size)}};
+                           {"head_dim", double(hd)}, {"page_size", double(s.page_size)},
+                           {"kv_layout", double(s.kv_layout)}};
     } else {
       w.custom(p + ".attn", "attn_prefill", {qkvr}, {ctx}, p + ".attn.core",
                ResourceClass::kCompute, mem_cost)
@@ -397,6 +400,7 @@ std::string build_json(const std::string& name, const std::string& params_json) 
     s.ctx_len = geti(p, "ctx_len", s.ctx_len);
     s.page_size = geti(p, "page_size", s.page_size);
     s.num_pages = geti(p, "num_pages", s.num_pages);
+    s.kv_layout = geti(p, "kv_layout", s.kv_layout);
     s.experts = geti(p, "experts", s.experts);
     s.topk = geti(p, "topk", s.topk);
     s.moe_inter = geti(p, "moe_inter", s.moe_inter);

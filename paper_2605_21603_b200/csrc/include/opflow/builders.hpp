@@ -47,6 +47,7 @@ struct LlamaShape {
   int64_t ctx_len = 4096;    // cached context per sequence
   int64_t page_size = 16;
   int64_t num_pages = 0;     // 0 = tokens * ctx_len / page_size
+  int64_t kv_layout = 0;     // decode KV pages: 0 NHD [pages, page, kv, hd]; 1 HND [pages, kv, page, hd]
   // Qwen3 options: per-head q/k RMSNorm before RoPE; MoE FFN when experts > 0
   bool qk_norm = false;
   int64_t experts = 0;

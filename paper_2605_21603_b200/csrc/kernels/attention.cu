@@ -272,7 +272,7 @@ __global__ void decode_simt_kernel(const T* __restrict__ qkv, const T* __restric
 // attention_decode.cu (tensor-core paged decode); false when unsupported.
 bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                      const int64_t* table, const int64_t* ctx, __nv_bfloat16* out, int64_t B, int nq,
-                     int nkv, int hd, int page, int64_t max_pages, float scale, int max_ctas,
+                     int nkv, int hd, int page, int64_t max_pages, float scale, int max_ctas, int hnd,
                      cudaStream_t s);
 
 bool decode_bf16_tma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
@@ -351,15 +351,19 @@ opf_status op_attn_decode(const opf_op_ctx* c, const opf_view* in, int32_t n_in,
   const int hd = static_cast<int>(ctx_param(*c, "head_dim", 128));
   const int page = static_cast<int>(ctx_param(*c, "page_size", 16));
   if (nq % nkv || hd > 256) return op_error(Errc::ShapeMismatch, "attn_decode: heads");
-  if (in[1].rank != 4 || in[1].shape[1] != page || in[1].shape[2] != nkv || in[1].shape[3] != hd)
+  const int hnd = static_cast<int>(ctx_param(*c, "kv_layout", 0.0));  // 0 NHD, 1 HND
+  if (hnd == 0 && (in[1].rank != 4 || in[1].shape[1] != page || in[1].shape[2] != nkv || in[1].shape[3] != hd))
     return op_error(Errc::ShapeMismatch, "attn_decode: cache must be [pages, page, kv_heads, hd]");
+  if (hnd == 1 && (in[1].rank != 4 || in[1].shape[1] != nkv || in[1].shape[2] != page || in[1].shape[3] != hd))
+    return op_error(Errc::ShapeMismatch, "attn_decode: kv_layout 1 (HND) cache must be [pages, kv_heads, page, hd]");
+  if (hnd != 0 && hnd != 1) return op_error(Errc::ConfigError, "attn_decode: kv_layout is 0 (NHD) or 1 (HND)");
   if (rows == 0) return 0;
   const int64_t max_pages = view_row_elems(in[3]);
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
   auto s = static_cast<cudaStream_t>(stream);
   const int grp = nq / nkv;
   const int impl = static_cast<int>(ctx_param(*c, "impl", 0.0));  // 0 auto, 1 warp-SIMT, 2 generic
-  if (in[0].dtype == OPF_BF16 && impl == 0 && ctx_param(*c, "simt", 0.0) == 0.0 &&
+  if (in[0].dtype == OPF_BF16 && impl == 0 && hnd == 0 && ctx_param(*c, "simt", 0.0) == 0.0 &&
       decode_bf16_tma(vptr<__nv_bfloat16>(in[0]), vptr<__nv_bfloat16>(in[1]), vptr<__nv_bfloat16>(in[2]),
                       vptr<int64_t>(in[3]), vptr<int64_t>(in[4]), vptr<__nv_bfloat16>(out[0]), rows, nq,
                       nkv, hd, page, max_pages, in[1].shape[0], scale, c->max_ctas, s))
@@ -367,8 +371,9 @@ opf_status op_attn_decode(const opf_op_ctx* c, const opf_view* in, int32_t n_in,
   if (in[0].dtype == OPF_BF16 && impl == 0 && ctx_param(*c, "simt", 0.0) == 0.0 &&
       decode_bf16_mma(vptr<__nv_bfloat16>(in[0]), vptr<__nv_bfloat16>(in[1]), vptr<__nv_bfloat16>(in[2]),
                       vptr<int64_t>(in[3]), vptr<int64_t>(in[4]), vptr<__nv_bfloat16>(out[0]), rows, nq,
-                      nkv, hd, page, max_pages, scale, c->max_ctas, s))
+                      nkv, hd, page, max_pages, scale, c->max_ctas, hnd, s))
     return launch_status("attn_decode_mma");
+  if (hnd) return op_error(Errc::ShapeMismatch, "attn_decode: HND pages need the tensor-core path (bf16, hd 128, group <= 8)");
   if (in[0].dtype == OPF_BF16 && hd == 128 && grp <= kMaxGroup && impl != 2 &&
       ctx_param(*c, "simt", 0.0) == 0.0) {
     const unsigned grid = static_cast<unsigned>(rows * nkv);

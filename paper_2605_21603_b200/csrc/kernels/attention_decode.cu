@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(W * 32)
     decode_t_kernel(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ kc,
                     const __nv_bfloat16* __restrict__ vc, const int64_t* __restrict__ table,
                     const int64_t* __restrict__ ctx_len, __nv_bfloat16* __restrict__ out, int nq, int nkv,
-                    int64_t max_pages, float scale_log2, int64_t n_items) {
+                    int64_t max_pages, float scale_log2, int64_t n_items, int hnd) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int kRing = D * 2 * kPageBytes;
   pdl_wait();
@@ -267,14 +267,18 @@ __global__ void __launch_bounds__(W * 32)
     const __nv_bfloat16* row = qkv + b * Wd;
     const int64_t ctx = ctx_len[b];
     const int n_pages = static_cast<int>((ctx + PAGE - 1) / PAGE);
-    const int64_t tok_stride = static_cast<int64_t>(nkv) * HD;
+    // NHD pages [16 tokens][nkv][128] (reference / vLLM layout) or HND pages
+    // [nkv][16 tokens][128]: one (page, kv head) block is 4 KB contiguous, which
+    // DRAM streams ~2-5% faster than 16 rows of 256 B at 2 KB stride
+    const int64_t tok_stride = hnd ? HD : static_cast<int64_t>(nkv) * HD;
+    const int64_t head_off = hnd ? static_cast<int64_t>(kh) * PAGE * HD : static_cast<int64_t>(kh) * HD;
     uint8_t* ring = smem + warp * kRing;
     auto k_slot = [&](int s) { return ring + s * 2 * kPageBytes; };
     auto v_slot = [&](int s) { return ring + s * 2 * kPageBytes + kPageBytes; };
     auto issue = [&](int page_idx, int s) {
       const int64_t pg = table[b * max_pages + page_idx];
-      const __nv_bfloat16* kp = kc + (pg * PAGE * nkv + kh) * HD;
-      const __nv_bfloat16* vp = vc + (pg * PAGE * nkv + kh) * HD;
+      const __nv_bfloat16* kp = kc + pg * PAGE * nkv * HD + head_off;
+      const __nv_bfloat16* vp = vc + pg * PAGE * nkv * HD + head_off;
       const uint32_t kd = saddr(k_slot(s)), vd = saddr(v_slot(s));
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -682,20 +686,21 @@ bool cache_map(CUtensorMap* m, const void* base, int nkv, int64_t pages) {
 template <int W, int D>
 bool launch_decode_t(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                      const int64_t* table, const int64_t* ctx, __nv_bfloat16* out, int nq, int nkv,
-                     int64_t max_pages, float scale_log2, int64_t items, int64_t grid, cudaStream_t s) {
+                     int64_t max_pages, float scale_log2, int64_t items, int64_t grid, int hnd,
+                     cudaStream_t s) {
   constexpr int kSmem = W * D * 2 * kPageBytes;
   static_assert(kSmem >= (W * 8 * (HD + 2) + 8) * 4, "merge buffers fit in the rings");
   static bool attr = cudaFuncSetAttribute(decode_t_kernel<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           kSmem) == cudaSuccess;
   if (!attr) return false;
   launch_pdl(decode_t_kernel<W, D>, dim3(static_cast<unsigned>(grid)), dim3(W * 32), kSmem, s, qkv, kc, vc, table,
-             ctx, out, nq, nkv, max_pages, scale_log2, items);
+             ctx, out, nq, nkv, max_pages, scale_log2, items, hnd);
   return true;
 }
 
 bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                      const int64_t* table, const int64_t* ctx, __nv_bfloat16* out, int64_t B, int nq,
-                     int nkv, int hd, int page, int64_t max_pages, float scale, int max_ctas,
+                     int nkv, int hd, int page, int64_t max_pages, float scale, int max_ctas, int hnd,
                      cudaStream_t s) {
   if (hd != HD || page != PAGE || nq % nkv != 0 || nq / nkv > 8) return false;
   // OPF_DECODE: t12x2 (default) | t8x3 | mma16 (group padded to M = 16)
@@ -712,16 +717,16 @@ bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __
   int64_t grid = max_ctas > 0 ? std::min<int64_t>(max_ctas, num_sms()) : num_sms();
   grid = std::max<int64_t>(1, std::min(grid, items));
   const float sl2 = scale * 1.4426950408889634f;
-  if (variant == 1) return launch_decode_t<8, 3>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, s);
-  if (variant == 2) return launch_decode_t<12, 2>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, s);
-  if (variant == 3) return launch_decode_t<14, 2>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, s);
-  if (variant == 4) return launch_decode_t<16, 1>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, s);
-  if (variant == 5) return launch_decode_t<6, 4>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, s);
+  if (variant == 1) return launch_decode_t<8, 3>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
+  if (variant == 2) return launch_decode_t<12, 2>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
+  if (variant == 3) return launch_decode_t<14, 2>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
+  if (variant == 4) return launch_decode_t<16, 1>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
+  if (variant == 5) return launch_decode_t<6, 4>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
   static bool attr = [] {
     return cudaFuncSetAttribute(decode_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemRing) == cudaSuccess;
   }();
-  if (!attr) return false;
+  if (!attr || hnd) return false;  // the M = 16 kernel reads NHD pages only
   launch_pdl(decode_mma_kernel, dim3(static_cast<unsigned>(grid)), dim3(kWarps * 32), kSmemRing, s,
              qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items);
   return true;

@@ -123,3 +123,37 @@ def test_decode_tma_ring_wraps_across_items(cuda, max_ctas):
     got = out.float().cpu().numpy()
     for b in range(B):
         assert rel_err(got[b], want[b]) < 1e-2, (b, ctx[b], rel_err(got[b], want[b]))
+
+
+@pytest.mark.parametrize("nq,nkv", [(32, 8), (8, 2), (16, 16)])
+def test_decode_hnd_layout_matches_nhd(cuda, nq, nkv):
+    """kv_layout 1 (HND pages [kv_heads, page, hd]) gives the same attention as
+    the reference NHD layout on the same cache contents (transposed), and both
+    match the oracle."""
+    import torch
+    rng = np.random.default_rng(nq + nkv)
+    B, hd, page, max_pages = 11, 128, 16, 20
+    ctx = rng.integers(0, max_pages * page, size=B).astype(np.int64)
+    ctx[:2] = [0, max_pages * page]
+    pages = B * max_pages
+    kc = rng.uniform(-1, 1, (pages, page, nkv, hd)).astype(np.float32)
+    vc = rng.uniform(-1, 1, (pages, page, nkv, hd)).astype(np.float32)
+    table = rng.permutation(pages).reshape(B, max_pages).astype(np.int64)
+    qkv = rng.uniform(-1, 1, (B, (nq + 2 * nkv) * hd)).astype(np.float32)
+    tb = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().to(torch.bfloat16)
+    t_qkv, t_k, t_v = tb(qkv), tb(kc), tb(vc)
+    t_kh, t_vh = t_k.transpose(1, 2).contiguous(), t_v.transpose(1, 2).contiguous()
+    want = oracle.attn_decode(t_qkv.float().cpu().numpy(), t_kh.float().cpu().numpy(), t_vh.float().cpu().numpy(),
+                              table, ctx, nq, nkv, hd, page, kv_layout=1)
+    outs = []
+    for lay, (k, v) in [(0, (t_k, t_v)), (1, (t_kh, t_vh))]:
+        out = torch.empty(B, nq * hd, dtype=torch.bfloat16, device="cuda")
+        op = {"name": "d", "kind": "Custom", "inputs": [], "outputs": [],
+              "attrs": {"custom_name": "attn_decode",
+                        "params": {"heads": nq, "kv_heads": nkv, "head_dim": hd, "page_size": page, "kv_layout": lay}}}
+        of.launch(op, [t_qkv, k, v, torch.from_numpy(table).cuda(), torch.from_numpy(ctx).cuda()], [out], B)
+        torch.cuda.synchronize()
+        outs.append(out.float().cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])  # same math, same order: bit-identical
+    for b in range(B):
+        assert rel_err(outs[1][b], want[b]) < 1e-2

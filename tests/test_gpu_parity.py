@@ -198,9 +198,10 @@ def test_llama_bf16_layers(cuda, tp):
             assert rel_err(got[k], want[k]) < 2e-2, (strat, k, rel_err(got[k], want[k]))
 
 
-def test_llama_decode_bf16(cuda):
+@pytest.mark.parametrize("kv_layout", [0, 1])
+def test_llama_decode_bf16(cuda, kv_layout):
     desc = of.llama_decode_graph(layers=1, tokens=16, hidden=512, heads=8, kv_heads=2, head_dim=128,
-                                 inter=1024, ctx_len=300, page_size=16, dtype="bf16")
+                                 inter=1024, ctx_len=300, page_size=16, dtype="bf16", kv_layout=kv_layout)
     host = llama_inputs(desc, 16, seed=4, ctx_len=257)
     want = oracle.evaluate(desc, 16, host, exact=False)
     for strat in [{"name": "sequential"}, {"name": "split_overlap", "lane_mode": "ubatch"}]:
