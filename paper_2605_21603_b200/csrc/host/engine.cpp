@@ -487,6 +487,45 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
       view_of[t] = arena_view(blk, t, base_row, nrows);
     }
 
+    // workspace + SM budget of one planned launch; the workspace block is live
+    // only for this launch (later launches of this dispatch may reuse it)
+    auto plan_ws = [&](PlannedLaunch& l) {
+      if (l.is_copy) return;
+      if (cfg_.gemm_sm_budget > 0 && d.lane == 0) l.max_ctas = cfg_.gemm_sm_budget;
+      if (d.lane < static_cast<int>(budgets.size()) && budgets[d.lane] > 0) l.max_ctas = budgets[d.lane];
+      opf_op_ctx c{};
+      c.kind = static_cast<int32_t>(l.kind);
+      c.world_size = l.attrs.world_size;
+      c.comm = comm_;
+      c.max_ctas = l.max_ctas;
+      std::vector<opf_view> iv, ov;
+      for (const auto& v : l.in) iv.push_back(make_view(nullptr, v.elem_offset, v.dtype, v.shape, v.batched));
+      for (const auto& v : l.out) ov.push_back(make_view(nullptr, v.elem_offset, v.dtype, v.shape, v.batched));
+      std::vector<const char*> pn;
+      std::vector<double> pv;
+      for (const auto& kv : l.attrs.params) {
+        pn.push_back(kv.first.c_str());
+        pv.push_back(kv.second);
+      }
+      c.n_params = static_cast<int32_t>(pn.size());
+      c.param_names = pn.data();
+      c.param_values = pv.data();
+      size_t ws = 0;
+      if (l.fn.empty()) {
+        ws = kind_workspace(c, iv.data(), static_cast<int>(iv.size()), ov.data(),
+                            static_cast<int>(ov.size()), l.rows);
+      } else if (const OpEntry* e = OpRegistry::global().find(l.fn); e && e->workspace) {
+        ws = e->workspace(c, iv.data(), static_cast<int>(iv.size()), ov.data(),
+                          static_cast<int>(ov.size()), l.rows);
+      }
+      if (ws > 0) {
+        const int32_t blk = pl.alloc(static_cast<int64_t>(ws), di);
+        l.ws_off = pl.blocks[blk].off;
+        l.ws_bytes = static_cast<int64_t>(ws);
+        pl.release(blk);
+      }
+    };
+
     // ---- launches
     auto weight_view = [&](int32_t t, const OperatorNode&) { return ext_view(t, 0, 0); };
     const bool fused = d.kind == Dispatch::Kind::kFused;
@@ -515,6 +554,7 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
                   std::to_string(e->n_out) + " tensors, fused subgraphs expose " +
                   std::to_string(l.in.size()) + "->" + std::to_string(l.out.size()));
       pd.launches.push_back(std::move(l));
+      plan_ws(pd.launches.back());
     } else {
       // Epilogue fusion (per-subgraph compilation): a bf16
       // MatMul whose output feeds only a silu_mul (or a rope) of the same
@@ -546,8 +586,23 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
           skip.insert(cons[0]);
         }
       }
-      // internal tensors of the subgraph get scratch blocks for this dispatch
-      for (int32_t op : ops) {
+      // internal tensors of the subgraph get arena blocks from their producer to
+      // their last consumer within this dispatch (launches of a dispatch run in
+      // order on its lane, so a block freed after op k is reusable from op k+1)
+      std::map<int32_t, int32_t> last_pos, int_blk;
+      for (int32_t k = 0; k < static_cast<int32_t>(ops.size()); ++k)
+        for (int32_t t : g_.ops[ops[k]].inputs) last_pos[t] = k;
+      auto retire_inputs = [&](int32_t k, const std::vector<int32_t>& ins) {
+        for (int32_t t : ins) {
+          auto ib = int_blk.find(t);
+          if (ib != int_blk.end() && last_pos[t] <= k) {
+            pl.release(ib->second);
+            int_blk.erase(ib);
+          }
+        }
+      };
+      for (int32_t k = 0; k < static_cast<int32_t>(ops.size()); ++k) {
+        const int32_t op = ops[k];
         if (skip.count(op)) continue;
         const OperatorNode& node = g_.ops[op];
         auto fa = fused_act.find(op);
@@ -557,6 +612,7 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
           if (!view_of.count(a_out)) {
             const int32_t blk = pl.alloc(tensor_bytes_rows(g_.tensors[a_out], nrows), di);
             scratch.push_back(blk);
+            int_blk[a_out] = blk;
             view_of[a_out] = arena_view(blk, a_out, 0, nrows);
           }
           const bool rope = act.attrs.custom_name == "rope";
@@ -576,12 +632,17 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
           l.prepacked = node.inputs[1];
           l.prepack_mode = rope ? 0 : 1;
           pd.launches.push_back(std::move(l));
+          plan_ws(pd.launches.back());
+          // only inputs whose last consumer is this MatMul retire here (an input
+          // also read by the skipped act or a later op stays to the dispatch end)
+          retire_inputs(k, node.inputs);
           continue;
         }
         for (int32_t t : node.outputs)
           if (!view_of.count(t)) {
             const int32_t blk = pl.alloc(tensor_bytes_rows(g_.tensors[t], nrows), di);
             scratch.push_back(blk);
+            int_blk[t] = blk;
             view_of[t] = arena_view(blk, t, 0, nrows);
           }
         PlannedLaunch l;
@@ -609,46 +670,10 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
           }
         }
         pd.launches.push_back(std::move(l));
+        plan_ws(pd.launches.back());
+        retire_inputs(k, node.inputs);
       }
     }
-    // workspace + SM budget
-    for (PlannedLaunch& l : pd.launches) {
-      if (l.is_copy) continue;
-      if (cfg_.gemm_sm_budget > 0 && d.lane == 0) l.max_ctas = cfg_.gemm_sm_budget;
-      if (d.lane < static_cast<int>(budgets.size()) && budgets[d.lane] > 0) l.max_ctas = budgets[d.lane];
-      opf_op_ctx c{};
-      c.kind = static_cast<int32_t>(l.kind);
-      c.world_size = l.attrs.world_size;
-      c.comm = comm_;
-      c.max_ctas = l.max_ctas;
-      std::vector<opf_view> iv, ov;
-      for (const auto& v : l.in) iv.push_back(make_view(nullptr, v.elem_offset, v.dtype, v.shape, v.batched));
-      for (const auto& v : l.out) ov.push_back(make_view(nullptr, v.elem_offset, v.dtype, v.shape, v.batched));
-      std::vector<const char*> pn;
-      std::vector<double> pv;
-      for (const auto& kv : l.attrs.params) {
-        pn.push_back(kv.first.c_str());
-        pv.push_back(kv.second);
-      }
-      c.n_params = static_cast<int32_t>(pn.size());
-      c.param_names = pn.data();
-      c.param_values = pv.data();
-      size_t ws = 0;
-      if (l.fn.empty()) {
-        ws = kind_workspace(c, iv.data(), static_cast<int>(iv.size()), ov.data(),
-                            static_cast<int>(ov.size()), l.rows);
-      } else if (const OpEntry* e = OpRegistry::global().find(l.fn); e && e->workspace) {
-        ws = e->workspace(c, iv.data(), static_cast<int>(iv.size()), ov.data(),
-                          static_cast<int>(ov.size()), l.rows);
-      }
-      if (ws > 0) {
-        const int32_t blk = pl.alloc(static_cast<int64_t>(ws), di);
-        scratch.push_back(blk);
-        l.ws_off = pl.blocks[blk].off;
-        l.ws_bytes = static_cast<int64_t>(ws);
-      }
-    }
-
     // ---- on_inputs: decrement ref counts, reclaim dead slices after the dispatch
     for (const auto& [t, s] : consumed) {
       (void)s;
@@ -1023,45 +1048,73 @@ std::string Session::schedule_json() const {
 
 std::string Session::trace_json() {
   require(last_ != nullptr, Errc::Unmaterialized, "no run yet");
-  // Profiled eager replay: timing events around every dispatch on its lane.
+  // Profiled eager replay: timing events around every dispatch on its lane
+  // (OPF_TRACE_LAUNCHES=1: around every kernel launch instead — the in-situ
+  // per-kernel breakdown of a step, unlike ncu's serialised cold-cache list).
+  const char* per_env = std::getenv("OPF_TRACE_LAUNCHES");
+  const bool per_launch = per_env && std::string(per_env) == "1";
   CompiledPlan& cp = *last_;
-  const std::size_t n = cp.dispatches.size();
-  std::vector<cudaEvent_t> b(n), e(n);
-  for (std::size_t i = 0; i < n; ++i) {
-    OPF_CUDA(cudaEventCreate(&b[i]));
-    OPF_CUDA(cudaEventCreate(&e[i]));
-  }
+  struct Ev {
+    cudaEvent_t b, e;
+    std::string name;
+    int lane;
+  };
+  std::vector<Ev> evs;
+  std::vector<cudaEvent_t> disp_end(cp.dispatches.size());
   cudaEvent_t t0;
   OPF_CUDA(cudaEventCreate(&t0));
   OPF_CUDA(cudaDeviceSynchronize());
   OPF_CUDA(cudaEventRecord(t0, lanes_[0]));
   for (auto& l : lanes_) OPF_CUDA(cudaStreamWaitEvent(l, t0, 0));
-  for (std::size_t i = 0; i < n; ++i) {
+  auto mk = [&](const std::string& name, int lane) {
+    Ev e{};
+    OPF_CUDA(cudaEventCreate(&e.b));
+    OPF_CUDA(cudaEventCreate(&e.e));
+    e.name = name;
+    e.lane = lane;
+    evs.push_back(e);
+    return evs.size() - 1;
+  };
+  for (std::size_t i = 0; i < cp.dispatches.size(); ++i) {
     const PlannedDispatch& pd = cp.dispatches[i];
     cudaStream_t s = lanes_[pd.d.lane];
-    for (int32_t w : pd.wait_on) OPF_CUDA(cudaStreamWaitEvent(s, e[w], 0));
-    OPF_CUDA(cudaEventRecord(b[i], s));
-    for (const PlannedLaunch& l : pd.launches) launch_one(l, s);
-    OPF_CUDA(cudaEventRecord(e[i], s));
+    for (int32_t w : pd.wait_on) OPF_CUDA(cudaStreamWaitEvent(s, disp_end[w], 0));
+    std::string dname;
+    for (int32_t sg : pd.d.subgraphs) dname += (dname.empty() ? "" : "+") + p_.subgraphs[sg].label;
+    dname += " u" + std::to_string(pd.d.u0) + (pd.d.u1 - pd.d.u0 > 1 ? "-" + std::to_string(pd.d.u1 - 1) : "");
+    std::size_t di = 0;
+    if (!per_launch) {
+      di = mk(dname, pd.d.lane);
+      OPF_CUDA(cudaEventRecord(evs[di].b, s));
+    }
+    for (const PlannedLaunch& l : pd.launches) {
+      std::size_t li = 0;
+      if (per_launch) {
+        li = mk(l.name + " u" + std::to_string(pd.d.u0), pd.d.lane);
+        OPF_CUDA(cudaEventRecord(evs[li].b, s));
+      }
+      launch_one(l, s);
+      if (per_launch) OPF_CUDA(cudaEventRecord(evs[li].e, s));
+    }
+    OPF_CUDA(cudaEventCreate(&disp_end[i]));
+    OPF_CUDA(cudaEventRecord(disp_end[i], s));
+    if (!per_launch) OPF_CUDA(cudaEventRecord(evs[di].e, s));
   }
   OPF_CUDA(cudaDeviceSynchronize());
   std::string out = "[";
-  for (std::size_t i = 0; i < n; ++i) {
+  for (std::size_t i = 0; i < evs.size(); ++i) {
     float ts = 0, te = 0;
-    OPF_CUDA(cudaEventElapsedTime(&ts, t0, b[i]));
-    OPF_CUDA(cudaEventElapsedTime(&te, t0, e[i]));
-    const PlannedDispatch& pd = cp.dispatches[i];
-    std::string name;
-    for (int32_t sg : pd.d.subgraphs) name += (name.empty() ? "" : "+") + p_.subgraphs[sg].label;
-    name += " u" + std::to_string(pd.d.u0) + (pd.d.u1 - pd.d.u0 > 1 ? "-" + std::to_string(pd.d.u1 - 1) : "");
+    OPF_CUDA(cudaEventElapsedTime(&ts, t0, evs[i].b));
+    OPF_CUDA(cudaEventElapsedTime(&te, t0, evs[i].e));
     char buf[128];
     std::snprintf(buf, sizeof buf, ",\"ts\":%.3f,\"dur\":%.3f,\"pid\":0,\"tid\":%d}", ts * 1e3,
-                  (te - ts) * 1e3, pd.d.lane);
-    out += std::string(i ? "," : "") + "{\"name\":" + json::quote(name) +
-           ",\"cat\":\"dispatch\",\"ph\":\"X\"" + buf;
-    cudaEventDestroy(b[i]);
-    cudaEventDestroy(e[i]);
+                  (te - ts) * 1e3, evs[i].lane);
+    out += std::string(i ? "," : "") + "{\"name\":" + json::quote(evs[i].name) +
+           ",\"cat\":\"" + (per_launch ? "launch" : "dispatch") + "\",\"ph\":\"X\"" + buf;
+    cudaEventDestroy(evs[i].b);
+    cudaEventDestroy(evs[i].e);
   }
+  for (auto& e : disp_end) cudaEventDestroy(e);
   cudaEventDestroy(t0);
   return out + "]";
 }

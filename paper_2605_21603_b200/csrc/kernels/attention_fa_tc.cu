@@ -27,7 +27,9 @@
 #include <cuda_bf16.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "opflow/device.hpp"
 
@@ -546,6 +548,330 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ------------------------------------------------------------------ ping-pong variant
+// Two heads of one GQA group per item (same q tile, same K_j / V_j tiles: one
+// K/V load feeds two S and two PV MMAs).  TMEM: S0/P0 0..127, S1/P1 128..255,
+// O0 256..383, O1 384..511.  Softmax warpgroup t (warps 4+4t..7+4t) owns head
+// t: one thread = one query row x all 128 keys (two 64-column passes over
+// TMEM, so no cross-warp exchange), P (bf16) written over the consumed S
+// columns.  The MMA warp interleaves the two heads — S0_{j+1} / S1_{j+1} are
+// issued right behind PV0_j / PV1_j — so one head's softmax overlaps the
+// other head's tensor work (FA4's ping-pong).  A commit after S_t,j also
+// covers PV_t,{j-1} (in-order tcgen05 completion), so the softmax may rescale
+// O_t without a separate PV tracker.
+constexpr int kPPThreads = 384;                  // 4 role warps + 2 softmax warpgroups
+constexpr uint32_t kPPQ = 0;                     // Q0, Q1
+constexpr uint32_t kPPK = 2 * kTile;             // [2 stages]
+constexpr uint32_t kPPV = kPPK + 2 * kTile;      // [2 stages]
+constexpr uint32_t kPPBar = kPPV + 2 * kTile;
+constexpr uint32_t kPPSmem = kPPBar + 256 + 1024;
+
+__global__ void __launch_bounds__(kPPThreads, 1)
+    fa_pp_kernel(const __grid_constant__ CUtensorMap mqkv, __nv_bfloat16* __restrict__ out, int nq, int nkv,
+                 int S, int n_seqs, float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kPPBar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;    // [2]
+  uint64_t* k_empty = bars + 4;   // [2]
+  uint64_t* v_full = bars + 6;    // [2]
+  uint64_t* v_empty = bars + 8;   // [2]
+  uint64_t* s_full = bars + 10;   // [2 heads]
+  uint64_t* p_full = bars + 12;   // [2 heads]
+  uint64_t* o_full = bars + 14;   // [2 heads]
+  uint64_t* o_free = bars + 16;   // [2 heads]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  static_assert(19 * 8 <= 256, "barrier area");
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int q_tiles = S / BQ;
+  const int grp = nq / nkv;
+  const int pairs = nq / 2;
+  const int64_t per_q = static_cast<int64_t>(pairs) * n_seqs;
+  const int64_t n_items = per_q * q_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mqkv)) : "memory");
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  } else if (warp == 1 && lane == 0) {
+    bar_init(q_full, 1);
+    bar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&k_full[i], 1);
+      bar_init(&k_empty[i], 1);
+      bar_init(&v_full[i], 1);
+      bar_init(&v_empty[i], 1);
+      bar_init(&s_full[i], 1);
+      bar_init(&p_full[i], 4);
+      bar_init(&o_full[i], 1);
+      bar_init(&o_free[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+
+  auto decode_item = [&](int64_t i, int& qt, int& hp, int& seq) {
+    qt = q_tiles - 1 - static_cast<int>(i / per_q);  // longest first
+    const int64_t r = i % per_q;
+    hp = static_cast<int>(r % pairs);
+    seq = static_cast<int>(r / pairs);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------------- TMA: Q pair, K tiles
+      int stage = 0;
+      uint32_t ph = 0, qph = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        int qt, hp, seq;
+        decode_item(it, qt, hp, seq);
+        const int h0 = 2 * hp, kh = h0 / grp;
+        const int row0 = seq * S;
+        bar_wait(q_empty, qph ^ 1);
+        qph ^= 1;
+        bar_expect(q_full, 2 * kTile);
+        for (int t = 0; t < 2; ++t) {
+          tma2d(su32(sm + kPPQ + t * kTile), &mqkv, q_full, (h0 + t) * HD, row0 + qt * BQ);
+          tma2d(su32(sm + kPPQ + t * kTile + kHalf), &mqkv, q_full, (h0 + t) * HD + 64, row0 + qt * BQ);
+        }
+        for (int j = 0; j <= qt; ++j) {
+          bar_wait(&k_empty[stage], ph ^ 1);
+          const uint32_t kd = su32(sm + kPPK + stage * kTile);
+          bar_expect(&k_full[stage], kTile);
+          tma2d(kd, &mqkv, &k_full[stage], (nq + kh) * HD, row0 + j * BKV);
+          tma2d(kd + kHalf, &mqkv, &k_full[stage], (nq + kh) * HD + 64, row0 + j * BKV);
+          if (++stage == 2) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {  // ---------------------------------------------- TMA: V tiles
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        int qt, hp, seq;
+        decode_item(it, qt, hp, seq);
+        const int kh = 2 * hp / grp;
+        const int row0 = seq * S;
+        for (int j = 0; j <= qt; ++j) {
+          bar_wait(&v_empty[stage], ph ^ 1);
+          const uint32_t vd = su32(sm + kPPV + stage * kTile);
+          bar_expect(&v_full[stage], kTile);
+          tma2d(vd, &mqkv, &v_full[stage], (nq + nkv + kh) * HD, row0 + j * BKV);
+          tma2d(vd + kHalf, &mqkv, &v_full[stage], (nq + nkv + kh) * HD + 64, row0 + j * BKV);
+          if (++stage == 2) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------------------------------------- MMA issuer
+      int kst = 0, vst = 0;
+      uint32_t kph = 0, vph = 0, qph = 0;
+      uint32_t pph[2] = {0, 0}, ofph[2] = {0, 0};
+      bool first_item = true;
+      const uint32_t S_id = idesc(false), PV_id = idesc(true);
+      auto issue_s = [&](int t) {  // S_t = Q_t K^T into TMEM cols t*128 (K tile in stage kst)
+        const uint32_t qa = su32(sm + kPPQ + t * kTile);
+        const uint32_t kb = su32(sm + kPPK + kst * kTile);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint64_t ad = sdesc(qa + (k >> 2) * kHalf + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = sdesc(kb + (k >> 2) * kHalf + (k & 3) * 32, 16, 1024);
+          mma_ss(tmem + t * 128, ad, bd, S_id, k != 0);
+        }
+        commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t V (P in TMEM over S_t's first 64 cols)
+        bar_wait(&p_full[t], pph[t]);
+        pph[t] ^= 1;
+        if (j == 0 && !first_item) {  // the epilogue must have read O_t of the previous item
+          bar_wait(&o_free[t], ofph[t]);
+          ofph[t] ^= 1;
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t vb = su32(sm + kPPV + vst * kTile);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint64_t bd = sdesc(vb + k * 2048, kHalf, 1024);
+          mma_ts(tmem + kColO + t * 128, tmem + t * 128 + k * 8, bd, PV_id, (j | k) != 0);
+        }
+      };
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        int qt, hp, seq;
+        decode_item(it, qt, hp, seq);
+        const int n = qt + 1;
+        bar_wait(q_full, qph);
+        qph ^= 1;
+        bar_wait(&k_full[kst], kph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        issue_s(0);
+        issue_s(1);
+        commit(&k_empty[kst]);
+        if (++kst == 2) {
+          kst = 0;
+          kph ^= 1;
+        }
+        if (n == 1) commit(q_empty);
+        for (int j = 0; j < n; ++j) {
+          bar_wait(&v_full[vst], vph);
+          const bool more = j + 1 < n;
+          if (more) {
+            bar_wait(&k_full[kst], kph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          }
+          issue_pv(0, j);
+          if (!more) commit(&o_full[0]);
+          if (more) issue_s(0);
+          issue_pv(1, j);
+          commit(&v_empty[vst]);
+          if (++vst == 2) {
+            vst = 0;
+            vph ^= 1;
+          }
+          if (!more) commit(&o_full[1]);
+          if (more) {
+            issue_s(1);
+            commit(&k_empty[kst]);
+            if (++kst == 2) {
+              kst = 0;
+              kph ^= 1;
+            }
+            if (j + 2 == n) commit(q_empty);
+          }
+        }
+        first_item = false;
+      }
+    }
+  } else if (warp >= 4) {  // ------------------------------------------ softmax warpgroups
+    const int t = (warp - 4) >> 2;  // head of the pair
+    const int q = warp & 3;         // TMEM lane quarter
+    const int r = q * 32 + lane;    // query row within the tile
+    const uint32_t srow = tmem + (static_cast<uint32_t>(q * 32) << 16) + t * 128;
+    const uint32_t orow = tmem + (static_cast<uint32_t>(q * 32) << 16) + kColO + t * 128;
+    uint32_t sph = 0, oph = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+      int qt, hp, seq;
+      decode_item(it, qt, hp, seq);
+      const int n = qt + 1;
+      float m_used = -FLT_MAX, l = 0.0f;
+      for (int j = 0; j < n; ++j) {
+        bar_wait(&s_full[t], sph);
+        sph ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const bool diag = j == qt;
+        // pass 1: row max over the 128 keys
+        float pm = -INFINITY;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float s[64];
+          tld32(srow + h * 64, *reinterpret_cast<float(*)[32]>(&s[0]));
+          tld32(srow + h * 64 + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float mx8[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            const float v = (diag && h * 64 + c > r) ? -INFINITY : s[c];
+            mx8[c & 7] = fmaxf(mx8[c & 7], v);
+          }
+          pm = fmaxf(pm, fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))));
+        }
+        const float mx = scale_log2 * pm;
+        float factor = 1.0f;
+        const bool rescale = mx > m_used + kRescaleThresh;
+        if (rescale) {
+          factor = ex2(m_used - mx);  // 0 on the first tile
+          m_used = mx;
+        }
+        l *= factor;
+        // O_t is stable here (this S's commit covered PV_t,{j-1})
+        if (j > 0 && __any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float o[32];
+            tld32(orow + c * 32, o);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] *= factor;
+            tst32(orow + c * 32, o);
+          }
+        }
+        // pass 2: P = 2^(s * scale - m) (bf16) over the consumed S columns
+        float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float s[64];
+          tld32(srow + h * 64, *reinterpret_cast<float(*)[32]>(&s[0]));
+          tld32(srow + h * 64 + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          uint32_t pk[32];
+#pragma unroll
+          for (int c2 = 0; c2 < 32; ++c2) {
+            const int c0 = h * 64 + 2 * c2;
+            const float x0 = (diag && c0 > r) ? -INFINITY : fmaf(s[2 * c2], scale_log2, -m_used);
+            const float x1 = (diag && c0 + 1 > r) ? -INFINITY : fmaf(s[2 * c2 + 1], scale_log2, -m_used);
+            const float p0 = c2 < kPolyPairs ? ex2_poly(x0) : ex2(x0);
+            const float p1 = c2 < kPolyPairs ? ex2_poly(x1) : ex2(x1);
+            sum8[(2 * c2) & 7] += p0;
+            sum8[(2 * c2 + 1) & 7] += p1;
+            pk[c2] = bf2(p0, p1);
+          }
+          tst32u(srow + h * 32, pk);
+        }
+        l += ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) bar_arrive(&p_full[t]);
+      }
+      // ---- epilogue: O_t / l -> bf16 -> global
+      bar_wait(&o_full[t], oph);
+      oph ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const float inv = l > 0.0f ? 1.0f / l : 0.0f;
+      __nv_bfloat16* op = out + (static_cast<int64_t>(seq) * S + qt * BQ + r) * (static_cast<int64_t>(nq) * HD) +
+                          static_cast<int64_t>(2 * hp + t) * HD;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float o[32];
+        tld32(orow + c * 32, o);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 u;
+          u.x = bf2(o[v * 8 + 0] * inv, o[v * 8 + 1] * inv);
+          u.y = bf2(o[v * 8 + 2] * inv, o[v * 8 + 3] * inv);
+          u.z = bf2(o[v * 8 + 4] * inv, o[v * 8 + 5] * inv);
+          u.w = bf2(o[v * 8 + 6] * inv, o[v * 8 + 7] * inv);
+          *reinterpret_cast<uint4*>(op + c * 32 + v * 8) = u;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) bar_arrive(&o_free[t]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                               CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -566,8 +892,16 @@ bool prefill_bf16_tcgen05(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t 
     return reinterpret_cast<EncodeFn>(p);
   }();
   static bool attr = cudaFuncSetAttribute(fa_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(kSmemTotal)) == cudaSuccess;
+                                          static_cast<int>(kSmemTotal)) == cudaSuccess &&
+                     cudaFuncSetAttribute(fa_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kPPSmem)) == cudaSuccess;
   if (!enc || !attr) return false;
+  // OPF_FA=pp: two heads of one GQA group per item (ping-pong; even groups only)
+  static const bool one_tile = [] {
+    const char* e = std::getenv("OPF_FA");
+    return !(e && std::string(e) == "pp");  // ping-pong measured slower (softmax issue-bound), opt-in
+  }();
+  const bool pp = !one_tile && (nq / nkv) % 2 == 0;
   const int64_t W = static_cast<int64_t>(nq + 2 * nkv) * HD;
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(rows)};
@@ -579,11 +913,15 @@ bool prefill_bf16_tcgen05(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t 
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
   const int n_seqs = static_cast<int>(rows / S);
-  const int64_t items = static_cast<int64_t>(S / BQ) * nq * n_seqs;
+  const int64_t items = static_cast<int64_t>(S / BQ) * (pp ? nq / 2 : nq) * n_seqs;
   int grid = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
   grid = static_cast<int>(std::min<int64_t>(grid, items));
-  launch_pdl(fa_tc_kernel, dim3(grid), dim3(kThreads), kSmemTotal, s, m, out, nq, nkv, S, n_seqs,
-             scale * 1.4426950408889634f);
+  if (pp)
+    launch_pdl(fa_pp_kernel, dim3(grid), dim3(kPPThreads), kPPSmem, s, m, out, nq, nkv, S, n_seqs,
+               scale * 1.4426950408889634f);
+  else
+    launch_pdl(fa_tc_kernel, dim3(grid), dim3(kThreads), kSmemTotal, s, m, out, nq, nkv, S, n_seqs,
+               scale * 1.4426950408889634f);
   return true;
 }
 

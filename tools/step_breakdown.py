@@ -1,0 +1,39 @@
+"""In-situ per-kernel breakdown of one step (eager replay of the compiled plan
+with CUDA events around every launch, OPF_TRACE_LAUNCHES=1): prefill
+(Llama-3-8B-shaped layers, 8 x 1024 tokens) or decode (512 x 4K, HND pages).
+Usage: python tools/step_breakdown.py [prefill|decode] [layers]"""
+import collections
+import json
+import os
+import sys
+
+os.environ["OPF_TRACE_LAUNCHES"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2605_21603_b200 import opflow as of  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "prefill"
+L = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+dev = torch.device("cuda:0")
+T, S = 8192, 1024
+desc = of.llama_graph(layers=L, tokens=T, seq_len=S, tp=1, dtype="bf16", **bench.LLAMA)
+g, plan, sess, bufs = bench.build_session(of, desc, [], dev, None, seed=1)
+sess.bind("positions", (torch.arange(T, device=dev) % S).to(torch.int64))
+spec = {"name": "sequential"}
+for _ in range(5):
+    sess.run(spec)
+torch.cuda.synchronize()
+tr = sess.trace()
+agg = collections.defaultdict(lambda: [0, 0.0])
+for e in tr:
+    key = e["name"].split(" u")[0]
+    key = key.split(".", 1)[1] if key.startswith("layer") else key
+    agg[key][0] += 1
+    agg[key][1] += e["dur"] / 1e3
+tot = sum(v[1] for v in agg.values())
+span = (max(e["ts"] + e["dur"] for e in tr) - min(e["ts"] for e in tr)) / 1e3
+rows = sorted(agg.items(), key=lambda kv: -kv[1][1])
+print(json.dumps({"which": which, "layers": L, "span_ms": round(span, 3), "sum_ms": round(tot, 3),
+                  "per_kernel_ms_per_layer": {k: round(v[1] / L, 4) for k, v in rows}}, indent=1))
