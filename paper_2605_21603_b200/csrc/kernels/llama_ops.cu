@@ -175,6 +175,17 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const float p = static_cast<float>(pos[row]);
   const int i0 = lane * 4;
+  // the rotation depends only on (position, dim): one sincos per lane element
+  // per row, shared by all q/k heads (reduced argument, MUFU sin/cos)
+  float cs[4], sn[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = (i0 + k) % (HD / 2);
+    const float ang = p * exp2f(-2.0f * static_cast<float>(j) / HD * log2_theta);
+    const float q = rintf(ang * 0.15915494309189535f);
+    const float red = fmaf(-q, 6.28318548202514648f, fmaf(-q, -1.7484556e-07f, ang));
+    __sincosf(red, &sn[k], &cs[k]);
+  }
   for (int h = warp; h < nq + nkv; h += blockDim.x / 32) {
     const uint2 u = *reinterpret_cast<const uint2*>(in + h * HD + i0);
     const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&u);
@@ -198,11 +209,7 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* 
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const float partner = __shfl_xor_sync(0xffffffffu, y[k], 16);
-      const int j = (i0 + k) % (HD / 2);
-      const float inv_freq = exp2f(-2.0f * static_cast<float>(j) / HD * log2_theta);
-      float sn, cs;
-      sincosf(p * inv_freq, &sn, &cs);
-      r[k] = lane < 16 ? y[k] * cs - partner * sn : y[k] * cs + partner * sn;
+      r[k] = lane < 16 ? y[k] * cs[k] - partner * sn[k] : y[k] * cs[k] + partner * sn[k];
     }
     uint2 w;
     __nv_bfloat162* w2 = reinterpret_cast<__nv_bfloat162*>(&w);

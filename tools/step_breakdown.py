@@ -1,4 +1,4 @@
-"""In-situ per-kernel breakdown of one step (eager replay of the compiled plan
+"""In-situ per-kernel breakdown of one step (prefill | moe) (eager replay of the compiled plan
 with CUDA events around every launch, OPF_TRACE_LAUNCHES=1): prefill
 (Llama-3-8B-shaped layers, 8 x 1024 tokens) or decode (512 x 4K, HND pages).
 Usage: python tools/step_breakdown.py [prefill|decode] [layers]"""
@@ -18,7 +18,10 @@ which = sys.argv[1] if len(sys.argv) > 1 else "prefill"
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 dev = torch.device("cuda:0")
 T, S = 8192, 1024
-desc = of.llama_graph(layers=L, tokens=T, seq_len=S, tp=1, dtype="bf16", **bench.LLAMA)
+if which == "moe":
+    desc = of.qwen3_moe_graph(layers=L, tokens=T, seq_len=S, dtype="bf16", ep=1, **bench.QWEN3)
+else:
+    desc = of.llama_graph(layers=L, tokens=T, seq_len=S, tp=1, dtype="bf16", **bench.LLAMA)
 g, plan, sess, bufs = bench.build_session(of, desc, [], dev, None, seed=1)
 sess.bind("positions", (torch.arange(T, device=dev) % S).to(torch.int64))
 spec = {"name": "sequential"}
