@@ -656,6 +656,198 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   }
 }
 
+__device__ __forceinline__ void tma4b(uint32_t dst, const CUtensorMap* map, uint32_t bar, int blk) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %3, %3, %4}], "
+      "[%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(0), "r"(blk)
+      : "memory");
+}
+
+// TMA-fed variant of decode_t_kernel for HND pages (OPF_DECODE=tt): one 4 KB
+// TMA per page and tensor (lane 0) instead of 16 cp.async per lane, per-slot
+// mbarriers, the same tokens-on-M math.
+template <int W, int D>
+__global__ void __launch_bounds__(W * 32)
+    decode_tt_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                     const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ kc,
+                    const __nv_bfloat16* __restrict__ vc, const int64_t* __restrict__ table,
+                    const int64_t* __restrict__ ctx_len, __nv_bfloat16* __restrict__ out, int nq, int nkv,
+                    int64_t max_pages, float scale_log2, int64_t n_items, int hnd) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int kRing = D * 2 * kPageBytes;
+  const uint32_t full0 = saddr(smem + W * kRing);  // [W][D] mbarriers
+  if (threadIdx.x < W * D) mbar_init_d(full0 + 8 * threadIdx.x, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  uint32_t issued = 0, consumed = 0;  // this warp's pages, across items (slot = n % D, phase = n / D)
+  pdl_wait();
+  pdl_trigger();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int g = lane >> 2, t = lane & 3;
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int64_t b = item / nkv;
+    const int kh = static_cast<int>(item % nkv);
+    const int G = nq / nkv;
+    const int64_t Wd = static_cast<int64_t>(nq + 2 * nkv) * HD;
+    const __nv_bfloat16* row = qkv + b * Wd;
+    const int64_t ctx = ctx_len[b];
+    const int n_pages = static_cast<int>((ctx + PAGE - 1) / PAGE);
+    // NHD pages [16 tokens][nkv][128] (reference / vLLM layout) or HND pages
+    // [nkv][16 tokens][128]: one (page, kv head) block is 4 KB contiguous, which
+    // DRAM streams ~2-5% faster than 16 rows of 256 B at 2 KB stride
+    const int64_t tok_stride = hnd ? HD : static_cast<int64_t>(nkv) * HD;
+    const int64_t head_off = hnd ? static_cast<int64_t>(kh) * PAGE * HD : static_cast<int64_t>(kh) * HD;
+    uint8_t* ring = smem + warp * kRing;
+    auto k_slot = [&](int s) { return ring + s * 2 * kPageBytes; };
+    auto v_slot = [&](int s) { return ring + s * 2 * kPageBytes + kPageBytes; };
+    auto issue = [&](int page_idx, int) {
+      // HND pages: one 4 KB (page, kv head) block per tensor, one TMA each
+      const int blk = static_cast<int>(table[b * max_pages + page_idx] * nkv + kh);
+      const int s = static_cast<int>(issued % D);
+      if (lane == 0) {
+        const uint32_t bar = full0 + 8 * (warp * D + s);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * kPageBytes)
+                     : "memory");
+        tma4b(saddr(k_slot(s)), &kmap, bar, blk);
+        tma4b(saddr(v_slot(s)), &vmap, bar, blk);
+      }
+      ++issued;
+    };
+    // Q^T as the B operand: n = head g of the group (zero for g >= G), k = dims
+    uint32_t qb[8][2];
+    {
+      const bool valid = g < G;
+      const __nv_bfloat16* qrow = row + static_cast<int64_t>(kh * G + (valid ? g : 0)) * HD;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        qb[kk][0] = valid ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t) : 0u;
+        qb[kk][1] = valid ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * t) : 0u;
+      }
+    }
+    float o[8][4];  // O^T: [dim tile][(dim g | g+8) x (head 2t | 2t+1)]
+#pragma unroll
+    for (int d = 0; d < 8; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.0f;
+    float m_r[2] = {-FLT_MAX, -FLT_MAX}, l_r[2] = {0.0f, 0.0f};  // heads 2t, 2t+1 (l: this lane's tokens)
+    int my_pages = 0;
+    for (int p = warp; p < n_pages; p += W) ++my_pages;
+#pragma unroll
+    for (int s2 = 0; s2 < D; ++s2)
+      if (s2 < my_pages) issue(warp + s2 * W, s2);
+    const int srcA = 8 * t + (g >> 1), srcB = srcA + 4;  // lanes holding tokens 2t / 2t+1 (and +8)
+    const bool odd = g & 1;
+    for (int i = 0; i < my_pages; ++i) {
+      const int sl = static_cast<int>(consumed % D);
+      const int page_idx = warp + i * W;
+      mbar_wait_d(full0 + 8 * (warp * D + sl), (consumed / D) & 1u);
+      ++consumed;
+      const uint32_t kb = saddr(k_slot(sl)), vb = saddr(v_slot(sl));
+      float sc[4] = {0, 0, 0, 0};  // (tok g, heads 2t|2t+1), (tok g+8, ...)
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        uint32_t a[4];
+        ldsm4(kb + swz2((lane & 7) + ((lane >> 3) & 1) * 8, kk * 2 + (lane >> 4)), a[0], a[1], a[2], a[3]);
+        mma(sc, a, qb[kk][0], qb[kk][1]);
+      }
+      const int64_t tok0 = static_cast<int64_t>(page_idx) * PAGE;
+      const bool v0 = tok0 + g < ctx, v1 = tok0 + g + 8 < ctx;
+      float p[4];
+      float corr[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float x0 = v0 ? sc[e] * scale_log2 : -FLT_MAX;
+        const float x1 = v1 ? sc[2 + e] * scale_log2 : -FLT_MAX;
+        float mx = fmaxf(x0, x1);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        mx = fmaxf(mx, m_r[e]);
+        corr[e] = exp2f(m_r[e] - mx);
+        p[e] = exp2f(x0 - mx);
+        p[2 + e] = exp2f(x1 - mx);
+        l_r[e] = l_r[e] * corr[e] + p[e] + p[2 + e];
+        m_r[e] = mx;
+      }
+      // P^T as the B operand: (tok 2t | 2t+1, head g) and (tok 2t+8 | 2t+9, head g)
+      const float a0 = __shfl_sync(0xffffffffu, p[0], srcA), a1 = __shfl_sync(0xffffffffu, p[1], srcA);
+      const float a2 = __shfl_sync(0xffffffffu, p[2], srcA), a3 = __shfl_sync(0xffffffffu, p[3], srcA);
+      const float b0 = __shfl_sync(0xffffffffu, p[0], srcB), b1 = __shfl_sync(0xffffffffu, p[1], srcB);
+      const float b2 = __shfl_sync(0xffffffffu, p[2], srcB), b3 = __shfl_sync(0xffffffffu, p[3], srcB);
+      const uint32_t pb0 = pk(odd ? a1 : a0, odd ? b1 : b0);
+      const uint32_t pb1 = pk(odd ? a3 : a2, odd ? b3 : b2);
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        o[d][0] *= corr[0];
+        o[d][1] *= corr[1];
+        o[d][2] *= corr[0];
+        o[d][3] *= corr[1];
+      }
+#pragma unroll
+      for (int dm = 0; dm < 8; ++dm) {
+        uint32_t a[4];
+        ldsm4t(vb + swz2((lane & 7) + (lane >> 4) * 8, dm * 2 + ((lane >> 3) & 1)), a[0], a[1], a[2], a[3]);
+        mma(o[dm], a, pb0, pb1);
+      }
+      __syncwarp();
+      if (i + D < my_pages) issue(warp + (i + D) * W, sl);
+    }
+    // ---- merge
+    __syncthreads();
+    float* sm_m = reinterpret_cast<float*>(smem);  // [W][8]
+    float* sm_l = sm_m + W * 8;                     // [W][8]
+    float* sm_o = sm_l + W * 8;                     // [W][8][HD]
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      l_r[e] += __shfl_xor_sync(0xffffffffu, l_r[e], 4);
+      l_r[e] += __shfl_xor_sync(0xffffffffu, l_r[e], 8);
+      l_r[e] += __shfl_xor_sync(0xffffffffu, l_r[e], 16);
+    }
+    if (g == 0) {
+      sm_m[warp * 8 + 2 * t] = m_r[0];
+      sm_m[warp * 8 + 2 * t + 1] = m_r[1];
+      sm_l[warp * 8 + 2 * t] = l_r[0];
+      sm_l[warp * 8 + 2 * t + 1] = l_r[1];
+    }
+#pragma unroll
+    for (int dm = 0; dm < 8; ++dm) {
+      sm_o[(warp * 8 + 2 * t) * HD + dm * 16 + g] = o[dm][0];
+      sm_o[(warp * 8 + 2 * t + 1) * HD + dm * 16 + g] = o[dm][1];
+      sm_o[(warp * 8 + 2 * t) * HD + dm * 16 + g + 8] = o[dm][2];
+      sm_o[(warp * 8 + 2 * t + 1) * HD + dm * 16 + g + 8] = o[dm][3];
+    }
+    __syncthreads();
+    float* sm_cur = sm_o + W * 8 * HD;  // [8]
+    const __nv_bfloat16* kcur = row + static_cast<int64_t>(nq + kh) * HD;
+    const __nv_bfloat16* vcur = row + static_cast<int64_t>(nq + nkv + kh) * HD;
+    for (int h = warp; h < G; h += W) {
+      const __nv_bfloat16* q = row + static_cast<int64_t>(kh * G + h) * HD;
+      float dot = 0.0f;
+      for (int d = lane; d < HD; d += 32) dot += __bfloat162float(q[d]) * __bfloat162float(kcur[d]);
+#pragma unroll
+      for (int s2 = 16; s2 > 0; s2 >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, s2);
+      if (lane == 0) sm_cur[h] = dot * scale_log2;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < G * HD; idx += blockDim.x) {
+      const int h = idx / HD, d = idx % HD;
+      float M = sm_cur[h];
+      for (int w = 0; w < W; ++w) M = fmaxf(M, sm_m[w * 8 + h]);
+      const float cc = exp2f(sm_cur[h] - M);
+      float L = cc, A = cc * __bfloat162float(vcur[d]);
+      for (int w = 0; w < W; ++w) {
+        if (sm_l[w * 8 + h] == 0.0f) continue;
+        const float c = exp2f(sm_m[w * 8 + h] - M);
+        L += sm_l[w * 8 + h] * c;
+        A += sm_o[(w * 8 + h) * HD + d] * c;
+      }
+      out[b * static_cast<int64_t>(nq) * HD + static_cast<int64_t>(kh * G + h) * HD + d] = __float2bfloat16(A / L);
+    }
+    __syncthreads();
+  }
+}
+
 using EncodeFnD = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -681,7 +873,43 @@ bool cache_map(CUtensorMap* m, const void* base, int nkv, int64_t pages) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool cache_map_hnd(CUtensorMap* m, const void* base, int nkv, int64_t pages) {
+  static EncodeFnD fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeFnD>(nullptr);
+    return reinterpret_cast<EncodeFnD>(p);
+  }();
+  if (!fn) return false;
+  // HND: [pages * nkv blocks][16 tokens][2 halves][64 dims] -> box [1][16][2][64] (one block)
+  const cuuint64_t dims[4] = {64, 2, PAGE, static_cast<cuuint64_t>(pages * nkv)};
+  const cuuint64_t strides[3] = {128, 256, static_cast<cuuint64_t>(PAGE) * HD * 2};
+  const cuuint32_t box[4] = {64, 2, PAGE, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
+
+template <int W, int D>
+bool launch_decode_tt(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
+                      const int64_t* table, const int64_t* ctx, __nv_bfloat16* out, int nq, int nkv,
+                      int64_t max_pages, int64_t cache_pages, float scale_log2, int64_t items, int64_t grid,
+                      cudaStream_t s) {
+  constexpr int kSmem = 1024 + W * D * 2 * kPageBytes + 1024;
+  static bool attr = cudaFuncSetAttribute(decode_tt_kernel<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kSmem) == cudaSuccess;
+  if (!attr) return false;
+  CUtensorMap km, vm;
+  if (!cache_map_hnd(&km, kc, nkv, cache_pages) || !cache_map_hnd(&vm, vc, nkv, cache_pages)) return false;
+  launch_pdl(decode_tt_kernel<W, D>, dim3(static_cast<unsigned>(grid)), dim3(W * 32), kSmem, s, km, vm, qkv, kc, vc,
+             table, ctx, out, nq, nkv, max_pages, scale_log2, items, 1);
+  return true;
+}
 
 template <int W, int D>
 bool launch_decode_t(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
@@ -701,7 +929,7 @@ bool launch_decode_t(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __
 bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                      const int64_t* table, const int64_t* ctx, __nv_bfloat16* out, int64_t B, int nq,
                      int nkv, int hd, int page, int64_t max_pages, float scale, int max_ctas, int hnd,
-                     cudaStream_t s) {
+                     int64_t cache_pages, cudaStream_t s) {
   if (hd != HD || page != PAGE || nq % nkv != 0 || nq / nkv > 8) return false;
   // OPF_DECODE: t12x2 (default) | t8x3 | mma16 (group padded to M = 16)
   static const int variant = [] {
@@ -711,12 +939,16 @@ bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __
     if (e && std::string(e) == "t14x2") return 3;
     if (e && std::string(e) == "t16x1") return 4;
     if (e && std::string(e) == "t6x4") return 5;
+    if (e && std::string(e) == "tt") return 6;
     return 2;
   }();
   const int64_t items = B * nkv;
   int64_t grid = max_ctas > 0 ? std::min<int64_t>(max_ctas, num_sms()) : num_sms();
   grid = std::max<int64_t>(1, std::min(grid, items));
   const float sl2 = scale * 1.4426950408889634f;
+  if (variant == 6 && hnd && (reinterpret_cast<uintptr_t>(kc) | reinterpret_cast<uintptr_t>(vc)) % 16 == 0)
+    return launch_decode_tt<12, 2>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, cache_pages, sl2, items, grid,
+                                   s);
   if (variant == 1) return launch_decode_t<8, 3>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
   if (variant == 2) return launch_decode_t<12, 2>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
   if (variant == 3) return launch_decode_t<14, 2>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);

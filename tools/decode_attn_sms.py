@@ -14,14 +14,17 @@ B, ctx, page, nq, nkv, hd = 512, 4096, 16, 32, 8, 128
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev).manual_seed(3)
 pages = B * ctx // page
-kc = torch.rand(pages, page, nkv, hd, device=dev, generator=g).to(torch.bfloat16)
-vc = torch.rand(pages, page, nkv, hd, device=dev, generator=g).to(torch.bfloat16)
+hnd = os.environ.get("DEC_LAYOUT", "hnd") == "hnd"
+shape = (pages, nkv, page, hd) if hnd else (pages, page, nkv, hd)
+kc = torch.rand(*shape, device=dev, generator=g).to(torch.bfloat16)
+vc = torch.rand(*shape, device=dev, generator=g).to(torch.bfloat16)
 table = torch.randperm(pages, device=dev, generator=g).view(B, -1)
 pos = torch.full((B,), ctx - 1, dtype=torch.int64, device=dev)
 qkv = torch.randn(B, (nq + 2 * nkv) * hd, device=dev).to(torch.bfloat16)
 out = torch.empty(B, nq * hd, device=dev, dtype=torch.bfloat16)
 op = {"name": "d", "kind": "Custom", "inputs": [], "outputs": [],
-      "attrs": {"custom_name": "attn_decode", "params": {"heads": nq, "kv_heads": nkv, "head_dim": hd, "page_size": page}}}
+      "attrs": {"custom_name": "attn_decode", "params": {"heads": nq, "kv_heads": nkv, "head_dim": hd, "page_size": page,
+                                                         "kv_layout": 1 if hnd else 0}}}
 kvb = 2.0 * B * ctx * nkv * hd * 2
 res = {}
 for sms in [148, 124, 108, 92, 74, 64, 48]:
@@ -37,4 +40,5 @@ for sms in [148, 124, 108, 92, 74, 64, 48]:
     ms = e0.elapsed_time(e1) / 10
     res[sms] = round(kvb / ms / 1e6)
 print(json.dumps({"lib": os.environ.get("OPF_LIB", "default"), "decode": os.environ.get("OPF_DECODE", ""),
+                  "layout": "hnd" if hnd else "nhd",
                   "gbs_by_sms": res}))

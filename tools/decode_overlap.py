@@ -18,13 +18,13 @@ H, nq, nkv, hd, I = 4096, 32, 8, 128, 14336
 dev = torch.device("cuda:0")
 nsm = torch.cuda.get_device_properties(dev).multi_processor_count
 desc = of.llama_decode_graph(layers=L, tokens=B, ctx_len=ctx, page_size=page, hidden=H, heads=nq,
-                             kv_heads=nkv, head_dim=hd, inter=I, dtype="bf16")
+                             kv_heads=nkv, head_dim=hd, inter=I, dtype="bf16", kv_layout=1)
 g = of.build_graph(desc)
 sess = of.Session(g, of.partition(g, [of.PartitionRule.by_func("attn_decode")]), {"lanes": 3})
 gen = torch.Generator(device=dev).manual_seed(5)
 pages = B * ctx // page
-kc = (torch.rand(pages, page, nkv, hd, device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
-vc = (torch.rand(pages, page, nkv, hd, device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
+kc = (torch.rand(pages, nkv, page, hd, device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
+vc = (torch.rand(pages, nkv, page, hd, device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
 keep = {}
 for t in g.description["tensors"]:
     n, shape = t["name"], t["shape"]
@@ -86,7 +86,8 @@ half = B // 2
 qkv = torch.randn(half, (nq + 2 * nkv) * hd, device=dev).to(torch.bfloat16)
 out = torch.empty(half, nq * hd, device=dev, dtype=torch.bfloat16)
 aop = {"name": "a", "kind": "Custom", "inputs": [], "outputs": [],
-       "attrs": {"custom_name": "attn_decode", "params": {"heads": nq, "kv_heads": nkv, "head_dim": hd, "page_size": page}}}
+       "attrs": {"custom_name": "attn_decode", "params": {"heads": nq, "kv_heads": nkv, "head_dim": hd, "page_size": page,
+                                                          "kv_layout": 1}}}
 ins = [qkv, kc, vc, keep["block_table"][:half], keep["positions"][:half]]
 kvb = 2.0 * half * ctx * nkv * hd * 2
 print("attention (half batch) alone:")
