@@ -66,6 +66,8 @@ def parse():
     p.add_argument("--moe-layers", type=int, default=1)
     p.add_argument("--decode-batch", type=int, default=512)
     p.add_argument("--decode-ctx", type=int, default=4096)
+    p.add_argument("--rounds", type=int, default=3, help="interleaved timing rounds per candidate (median)")
+    p.add_argument("--soak", type=float, default=2.0, help="seconds of power soak before each leg's timing")
     p.add_argument("--sm-sweep", type=int, nargs="*", default=None,
                    help="decode: also try NanoFlow SM partitions with G SMs for the GEMM lane")
     return p.parse_args()
@@ -187,7 +189,10 @@ def time_steps(torch, fn, steps, warmup, stream, world):
     return allreduce_max(ms, world)
 
 
-def time_candidates(torch, sess, cands, steps, warmup, stream, world, rounds=3, soak_s=2.0):
+ROUNDS, SOAK_S = 3, 2.0
+
+
+def time_candidates(torch, sess, cands, steps, warmup, stream, world, rounds=None, soak_s=None):
     """Every candidate schedule timed over `rounds` interleaved rounds (each a
     W-warm-up + K-step CUDA-event region), median per candidate.  A soak of
     ~soak_s seconds first brings the GPU to its power-capped steady state, so
@@ -195,6 +200,8 @@ def time_candidates(torch, sess, cands, steps, warmup, stream, world, rounds=3, 
     sw_power_cap within seconds of dense load: measured 1183 -> 1279 us for the
     same MoE plan, tools/host_overhead.py)."""
     import statistics
+    rounds = ROUNDS if rounds is None else rounds
+    soak_s = SOAK_S if soak_s is None else soak_s
     first = next(iter(cands.values()))
     if soak_s > 0:
         # a fixed step count agreed by all ranks (collectives must match)
@@ -214,14 +221,17 @@ def time_candidates(torch, sess, cands, steps, warmup, stream, world, rounds=3, 
     return {k: statistics.median(v) for k, v in per.items()}
 
 
-def time_auto(torch, sess, cands, steps, warmup, stream, world):
-    """DynaFlow's context-aware choice: the engine's `auto` strategy times every
-    candidate (sequential included) on the device once per row count and
-    replays the winner.  Returns (ms per step, chosen candidate name)."""
-    if world > 1:  # per-rank device timing could pick different plans -> mismatched collectives
+def auto_spec(cands):
+    return {"name": "auto", "reps": 3, "candidates": list(cands.values())}
+
+
+def auto_result(sess, cands, ms):
+    """DynaFlow's context-aware choice, timed in the same interleaved rounds as
+    the fixed candidates: the engine's `auto` strategy times every candidate
+    (sequential included) on the device once per row count and replays the
+    winner.  Returns (ms per step, chosen candidate name) or (nan, None)."""
+    if ms is None:
         return float("nan"), None
-    spec = {"name": "auto", "reps": 3, "candidates": list(cands.values())}
-    ms = time_steps(torch, lambda: sess.run(spec, stream), steps, warmup, stream, world)
     chosen = None
     try:
         c = json.loads(sess.stats()["auto"][-1]["chosen"])
@@ -229,6 +239,14 @@ def time_auto(torch, sess, cands, steps, warmup, stream, world):
     except Exception:  # noqa: BLE001
         pass
     return ms, chosen
+
+
+def with_auto(cands, world):
+    """Candidates plus DynaFlow `auto` (single process only: per-rank device
+    timing could pick different plans and mismatch the collectives)."""
+    if world > 1:
+        return dict(cands)
+    return dict(cands, dynaflow_auto=auto_spec(cands))
 
 
 def gemm_roofline(of, torch, dev, shapes, reps=20):
@@ -308,8 +326,8 @@ def run_ours(args):
     results = {}
     out_name = [t["name"] for t in g.description["tensors"] if t["role"] == "output"][0]
     with Clocks(local) as clk:
-        results = time_candidates(torch, sess, cands, args.steps, args.warmup, stream, world)
-        auto_ms, auto_pick = time_auto(torch, sess, cands, args.steps, args.warmup, stream, world)
+        results = time_candidates(torch, sess, with_auto(cands, world), args.steps, args.warmup, stream, world)
+        auto_ms, auto_pick = auto_result(sess, cands, results.pop("dynaflow_auto", None))
     best = min((k for k in results if k != "sequential"), key=lambda k: results[k], default="sequential")
     seq_ms, best_ms = results["sequential"], results[best]
     tokens_job = T * 1  # TP: every rank processes the same T tokens of one replica
@@ -509,8 +527,8 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
     for gsm in (args.sm_sweep if args.sm_sweep is not None else [24, 40, 56, 72]):
         cands[f"nanoflow_class_sm{gsm}"] = {"name": "split_overlap", "n_microbatches": 2,
                                             "lane_sm_budget": [gsm, nsm - gsm, 0]}
-    res = time_candidates(torch, sess, cands, args.steps, args.warmup, stream, world)
-    auto_ms, auto_pick = time_auto(torch, sess, cands, args.steps, args.warmup, stream, world)
+    res = time_candidates(torch, sess, with_auto(cands, world), args.steps, args.warmup, stream, world)
+    auto_ms, auto_pick = auto_result(sess, cands, res.pop("dynaflow_auto", None))
     best = min((k for k in res if k != "sequential"), key=lambda k: res[k])
     # attention kernel alone: CUDA events around back-to-back launches on `stream`
     op = {"name": "a", "kind": "Custom", "inputs": [], "outputs": [],
@@ -609,9 +627,9 @@ def run_moe(of, torch, dev, args, rank, world, stream, comm=None):
         need = max(of.dry_run(g, plan, spec, rows=T, config={"lanes": 3, "world": world})[1]["last"]["plan_arena_bytes"]
                    for spec in cands.values())
         sess.enable_peer_arena(need)
-    res = time_candidates(torch, sess, cands, args.steps, args.warmup, stream, world)
+    res = time_candidates(torch, sess, with_auto(cands, world), args.steps, args.warmup, stream, world)
     launches = sess.stats()["last"]["launches"]
-    auto_ms, auto_pick = time_auto(torch, sess, cands, args.steps, args.warmup, stream, world)
+    auto_ms, auto_pick = auto_result(sess, cands, res.pop("dynaflow_auto", None))
     best = min((k for k in res if k != "sequential"), key=lambda k: res[k])
     del sess, bufs
     torch.cuda.synchronize()
@@ -754,6 +772,7 @@ def run_reference(args):
 
 if __name__ == "__main__":
     a = parse()
+    ROUNDS, SOAK_S = max(1, a.rounds), max(0.0, a.soak)
     if a.impl == "reference":
         run_reference(a)
     else:
