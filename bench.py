@@ -443,7 +443,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(xh[0].numel() * 2),
                     "d2h_bytes_per_step": int(oh[0].numel() * 2),
                     "pipelining": "two sessions alternate; step i+1 H2D and step i-1 D2H overlap step i"},
-            "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05, bf16)",
+            "roofline": {"bound": "tensor", "kernel": "gemm_tc2_kernel (tcgen05 cta_group::2, bf16; EPI 0/1/2 = plain / SiLU-mul / RoPE)",
                          "achieved": round(achieved, 1),
                          "peak": PEAKS["bf16_tflops"], "unit": "TFLOP/s",
                          "frac": round(achieved / PEAKS["bf16_tflops"], 4),
