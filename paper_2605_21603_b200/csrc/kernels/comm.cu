@@ -24,7 +24,7 @@
 namespace opflow {
 
 bool ar_add_rmsnorm_p2p(const opf_comm* c, const opf_view& o, const opf_view& x, const opf_view& g,
-                        opf_view& x_out, opf_view& y, int64_t rows, float eps, int max_ctas,
+                        opf_view& x_out, opf_view& y, int64_t rows, float eps, int max_ctas, int mode,
                         cudaStream_t s);
 
 namespace {
@@ -218,9 +218,11 @@ opf_status op_ar_add_rmsnorm(const opf_op_ctx* c, const opf_view* in, int32_t n_
   auto s = static_cast<cudaStream_t>(stream);
   const opf_comm* comm = static_cast<const opf_comm*>(c->comm);
   const float eps = static_cast<float>(ctx_param(*c, "eps", 1e-5));
-  // one-shot peer-memory kernel when the communicator has a window
+  // peer-memory kernel (one-shot, or two-shot for large messages at W >= 4;
+  // params.ar_mode 1 / 2 forces one / two-shot) when the communicator has a window
+  const int mode = static_cast<int>(ctx_param(*c, "ar_mode", 0.0));
   if (comm && comm->world > 1 && !comm->peer_buf.empty() &&
-      ar_add_rmsnorm_p2p(comm, in[0], in[1], in[2], out[0], out[1], rows, eps, c->max_ctas, s))
+      ar_add_rmsnorm_p2p(comm, in[0], in[1], in[2], out[0], out[1], rows, eps, c->max_ctas, mode, s))
     return launch_status("allreduce_add_rmsnorm_p2p");
   if (in[0].dtype == OPF_BF16)
     return launch_ar_norm<__nv_bfloat16>(comm, in[0], &in[1], &in[2], &out[0], out[1], rows, eps,

@@ -18,7 +18,9 @@
 // of hanging the GPU.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "opflow/comm.hpp"
 #include "opflow/device.hpp"
@@ -98,6 +100,99 @@ __global__ void __launch_bounds__(kThreads) ar_add_rmsnorm_p2p_kernel(
     __syncthreads();
   }
   // 4. peers are done reading my staging rows
+  cta_barrier(pp, my_epoch, world, rank, err);
+}
+
+// Two-shot variant (reduce-scatter -> residual add + RMSNorm -> all-gather)
+// for large messages at W >= 4: rank q reduces and normalises only row block
+// q (rows [q*B, (q+1)*B)), publishes x1 / h of its block in its window, and
+// every rank then gathers all blocks.  NVLink bytes pulled per rank:
+// 3 (W-1)/W x rows x H x 2 instead of the one-shot's (W-1) x rows x H x 2.
+// Row r's in-block index i decides its CTA (i mod grid) in every phase and on
+// every rank, so each CTA's pairwise per-slot barrier orders exactly the rows
+// it reads next (no grid-wide barrier).  Window: [partials | x1 | h].
+__global__ void __launch_bounds__(kThreads) ar2_add_rmsnorm_p2p_kernel(
+    PeerPtrs pp, int world, int rank, const __nv_bfloat16* __restrict__ partial,
+    __nv_bfloat16* __restrict__ my_stage, uint32_t* my_epoch, const __nv_bfloat16* __restrict__ resid,
+    const __nv_bfloat16* __restrict__ gamma, __nv_bfloat16* __restrict__ x_out,
+    __nv_bfloat16* __restrict__ y, int64_t rows, int64_t H, float eps, uint32_t* err) {
+  extern __shared__ float rowbuf[];
+  __shared__ float red[kThreads / 32];
+  const int64_t n8 = H / 8;
+  const int64_t blk = (rows + world - 1) / world;
+  const int64_t plane = rows * H;  // elements per window plane
+  // 1. publish my partial rows (every block)
+  for (int64_t i = blockIdx.x; i < blk; i += gridDim.x)
+    for (int q = 0; q < world; ++q) {
+      const int64_t r = q * blk + i;
+      if (r >= rows) continue;
+      for (int64_t c = threadIdx.x; c < n8; c += kThreads)
+        reinterpret_cast<uint4*>(my_stage + r * H)[c] = reinterpret_cast<const uint4*>(partial + r * H)[c];
+    }
+  if (!cta_barrier(pp, my_epoch, world, rank, err)) return;
+  // 2. reduce-scatter + residual + norm for my block, results into my window
+  for (int64_t i = blockIdx.x; i < blk; i += gridDim.x) {
+    const int64_t r = rank * blk + i;
+    if (r >= rows) continue;
+    float ss = 0.0f;
+    for (int64_t c = threadIdx.x; c < n8; c += kThreads) {
+      float acc[8];
+      {
+        const uint4 u = reinterpret_cast<const uint4*>(resid + r * H)[c];
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h2[e]);
+          acc[2 * e] = f.x;
+          acc[2 * e + 1] = f.y;
+        }
+      }
+      for (int p = 0; p < world; ++p) {
+        const uint4 u = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(pp.buf[p]) + r * H)[c];
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h2[e]);
+          acc[2 * e] += f.x;
+          acc[2 * e + 1] += f.y;
+        }
+      }
+      uint4 o;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        o2[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+        rowbuf[c * 8 + 2 * e] = acc[2 * e];
+        rowbuf[c * 8 + 2 * e + 1] = acc[2 * e + 1];
+        ss += acc[2 * e] * acc[2 * e] + acc[2 * e + 1] * acc[2 * e + 1];
+      }
+      reinterpret_cast<uint4*>(my_stage + plane + r * H)[c] = o;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = ss;
+    __syncthreads();
+    float tot = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) tot += red[w];
+    const float inv = rsqrtf(tot / static_cast<float>(H) + eps);
+    for (int64_t c = threadIdx.x; c < H; c += kThreads)
+      my_stage[2 * plane + r * H + c] = __float2bfloat16(rowbuf[c] * inv * __bfloat162float(gamma[c]));
+    __syncthreads();
+  }
+  if (!cta_barrier(pp, my_epoch, world, rank, err)) return;
+  // 3. all-gather x1 / h of every block from its owner
+  for (int64_t i = blockIdx.x; i < blk; i += gridDim.x)
+    for (int q = 0; q < world; ++q) {
+      const int64_t r = q * blk + i;
+      if (r >= rows) continue;
+      const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(pp.buf[q]);
+      for (int64_t c = threadIdx.x; c < n8; c += kThreads) {
+        reinterpret_cast<uint4*>(x_out + r * H)[c] = reinterpret_cast<const uint4*>(src + plane + r * H)[c];
+        reinterpret_cast<uint4*>(y + r * H)[c] = reinterpret_cast<const uint4*>(src + 2 * plane + r * H)[c];
+      }
+    }
+  // 4. peers are done reading my window
   cta_barrier(pp, my_epoch, world, rank, err);
 }
 
@@ -198,7 +293,7 @@ uint32_t comm_window_error(const opf_comm* c) {
 }
 
 bool ar_add_rmsnorm_p2p(const opf_comm* c, const opf_view& o, const opf_view& x, const opf_view& g,
-                        opf_view& x_out, opf_view& y, int64_t rows, float eps, int max_ctas,
+                        opf_view& x_out, opf_view& y, int64_t rows, float eps, int max_ctas, int mode,
                         cudaStream_t s) {
   if (!c || c->peer_buf.empty() || o.dtype != OPF_BF16) return false;
   const int64_t H = view_row_elems(o);
@@ -212,6 +307,27 @@ bool ar_add_rmsnorm_p2p(const opf_comm* c, const opf_view& o, const opf_view& x,
   }
   char* base = static_cast<char*>(c->window_base);
   int grid = max_ctas > 0 ? max_ctas : num_sms();
+  // two-shot for large messages at W >= 4 (3(W-1)/W vs (W-1) row-planes over
+  // NVLink) when the window holds partials + x1 + h; OPF_AR=oneshot|twoshot forces
+  static const int ar_mode = [] {
+    const char* e = std::getenv("OPF_AR");
+    if (e && std::string(e) == "oneshot") return 1;
+    if (e && std::string(e) == "twoshot") return 2;
+    return 0;
+  }();
+  const bool fits2 = static_cast<size_t>(3 * rows * H * 2) <= c->peer_bytes;
+  const int m = mode ? mode : ar_mode;
+  const bool two = fits2 && (m == 2 || (m == 0 && c->world >= 4 && rows * H * 2 >= (1 << 20)));
+  if (two) {
+    const int64_t blk = (rows + c->world - 1) / c->world;
+    grid = static_cast<int>(std::min<int64_t>(std::min(grid, kBarrierSlot), blk));
+    ar2_add_rmsnorm_p2p_kernel<<<std::max(grid, 1), kThreads, H * sizeof(float), s>>>(
+        pp, c->world, c->rank, vptr<__nv_bfloat16>(o), reinterpret_cast<__nv_bfloat16*>(base),
+        reinterpret_cast<uint32_t*>(base + eo), vptr<__nv_bfloat16>(x), vptr<__nv_bfloat16>(g),
+        vptr<__nv_bfloat16>(x_out), vptr<__nv_bfloat16>(y), rows, H, eps,
+        reinterpret_cast<uint32_t*>(base + eo + sizeof(uint32_t) * kMaxCtas));
+    return true;
+  }
   grid = static_cast<int>(std::min<int64_t>(std::min(grid, kBarrierSlot), rows));
   ar_add_rmsnorm_p2p_kernel<<<std::max(grid, 1), kThreads, H * sizeof(float), s>>>(
       pp, c->world, c->rank, vptr<__nv_bfloat16>(o), reinterpret_cast<__nv_bfloat16*>(base),

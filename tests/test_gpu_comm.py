@@ -14,17 +14,22 @@ pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("built")]
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_fused_allreduce_add_rmsnorm_virtual_ranks(cuda, world):
+@pytest.mark.parametrize("ar_mode,rows", [(1, 64), (2, 64), (2, 61)])
+def test_fused_allreduce_add_rmsnorm_virtual_ranks(cuda, world, ar_mode, rows):
+    """ar_mode 1: one-shot (every rank reduces every row); 2: two-shot
+    (reduce-scatter by row blocks -> add + norm -> all-gather), incl. a row
+    count that does not divide by the world size."""
     import torch
-    rows, H = 64, 4096
-    comms = of.Comm.virtual(world, 0, rows * H * 2)
+    H = 4096
+    comms = of.Comm.virtual(world, 0, 3 * rows * H * 2)
     rng = np.random.default_rng(world)
     tb = lambda a: torch.from_numpy(a.astype(np.float32)).cuda().to(torch.bfloat16)
     x = tb(rng.uniform(-1, 1, (rows, H)))
     g = tb(1 + 0.1 * rng.uniform(-1, 1, H))
     streams = [torch.cuda.Stream() for _ in range(world)]
     op = {"name": "f", "kind": "Custom", "inputs": [], "outputs": [],
-          "attrs": {"custom_name": "allreduce_add_rmsnorm", "world_size": world, "params": {"eps": 1e-5}}}
+          "attrs": {"custom_name": "allreduce_add_rmsnorm", "world_size": world,
+                    "params": {"eps": 1e-5, "ar_mode": ar_mode}}}
     for it in range(3):  # epochs advance on the device across calls
         parts = [tb(rng.uniform(-1, 1, (rows, H))) for _ in range(world)]
         outs = [(torch.empty_like(x), torch.empty_like(x)) for _ in range(world)]
