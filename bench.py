@@ -136,6 +136,22 @@ def allreduce_max(x: float, world: int) -> float:
     return float(t.item())
 
 
+def enable_window_all(of, comm, stage_bytes, world):
+    """Peer window (CUDA IPC) for the fused peer-memory collectives; every rank
+    agrees on success (all-reduce of a flag) or the run stays NCCL-only."""
+    import torch
+    import torch.distributed as dist
+    ok = 1.0
+    try:
+        comm.enable_window(stage_bytes)
+    except Exception as e:  # noqa: BLE001
+        print(f"[bench] peer window unavailable ({e}); NCCL-only collectives", file=sys.stderr)
+        ok = 0.0
+    t = torch.tensor([ok])
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item() > 0)
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -299,11 +315,13 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     comm = None
+    comm_window_ok = False
     if world > 1:
         import torch.distributed as dist
         uid = [of.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = of.Comm(world, rank, local, uid[0])
+        comm_window_ok = enable_window_all(of, comm, 3 * args.tokens * LLAMA["hidden"] * 2, world)
     tp = world
     T, S, L = args.tokens, args.seq_len, args.layers
     desc = of.llama_graph(layers=L, tokens=T, seq_len=S, tp=tp, dtype="bf16", **LLAMA)
@@ -417,7 +435,7 @@ def run_ours(args):
     if not args.no_moe and args.tokens % (world * args.seq_len) == 0:
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
-        moe = run_moe(of, torch, dev, args, rank, world, stream, comm)
+        moe = run_moe(of, torch, dev, args, rank, world, stream, comm, comm_window_ok)
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(args, T, S, tp)
         line = {
@@ -602,7 +620,7 @@ def time_op(of, torch, dev, stream, fn, ins, outs, params, rows, reps=20):
     return e0.elapsed_time(e1) / reps
 
 
-def run_moe(of, torch, dev, args, rank, world, stream, comm=None):
+def run_moe(of, torch, dev, args, rank, world, stream, comm=None, window_ok=True):
     """BASELINE configs[4]: Qwen3-30B-A3B-shaped MoE layer (q/k-norm GQA
     attention + 128-expert top-8 FFN), 8192 tokens (8 x 1024), dual-batch
     overlap vs sequential on one GPU (EP=1: dispatch/combine are local
@@ -622,8 +640,10 @@ def run_moe(of, torch, dev, args, rank, world, stream, comm=None):
     cands = {"sequential": {"name": "sequential"}, "dbo": {"name": "dbo", "align": S},
              "nanoflow_u2": {"name": "split_overlap", "n_microbatches": 2, "align": S, "lane_mode": "ubatch"}}
     if world > 1:
-        # peer window (count exchange + barriers) and symmetric arena sized for every candidate plan
-        comm.enable_window(1 << 16)
+        # the run's peer window (count exchange + barriers) and a symmetric arena
+        # sized for every candidate plan; EP needs both, so no window -> no MoE leg
+        if not window_ok:
+            return {"skipped": "expert parallelism needs the CUDA-IPC peer window, unavailable on this box"}
         need = max(of.dry_run(g, plan, spec, rows=T, config={"lanes": 3, "world": world})[1]["last"]["plan_arena_bytes"]
                    for spec in cands.values())
         sess.enable_peer_arena(need)

@@ -176,8 +176,12 @@ opf_status launch_kind(const opf_op_ctx& c, const opf_view* in, int n_in, opf_vi
         return launch_status("RowScale");
       case OperatorKind::kAllReduce: {
         const opf_comm* comm = static_cast<const opf_comm*>(c.comm);
+        // one-shot peer-memory all-reduce for small (decode-size) messages; large
+        // (prefill) ones go to NCCL's bandwidth-optimal algorithms, whose
+        // per-rank NVLink traffic is 2(W-1)/W instead of (W-1) row-planes
+        const int64_t msg = view_numel(in[0]) * (in[0].dtype == OPF_F32 ? 4 : in[0].dtype == OPF_I64 ? 8 : 2);
         if (comm && comm->world > 1 && !comm->peer_buf.empty() && comm->world == c.world_size &&
-            allreduce_p2p(comm, in[0], out[0], rows, c.max_ctas, s))
+            msg <= (int64_t{4} << 20) && allreduce_p2p(comm, in[0], out[0], rows, c.max_ctas, s))
           return launch_status("AllReduce(p2p)");
         if (comm && comm->world > 1) {
           if (comm->world != c.world_size)
