@@ -48,8 +48,8 @@ constexpr uint32_t kSmemV = kSmemK + kStages * kTile;   // [kStages]
 constexpr uint32_t kSmemBar = kSmemV + kStages * kTile;
 // TMEM columns: S[0] 0..127, S[1] 128..255, O 256..383, P[0] 384..447, P[1] 448..511
 constexpr uint32_t kColO = 256, kColP = 384;
-constexpr uint32_t kSmemXch = kSmemBar + 256;           // row max / sum exchange [2][2][128] f32
-constexpr uint32_t kSmemTotal = kSmemXch + 2048 + 1024;  // + alignment slack
+constexpr uint32_t kSmemXch = kSmemBar + 256;           // row max / sum exchange [2][NP <= 4][128] f32
+constexpr uint32_t kSmemTotal = kSmemXch + 4096 + 1024;  // + alignment slack
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
 // kind::f16, D f32, A/B bf16, M=128, N=128; b_mn: B operand MN-major
@@ -113,6 +113,14 @@ __device__ __forceinline__ void tst32u(uint32_t a, const uint32_t* v) {
       "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
       "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
       "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tst16u(uint32_t a, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16};" ::"r"(a),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
 }
 __device__ __forceinline__ void commit(uint64_t* b) {
@@ -198,9 +206,16 @@ __device__ long long g_fa_trace[12][64];
   } while (0)
 #endif
 
-__global__ void __launch_bounds__(kThreads, 1)
+// NP = column parts per query row: NP x 4 softmax warps, each thread owning
+// one row x 128/NP key columns (NP = 2: 8 warps, the round-1 default; NP = 4:
+// 16 warps with 32 columns each — more warps to hide the softmax latency chain).
+template <int NP>
+__global__ void __launch_bounds__(128 + NP * 128, 1)
     fa_tc_kernel(const __grid_constant__ CUtensorMap mqkv, __nv_bfloat16* __restrict__ out, int nq,
                  int nkv, int S, int n_seqs, float scale_log2) {
+  constexpr int CP = 128 / NP;         // key (and O) columns per softmax thread
+  constexpr int kSoftW = 4 * NP;       // softmax warps
+  constexpr int kPoly = kPolyPairs * CP / 64;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kSmemBar);
@@ -239,11 +254,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       bar_init(&k_empty[i], 1);
       bar_init(&v_empty[i], 1);
       bar_init(&s_full[i], 1);
-      bar_init(&s_free[i], 8);
+      bar_init(&s_free[i], kSoftW);
     }
-    bar_init(p_full, 8);
+    bar_init(p_full, kSoftW);
     bar_init(o_done, 1);
-    bar_init(o_free, 8);
+    bar_init(o_free, kSoftW);
     *pv_count = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -406,23 +421,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {  // ---------------------------------------- softmax / epilogue
-    // Two warps per TMEM lane quarter: hf = 0 takes key columns 0..63 (and O
-    // columns 0..63), hf = 1 columns 64..127.  Row max / row sum halves meet in
-    // a double-buffered smem exchange behind a 64-thread named barrier.
+    // NP warps per TMEM lane quarter: part pt takes key columns pt*CP.. (and the
+    // same O columns).  Row max / row sum parts meet in a double-buffered smem
+    // exchange behind a per-quarter named barrier.
     const int q = warp & 3;             // TMEM lane quarter
-    const int hf = (warp - 4) >> 2;     // column half
+    const int pt = (warp - 4) >> 2;     // column part
     const int r = q * 32 + lane;        // query row within the tile
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + hf * 64;   // S columns
-    const uint32_t o_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + kColO + hf * 64;
-    const uint32_t p_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + kColP + hf * 32;
-    float* xch = reinterpret_cast<float*>(sm + kSmemXch);  // [2 parity][2 half][128 rows]
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + pt * CP;   // S columns
+    const uint32_t o_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + kColO + pt * CP;
+    const uint32_t p_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + kColP + pt * (CP / 2);
+    float* xch = reinterpret_cast<float*>(sm + kSmemXch);  // [2 parity][NP parts][128 rows]
     uint32_t xpar = 0;
-    auto exchange = [&](float v) {  // returns the partner half's value for row r
-      xch[(xpar * 2 + hf) * 128 + r] = v;
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-      const float o = xch[(xpar * 2 + (hf ^ 1)) * 128 + r];
+    auto exchange = [&](float v, bool is_max) {  // reduction of v over the row's NP parts
+      xch[(xpar * NP + pt) * 128 + r] = v;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "n"(NP * 32) : "memory");
+      float acc = xch[(xpar * NP) * 128 + r];
+#pragma unroll
+      for (int o = 1; o < NP; ++o) {
+        const float w = xch[(xpar * NP + o) * 128 + r];
+        acc = is_max ? fmaxf(acc, w) : acc + w;
+      }
       xpar ^= 1;
-      return o;
+      return acc;
     };
     uint32_t sfull_ph = 0;  // per-S-buffer bits
     uint32_t pv_seen = 0;   // PV count at the start of this item
@@ -430,16 +450,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       int qt, h, seq;
       decode_item(it, qt, h, seq);
       const int n = qt + 1;
-      float m_used = -FLT_MAX, l = 0.0f;  // m_used in scaled log2 units; l over this half
+      float m_used = -FLT_MAX, l = 0.0f;  // m_used in scaled log2 units; l over this part
       for (int j = 0; j < n; ++j) {
         const int b = j & 1;
         bar_wait(&s_full[b], (sfull_ph >> b) & 1u);
         if (lane == 0 && warp == 4) FA_T(5, tile_sm);
         sfull_ph ^= 1u << b;
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        float s[64];
-        tld32(lane_base + b * 128, *reinterpret_cast<float(*)[32]>(&s[0]));
-        tld32(lane_base + b * 128 + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+        float s[CP];
+#pragma unroll
+        for (int c = 0; c < CP / 32; ++c)
+          tld32(lane_base + b * 128 + c * 32, *reinterpret_cast<float(*)[32]>(&s[c * 32]));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
@@ -452,17 +473,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
         if (j == qt) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) {
-            if (hf * 64 + c > r) s[c] = -INFINITY;
+          for (int c = 0; c < CP; ++c) {
+            if (pt * CP + c > r) s[c] = -INFINITY;
             mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
+          for (int c = 0; c < CP; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
         }
         const float pm = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-        const float mx = scale_log2 * fmaxf(pm, exchange(pm));  // identical in both halves
+        const float mx = scale_log2 * exchange(pm, true);  // identical in every part
         if (lane == 0 && warp == 4) FA_T(8, tile_sm);
         // lazy rescale of the exponent base (log2 units)
         float factor = 1.0f;
@@ -473,14 +494,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         l *= factor;
         float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        uint32_t pk[32];  // P row half, packed bf16x2
+        uint32_t pk[CP / 2];  // P row part, packed bf16x2
 #pragma unroll
-        for (int c2 = 0; c2 < 32; ++c2) {
-          // FA4-style split: the first kPolyPairs pairs use the FMA-pipe polynomial,
+        for (int c2 = 0; c2 < CP / 2; ++c2) {
+          // FA4-style split: the first kPoly pairs use the FMA-pipe polynomial,
           // the rest MUFU ex2 (the pipes run concurrently)
           const float x0 = fmaf(s[2 * c2], scale_log2, -m_used), x1 = fmaf(s[2 * c2 + 1], scale_log2, -m_used);
-          const float p0 = c2 < kPolyPairs ? ex2_poly(x0) : ex2(x0);
-          const float p1 = c2 < kPolyPairs ? ex2_poly(x1) : ex2(x1);
+          const float p0 = c2 < kPoly ? ex2_poly(x0) : ex2(x0);
+          const float p1 = c2 < kPoly ? ex2_poly(x1) : ex2(x1);
           sum8[(2 * c2) & 7] += p0;
           sum8[(2 * c2 + 1) & 7] += p1;
           pk[c2] = bf2(p0, p1);
@@ -494,9 +515,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (lane == 0 && warp == 4) FA_T(10, tile_sm);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (any_rescale) {  // this half's 64 O columns
+        if (any_rescale) {  // this part's CP O columns
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
+          for (int c = 0; c < CP / 32; ++c) {
             float o[32];
             tld32(o_base + c * 32, o);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -505,7 +526,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             tst32(o_base + c * 32, o);
           }
         }
-        tst32u(p_base + (j & 1) * 64, pk);
+        if constexpr (CP == 64)
+          tst32u(p_base + (j & 1) * 64, pk);
+        else
+          tst16u(p_base + (j & 1) * 64, pk);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
@@ -514,16 +538,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++tile_sm;
       }
       // ---- epilogue: wait for the item's last PV, O / l -> bf16 -> global
-      const float l_all = l + exchange(l);
+      const float l_all = exchange(l, false);
       while (ld_acquire(pv_count_addr) < pv_seen + static_cast<uint32_t>(n)) {
       }
       pv_seen += n;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const float inv = l_all > 0.0f ? 1.0f / l_all : 0.0f;
       __nv_bfloat16* orow = out + (static_cast<int64_t>(seq) * S + qt * BQ + r) * (static_cast<int64_t>(nq) * HD) +
-                            static_cast<int64_t>(h) * HD + hf * 64;
+                            static_cast<int64_t>(h) * HD + pt * CP;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < CP / 32; ++c) {
         float o[32];
         tld32(o_base + c * 32, o);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -891,7 +915,9 @@ bool prefill_bf16_tcgen05(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t 
       return static_cast<EncodeFn>(nullptr);
     return reinterpret_cast<EncodeFn>(p);
   }();
-  static bool attr = cudaFuncSetAttribute(fa_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static bool attr = cudaFuncSetAttribute(fa_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kSmemTotal)) == cudaSuccess &&
+                     cudaFuncSetAttribute(fa_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(kSmemTotal)) == cudaSuccess &&
                      cudaFuncSetAttribute(fa_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(kPPSmem)) == cudaSuccess;
@@ -902,6 +928,10 @@ bool prefill_bf16_tcgen05(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t 
     return !(e && std::string(e) == "pp");  // ping-pong measured slower (softmax issue-bound), opt-in
   }();
   const bool pp = !one_tile && (nq / nkv) % 2 == 0;
+  static const int parts = [] {  // OPF_FA_PARTS=2|4 softmax column parts per row
+    const char* e = std::getenv("OPF_FA_PARTS");
+    return e && std::atoi(e) == 4 ? 4 : 2;
+  }();
   const int64_t W = static_cast<int64_t>(nq + 2 * nkv) * HD;
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(rows)};
@@ -919,8 +949,11 @@ bool prefill_bf16_tcgen05(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t 
   if (pp)
     launch_pdl(fa_pp_kernel, dim3(grid), dim3(kPPThreads), kPPSmem, s, m, out, nq, nkv, S, n_seqs,
                scale * 1.4426950408889634f);
+  else if (parts == 4)
+    launch_pdl(fa_tc_kernel<4>, dim3(grid), dim3(128 + 4 * 128), kSmemTotal, s, m, out, nq, nkv, S, n_seqs,
+               scale * 1.4426950408889634f);
   else
-    launch_pdl(fa_tc_kernel, dim3(grid), dim3(kThreads), kSmemTotal, s, m, out, nq, nkv, S, n_seqs,
+    launch_pdl(fa_tc_kernel<2>, dim3(grid), dim3(128 + 2 * 128), kSmemTotal, s, m, out, nq, nkv, S, n_seqs,
                scale * 1.4426950408889634f);
   return true;
 }
