@@ -124,6 +124,23 @@ opf_status opf_launch_comm(const char* op_json, const opf_view* in, int32_t n_in
                            int32_t n_out, int64_t rows, opf_comm* comm, int32_t max_ctas,
                            void* stream);
 
+/* ---------------------------------------------------------------- paged KV cache */
+/* Per-layer K / V page pools (bf16; layout 0 NHD [pages, page, kv, hd], 1 HND
+ * [pages, kv, page, hd]) with a free-list page allocator.  dry = 1: host logic
+ * only (no device pools).  Slots (page * page_size + offset) feed the kv_write
+ * op; block tables feed attn_decode. */
+typedef struct opf_kvcache opf_kvcache;
+opf_status opf_kv_create(int32_t layers, int64_t pages, int32_t page_size, int32_t kv_heads, int32_t head_dim,
+                         int32_t layout, int32_t device, int32_t dry, opf_kvcache** out);
+void opf_kv_free(opf_kvcache* c);
+opf_status opf_kv_cache_ptr(opf_kvcache* c, int32_t layer, int32_t which, void** out);
+opf_status opf_kv_append(opf_kvcache* c, const int64_t* seq_ids, const int32_t* n_new, int32_t n,
+                         int64_t* slots_out, int64_t* positions_out);
+opf_status opf_kv_release(opf_kvcache* c, int64_t seq_id);
+opf_status opf_kv_block_table(opf_kvcache* c, const int64_t* seq_ids, int32_t n, int64_t max_pages,
+                              int64_t* table_out, int64_t* lens_out);
+opf_status opf_kv_stats(opf_kvcache* c, int64_t* free_pages, int64_t* sequences);
+
 /* ---------------------------------------------------------------- comm (TP/EP) */
 typedef struct opf_comm opf_comm;
 /* NCCL unique id is 128 bytes; exchange it with any out-of-band channel. */

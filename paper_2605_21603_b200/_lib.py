@@ -67,6 +67,16 @@ _SIGS = {
     "opf_launch": (C.c_int32, [C.c_char_p, C.POINTER(opf_view), C.c_int32, C.POINTER(opf_view),
                                C.c_int32, C.c_int64, C.c_void_p]),
     "opf_gemm_splits": (C.c_int32, [C.c_int64, C.c_int64, C.c_int64, C.c_int32]),
+    "opf_kv_create": (C.c_int32, [C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                  C.c_int32, C.POINTER(C.c_void_p)]),
+    "opf_kv_free": (None, [C.c_void_p]),
+    "opf_kv_cache_ptr": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "opf_kv_append": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.c_int32,
+                                  C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "opf_kv_release": (C.c_int32, [C.c_void_p, C.c_int64]),
+    "opf_kv_block_table": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int64), C.c_int32, C.c_int64,
+                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "opf_kv_stats": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "opf_view_rows": (C.c_int32, [C.POINTER(opf_view), C.c_int64, C.c_int64, C.POINTER(opf_view)]),
     "opf_comm_unique_id": (C.c_int32, [C.POINTER(C.c_uint8)]),
     "opf_comm_init": (C.c_int32, [C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32,

@@ -55,6 +55,7 @@ OpRegistry::OpRegistry() {
   register_attention_ops(*this);
   register_comm_ops(*this);
   register_moe_ops(*this);
+  register_kv_ops(*this);
 }
 
 OpRegistry& OpRegistry::global() {

@@ -103,6 +103,7 @@ void register_llama_ops(OpRegistry& r);
 void register_attention_ops(OpRegistry& r);
 void register_comm_ops(OpRegistry& r);
 void register_moe_ops(OpRegistry& r);
+void register_kv_ops(OpRegistry& r);
 
 // ---- kernel launchers used across translation units -------------------------------
 // Stand-in kinds (bit-exact with the reference kernels for i64 / f32).

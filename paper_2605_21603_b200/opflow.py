@@ -630,6 +630,81 @@ class Session:
             self._h = C.c_void_p()
 
 
+class KvCache:
+    """Paged KV-cache manager (per-layer bf16 K / V page pools + a free-list page
+    allocator).  append() reserves cache slots for new tokens of sequences (the
+    kv_write op stores K / V there), block_table() gives attn_decode its rows.
+    dry=True runs the allocator without device pools (CPU)."""
+
+    def __init__(self, layers: int, pages: int, kv_heads: int, head_dim: int = 128, page_size: int = 16,
+                 kv_layout: int = 0, device: int = 0, dry: bool = False):
+        self._h = C.c_void_p()
+        check(lib().opf_kv_create(layers, pages, page_size, kv_heads, head_dim, kv_layout, device, int(dry),
+                                  C.byref(self._h)))
+        self.layers, self.pages, self.page_size = layers, pages, page_size
+        self.kv_heads, self.head_dim, self.kv_layout = kv_heads, head_dim, kv_layout
+
+    def cache(self, layer: int, which: str):
+        """The layer's K ('k') or V ('v') pool as a torch bf16 tensor (a view of
+        the manager's device memory, shaped for attn_decode / kv_write)."""
+        import torch
+        p = C.c_void_p()
+        check(lib().opf_kv_cache_ptr(self._h, layer, 0 if which == "k" else 1, C.byref(p)))
+        shape = ((self.pages, self.kv_heads, self.page_size, self.head_dim) if self.kv_layout == 1
+                 else (self.pages, self.page_size, self.kv_heads, self.head_dim))
+        n = self.pages * self.page_size * self.kv_heads * self.head_dim
+        return _device_tensor(p.value, n, torch.bfloat16).view(*shape)
+
+    def append(self, seq_ids: Sequence[int], n_new: Sequence[int]):
+        """Reserve n_new[i] tokens for seq_ids[i]; returns (slots, positions) int64 numpy arrays."""
+        import numpy as np
+        n = len(seq_ids)
+        ids = (C.c_int64 * max(n, 1))(*seq_ids)
+        cnt = (C.c_int32 * max(n, 1))(*n_new)
+        total = int(sum(n_new))
+        slots = (C.c_int64 * max(total, 1))()
+        pos = (C.c_int64 * max(total, 1))()
+        check(lib().opf_kv_append(self._h, ids, cnt, n, slots, pos))
+        return np.ctypeslib.as_array(slots)[:total].copy(), np.ctypeslib.as_array(pos)[:total].copy()
+
+    def release(self, seq_id: int) -> None:
+        check(lib().opf_kv_release(self._h, seq_id))
+
+    def block_table(self, seq_ids: Sequence[int], max_pages: int):
+        """(table [n, max_pages] int64 with -1 past each sequence's pages, lens [n]) as numpy."""
+        import numpy as np
+        n = len(seq_ids)
+        ids = (C.c_int64 * max(n, 1))(*seq_ids)
+        tab = (C.c_int64 * max(n * max_pages, 1))()
+        lens = (C.c_int64 * max(n, 1))()
+        check(lib().opf_kv_block_table(self._h, ids, n, max_pages, tab, lens))
+        return (np.ctypeslib.as_array(tab)[:n * max_pages].reshape(n, max_pages).copy(),
+                np.ctypeslib.as_array(lens)[:n].copy())
+
+    def stats(self) -> dict:
+        f, q = C.c_int64(), C.c_int64()
+        check(lib().opf_kv_stats(self._h, C.byref(f), C.byref(q)))
+        return {"free_pages": f.value, "sequences": q.value}
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and lib is not None:
+            lib().opf_kv_free(self._h)
+            self._h = C.c_void_p()
+
+
+def _device_tensor(ptr: int, numel: int, dtype):
+    """A torch tensor aliasing device memory owned by the library (no copy)."""
+    import torch
+
+    class _Holder:
+        def __init__(self, p, nbytes):
+            self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (p, False),
+                                             "version": 3}
+
+    nbytes = numel * torch.tensor([], dtype=dtype).element_size()
+    return torch.as_tensor(_Holder(ptr, nbytes), device="cuda").view(dtype)
+
+
 def launch(op: OpDecl | dict, inputs: Sequence, outputs: Sequence, rows: int, stream=None,
            comm: Optional[Comm] = None, max_ctas: int = 0) -> None:
     """Device eval_op_into: run one operator into caller-provided tensors."""
