@@ -498,7 +498,7 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
     # HND pages ([pages, kv_heads, 16, 128]: one (page, head) block is 4 KB
     # contiguous; measured +2.4% attention bandwidth over the NHD layout)
     desc = of.llama_decode_graph(layers=L, tokens=B, ctx_len=ctx, page_size=page, tp=tp, dtype="bf16",
-                                 kv_layout=1, **LLAMA)
+                                 kv_layout=1, kv_write=1, **LLAMA)
     g = of.build_graph(desc)
     # attention gets its own subgraphs (NanoFlow: memory-bound attention on one
     # lane, the compute-bound GEMM fillers between attentions on the other)
@@ -525,6 +525,10 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
             x = torch.full((B,), ctx - 1, dtype=torch.int64, device=dev)
         elif name == "block_table":
             x = torch.randperm(pages, device=dev, generator=gen).view(B, max_pages).to(torch.int64)
+        elif name == "slots":  # the step's token goes to cache position ctx - 1 of its sequence
+            continue
+        elif t["role"] == "output" and t.get("dtype") == "i64":  # kv_written: left to the arena
+            continue
         elif t["role"] == "output":
             x = torch.empty(shape, dtype=torch.bfloat16, device=dev)
         elif name.endswith("norm.w"):
@@ -535,6 +539,9 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
             x = (torch.rand(shape, device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
         keep[name] = x
         sess.bind(name, x)
+    # slot of each sequence's new token: (page of position ctx - 1) * page + offset
+    keep["slots"] = keep["block_table"][:, (ctx - 1) // page] * page + (ctx - 1) % page
+    sess.bind("slots", keep["slots"])
     cands = {"sequential": {"name": "sequential"},
              "nanoflow_u2": {"name": "split_overlap", "n_microbatches": 2, "lane_mode": "ubatch"},
              "nanoflow_class": {"name": "split_overlap", "n_microbatches": 2}}
@@ -570,7 +577,7 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
     achieved = kv_bytes / (attn_ms / 1e3) / 1e9
     del sess
     return {"workload": f"llama3-8b-shaped decode, {L} layers, batch {B} x ctx {ctx}, paged KV "
-                        f"(page {page}, HND pages, random block table), TP={tp}",
+                        f"(page {page}, HND pages, random block table, each step appends its K/V), TP={tp}",
             "tokens_per_s": round(B / (res[best] / 1e3), 1), "strategy": best,
             "sequential_tokens_per_s": round(B / (res["sequential"] / 1e3), 1),
             "speedup_vs_sequential": round(res["sequential"] / res[best], 4),

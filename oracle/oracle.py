@@ -25,7 +25,7 @@ from __future__ import annotations
 
 import heapq
 import json
-from typing import Dict, List
+from typing import Dict, List, Optional
 
 import numpy as np
 
@@ -353,13 +353,33 @@ def topo_order(desc: dict) -> List[int]:
     return order
 
 
+def kv_write(qkv, slots, kc, vc, heads, kv_heads, head_dim, page_size, kv_layout=0):
+    """Store each row's K / V (qkv columns of head nq + kh / nq + nkv + kh) into
+    its paged-cache slot (page * page_size + offset; < 0 skipped), in place."""
+    for t, s in enumerate(np.asarray(slots).reshape(-1)):
+        if s < 0:
+            continue
+        pg, off = int(s) // page_size, int(s) % page_size
+        for kh in range(kv_heads):
+            k = qkv[t, (heads + kh) * head_dim:(heads + kh + 1) * head_dim]
+            v = qkv[t, (heads + kv_heads + kh) * head_dim:(heads + kv_heads + kh + 1) * head_dim]
+            if kv_layout == 1:
+                kc[pg, kh, off], vc[pg, kh, off] = k, v
+            else:
+                kc[pg, off, kh], vc[pg, off, kh] = k, v
+    return np.asarray(slots).reshape(-1).astype(np.int64)
+
+
 def evaluate(desc_json: str, rows: int, bindings: Dict[str, np.ndarray],
-             exact: bool = True, allreduce=None) -> Dict[str, np.ndarray]:
+             exact: bool = True, allreduce=None, caches_out: Optional[Dict[str, np.ndarray]] = None
+             ) -> Dict[str, np.ndarray]:
     """eval_reference restated; bf16 graphs evaluate in fp32 (oracle precision).
 
     `allreduce(x, world_size)` overrides the reference's single-process
     AllReduce stand-in (x * world_size, eval.cpp:63-70) with a real collective
-    (used by the tensor-parallel host tests)."""
+    (used by the tensor-parallel host tests).  kv_write ops update the oracle's
+    copies of the caches in place; `caches_out` (a dict) receives them after the
+    step, for multi-step decode loops."""
     desc = json.loads(desc_json) if isinstance(desc_json, str) else desc_json
     tmeta = {t["name"]: t for t in desc["tensors"]}
     vals: Dict[str, np.ndarray] = {}
@@ -417,6 +437,11 @@ def evaluate(desc_json: str, rows: int, bindings: Dict[str, np.ndarray],
                 r = [moe_experts(x[0], x[1], x[2], int(p.get("experts", 128)), fn == "moe_gate_up")]
             elif fn == "moe_combine":
                 r = [moe_combine(x[0], x[1], x[2])]
+            elif fn == "kv_write":
+                r = [kv_write(x[0], x[1], x[2], x[3], int(p["heads"]), int(p["kv_heads"]), int(p["head_dim"]),
+                              int(p.get("page_size", 16)), int(p.get("kv_layout", 0)))]
+                if caches_out is not None:
+                    caches_out[o["inputs"][2]], caches_out[o["inputs"][3]] = x[2], x[3]
             elif fn == "attn_decode":
                 r = [attn_decode(x[0], x[1], x[2], x[3], x[4], int(p["heads"]), int(p["kv_heads"]),
                                  int(p["head_dim"]), int(p.get("page_size", 16)), int(p.get("kv_layout", 0)))]

@@ -145,6 +145,11 @@ GraphDescription llama_graph(const LlamaShape& s) {
   if (s.decode)
     table = w.tensor("block_table", {T, max_pages}, BatchSemantics::kBatched,
                      TensorRole::kGraphInput, Dtype::kI64);
+  require(!s.kv_write || s.decode || s.num_pages > 0, Errc::ConfigError,
+          "llama: kv_write in prefill needs num_pages (the cache pool size)");
+  std::string slots;
+  if (s.kv_write)
+    slots = w.tensor("slots", {T}, BatchSemantics::kBatched, TensorRole::kGraphInput, Dtype::kI64);
   // Layer l: [rmsnorm (l==0)] qkv -> rope -> attn -> o_proj [-> AllReduce]
   //   -> add_rmsnorm (residual + mlp norm) -> gate_up -> silu_mul -> down
   //   [-> AllReduce] -> add_rmsnorm with layer l+1's attn norm (ElemAdd on the
@@ -164,7 +169,7 @@ GraphDescription llama_graph(const LlamaShape& s) {
     const std::string wgu = moe ? w.weight(p + ".experts.gate_up.w", {El, H, 2 * MI})
                                 : w.weight(p + ".gate_up.w", {H, 2 * I});
     const std::string wd = moe ? w.weight(p + ".experts.down.w", {El, MI, H}) : w.weight(p + ".down.w", {I, H});
-    if (s.decode) {
+    if (s.decode || s.kv_write) {
       const int64_t pages = s.num_pages ? s.num_pages : T * max_pages;
       const std::vector<int64_t> cshape = s.kv_layout == 1 ? std::vector<int64_t>{pages, nkv, s.page_size, hd}
                                                            : std::vector<int64_t>{pages, s.page_size, nkv, hd};
@@ -192,6 +197,16 @@ GraphDescription llama_graph(const LlamaShape& s) {
                mem_cost)
           .attrs.params = {{"heads", double(nq)}, {"kv_heads", double(nkv)},
                            {"head_dim", double(hd)}, {"theta", s.theta}};
+    }
+    if (s.kv_write) {  // this step's rows join the paged cache (decode reads ctx < their position)
+      // a graph output (the graph model allows no dead intermediates); unbound,
+      // it lives in the session arena
+      const std::string wr = w.tensor(p + ".kv_written", {T}, BatchSemantics::kBatched,
+                                      TensorRole::kGraphOutput, Dtype::kI64);
+      w.custom(p + ".kv_write", "kv_write", {qkvr, slots, kc, vc}, {wr}, p + ".attn.kv", ResourceClass::kMemory,
+               CostParams{2.0, nkv * hd * 4.0 / 6.5e6})
+          .attrs.params = {{"heads", double(nq)}, {"kv_heads", double(nkv)}, {"head_dim", double(hd)},
+                           {"page_size", double(s.page_size)}, {"kv_layout", double(s.kv_layout)}};
     }
     if (s.decode) {
       w.custom(p + ".attn", "attn_decode", {qkvr, kc, vc, table, pos}, {ctx}, p + ".attn.core",
@@ -401,6 +416,7 @@ std::string build_json(const std::string& name, const std::string& params_json) 
     s.page_size = geti(p, "page_size", s.page_size);
     s.num_pages = geti(p, "num_pages", s.num_pages);
     s.kv_layout = geti(p, "kv_layout", s.kv_layout);
+    s.kv_write = geti(p, "kv_write", s.kv_write ? 1 : 0) != 0;
     s.experts = geti(p, "experts", s.experts);
     s.topk = geti(p, "topk", s.topk);
     s.moe_inter = geti(p, "moe_inter", s.moe_inter);

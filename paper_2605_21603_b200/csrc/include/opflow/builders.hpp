@@ -48,6 +48,9 @@ struct LlamaShape {
   int64_t page_size = 16;
   int64_t num_pages = 0;     // 0 = tokens * ctx_len / page_size
   int64_t kv_layout = 0;     // decode KV pages: 0 NHD [pages, page, kv, hd]; 1 HND [pages, kv, page, hd]
+  // paged KV-cache writes: every layer stores the rows' roped K / V into their
+  // cache slots (graph input "slots" [T] i64, -1 = skip); prefill needs num_pages
+  bool kv_write = false;
   // Qwen3 options: per-head q/k RMSNorm before RoPE; MoE FFN when experts > 0
   bool qk_norm = false;
   int64_t experts = 0;

@@ -54,3 +54,62 @@ def test_prefill_write_then_decode_matches_causal_attention(cuda, kv_layout, nq,
         full = tb(seqs[b]).float().cpu().numpy()  # the bf16 values the GPU saw
         want = oracle.attn_prefill(full, nq, nkv, hd, L + 1)[-1]
         assert rel_err(got[b], want) < 1e-2, (b, L, rel_err(got[b], want))
+
+
+def test_two_step_decode_loop_through_the_engine(cuda):
+    """A serving loop: two decode steps of llama_decode_graph(kv_write=1) over
+    manager-owned HND page pools.  Step 1 appends each sequence's token to the
+    cache; step 2 attends over it.  Both steps' outputs match the oracle, which
+    carries its own caches across the steps (its kv_write semantics)."""
+    import torch
+    from paper_2605_21603_b200.workloads import llama_inputs
+    B, ctx_max, page, layers = 6, 64, 16, 2
+    shape = dict(layers=layers, tokens=B, hidden=256, heads=4, kv_heads=2, head_dim=128, inter=512,
+                 ctx_len=ctx_max, page_size=page, dtype="bf16", kv_layout=1, kv_write=1, num_pages=40)
+    desc = of.llama_decode_graph(**shape)
+    kv = of.KvCache(layers=layers, pages=40, kv_heads=2, head_dim=128, page_size=page, kv_layout=1)
+    lens = [3, 15, 16, 17, 30, 47]
+    kv.append(list(range(B)), lens)  # prompt pages, filled with random K / V below
+    host = llama_inputs(desc, B, seed=31, ctx_len=8)
+    g = of.build_graph(desc)
+    sess = of.Session(g, of.partition(g, [of.PartitionRule.by_func("attn_decode")]), {"lanes": 3})
+    keep = {}
+    rng = np.random.default_rng(3)
+    for l in range(layers):
+        for w in ("k", "v"):
+            t = kv.cache(l, w)
+            t.copy_(torch.from_numpy(rng.uniform(-1, 1, t.shape).astype(np.float32)).to(torch.bfloat16))
+            keep[f"layer{l}.{w}_cache"] = t
+    for t in g.description["tensors"]:
+        n = t["name"]
+        if t["role"] == "weight" and n not in keep:
+            keep[n] = torch.from_numpy(host[n]).cuda().to(torch.bfloat16)
+    for n, t in keep.items():
+        sess.bind(n, t)
+    out = torch.empty(B, shape["hidden"], dtype=torch.bfloat16, device="cuda")
+    out_name = [t["name"] for t in g.description["tensors"] if t["role"] == "output" and t.get("dtype") != "i64"][0]
+    sess.bind(out_name, out)
+    oracle_caches = {n: v.float().cpu().numpy() for n, v in keep.items() if n.endswith("_cache")}
+    for step in range(2):
+        slots, pos = kv.append(list(range(B)), [1] * B)
+        table, _ = kv.block_table(list(range(B)), ctx_max // page)
+        table = np.where(table < 0, 0, table)
+        x = rng.uniform(-1, 1, (B, shape["hidden"])).astype(np.float32)
+        step_in = {"x": torch.from_numpy(x).cuda().to(torch.bfloat16), "positions": torch.from_numpy(pos).cuda(),
+                   "slots": torch.from_numpy(slots).cuda(), "block_table": torch.from_numpy(table).cuda()}
+        for n, v in step_in.items():
+            keep[n] = v
+            sess.bind(n, v)
+        sess.run({"name": "split_overlap", "n_microbatches": 2, "lane_mode": "ubatch"})
+        torch.cuda.synchronize()
+        ohost = dict(host)
+        ohost.update({n: v for n, v in oracle_caches.items()})
+        ohost.update({"x": step_in["x"].float().cpu().numpy(), "positions": pos, "slots": slots, "block_table": table})
+        for n in ohost:
+            if n.endswith(".w"):
+                ohost[n] = keep[n].float().cpu().numpy()
+        new_caches = {}
+        want = oracle.evaluate(desc, B, ohost, exact=False, caches_out=new_caches)
+        oracle_caches.update(new_caches)
+        err = rel_err(out.float().cpu().numpy(), want[out_name])
+        assert err < 2e-2, (step, err)

@@ -120,6 +120,8 @@ def evaluate(desc_json: str, rows: int, bind: dict) -> dict:
             elif fn == "attn_prefill":
                 r = [_attn_prefill(x[0], int(p["heads"]), int(p["kv_heads"]), int(p["head_dim"]),
                                    int(p["seq_len"]))]
+            elif fn == "kv_write":
+                r = [x[1]]  # the step's own attention reads only earlier positions
             elif fn == "attn_decode":
                 r = [_attn_decode(x[0], bind[o["inputs"][1]], bind[o["inputs"][2]], x[3], x[4],
                                   int(p["heads"]), int(p["kv_heads"]), int(p["head_dim"]),
