@@ -113,3 +113,68 @@ def test_two_step_decode_loop_through_the_engine(cuda):
         oracle_caches.update(new_caches)
         err = rel_err(out.float().cpu().numpy(), want[out_name])
         assert err < 2e-2, (step, err)
+
+
+def test_prefill_then_decode_equals_longer_prefill(cuda):
+    """End to end over every layer: a prefill graph (kv_write=1) fills the
+    paged caches for B prompts of S tokens, then one decode step (kv_write=1)
+    on token S; its output must equal the last row of a plain prefill over the
+    S + 1 tokens (causal attention), layer stack and all."""
+    import torch
+    from paper_2605_21603_b200.workloads import llama_inputs
+    B, S, layers, page, pages = 3, 16, 2, 16, 24
+    base = dict(layers=layers, hidden=256, heads=4, kv_heads=2, head_dim=128, inter=512, dtype="bf16")
+    pre = of.llama_graph(tokens=B * S, seq_len=S, kv_write=1, num_pages=pages, kv_layout=1, page_size=page, **base)
+    dec = of.llama_decode_graph(tokens=B, ctx_len=S + page, page_size=page, kv_layout=1, kv_write=1,
+                                num_pages=pages, **base)
+    full = of.llama_graph(tokens=B * (S + 1), seq_len=S + 1, **base)
+    w = llama_inputs(full, B * (S + 1), seed=41)
+    rng = np.random.default_rng(41)
+    xs = rng.uniform(-1, 1, (B, S + 1, base["hidden"])).astype(np.float32)
+    tb = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().to(torch.bfloat16)
+    kv = of.KvCache(layers=layers, pages=pages, kv_heads=2, head_dim=128, page_size=page, kv_layout=1)
+    keep = []
+
+    def session(desc, binds):
+        g = of.build_graph(desc)
+        sess = of.Session(g, of.partition(g, []), {"lanes": 3})
+        out = None
+        for t in g.description["tensors"]:
+            n = t["name"]
+            if t["role"] == "output":
+                if t.get("dtype") == "i64":
+                    continue
+                out = torch.empty(list(t["shape"]), dtype=torch.bfloat16, device="cuda")
+                sess.bind(n, out)
+            elif n in binds:
+                sess.bind(n, binds[n])
+            elif n.endswith("_cache"):
+                l = int(n.split(".")[0][5:])
+                sess.bind(n, kv.cache(l, "k" if n.endswith("k_cache") else "v"))
+            elif t["role"] == "weight":
+                v = tb(w[n])
+                keep.append(v)
+                sess.bind(n, v)
+        keep.append(binds)
+        return sess, out
+
+    # prefill of the prompts: fills every layer's pages
+    slots, pos = kv.append(list(range(B)), [S] * B)
+    sp, _ = session(pre, {"x": tb(xs[:, :S].reshape(B * S, -1)), "positions": torch.from_numpy(pos).cuda(),
+                          "slots": torch.from_numpy(slots).cuda()})
+    sp.run({"name": "sequential"})
+    # one decode step on token S
+    slots, pos = kv.append(list(range(B)), [1] * B)
+    table, _ = kv.block_table(list(range(B)), (S + page) // page)
+    sd, out = session(dec, {"x": tb(xs[:, S]), "positions": torch.from_numpy(pos).cuda(),
+                            "slots": torch.from_numpy(slots).cuda(),
+                            "block_table": torch.from_numpy(np.where(table < 0, 0, table)).cuda()})
+    sd.run({"name": "split_overlap", "n_microbatches": 2, "lane_mode": "ubatch"})
+    # the same tokens as one causal prefill of S + 1 per sequence
+    sf, ref = session(full, {"x": tb(xs.reshape(B * (S + 1), -1)),
+                             "positions": torch.from_numpy((np.arange(B * (S + 1)) % (S + 1)).astype(np.int64)).cuda()})
+    sf.run({"name": "sequential"})
+    torch.cuda.synchronize()
+    want = ref.float().view(B, S + 1, -1)[:, S].cpu().numpy()
+    err = rel_err(out.float().cpu().numpy(), want)
+    assert err < 2e-2, err
