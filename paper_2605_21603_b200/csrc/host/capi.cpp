@@ -522,7 +522,8 @@ opf_status opf_dry_run(const opf_graph* g, const opf_plan* p, const char* config
     need(p, "plan");
     validate_plan(p->p, g->g);
     auto s = Session::dry(g->g, p->p, parse_config(config), rows);
-    const std::string spec = strategy ? strategy : "{}";
+    // a calibrated auto table resolves without a device; timed auto raises
+    const std::string spec = s->choose(strategy ? strategy : "{}", nullptr);
     auto strat = make_strategy(spec);
     for (int32_t i = 0; i < std::max(1, repeats); ++i) s->plan_only(*strat, "builtin:" + spec);
     if (schedule_json) *schedule_json = dup_string(s->schedule_json());

@@ -833,6 +833,35 @@ void Session::plan_only(Scheduler& strat, const std::string& key) {
   last_ = lookup_or_build(strat, key);
 }
 
+namespace {
+// serialise a parsed spec back to text (plain objects of scalars / arrays)
+std::string dump_json(const json::Value& x) {
+  switch (x.t) {
+    case json::Value::T::Null: return "null";
+    case json::Value::T::Bool: return x.b ? "true" : "false";
+    case json::Value::T::Int: return x.is_neg ? std::to_string(x.i) : std::to_string(x.u);
+    case json::Value::T::Double: {
+      char b[64];
+      std::snprintf(b, sizeof b, "%.17g", x.d);
+      return b;
+    }
+    case json::Value::T::String: return json::quote(x.s);
+    case json::Value::T::Array: {
+      std::string o = "[";
+      for (std::size_t i = 0; i < x.a->size(); ++i) o += (i ? "," : "") + dump_json((*x.a)[i]);
+      return o + "]";
+    }
+    case json::Value::T::Object: {
+      std::string o = "{";
+      for (std::size_t i = 0; i < x.o->size(); ++i)
+        o += (i ? "," : "") + json::quote((*x.o)[i].first) + ":" + dump_json((*x.o)[i].second);
+      return o + "}";
+    }
+  }
+  return "null";
+}
+}  // namespace
+
 std::string Session::choose(const std::string& spec, cudaStream_t stream) {
   json::Value v;
   try {
@@ -842,40 +871,43 @@ std::string Session::choose(const std::string& spec, cudaStream_t stream) {
   }
   const json::Value* name = v.get("name");
   if (!name || name->t != json::Value::T::String || name->str() != "auto") return spec;
-  const json::Value* cands = v.get("candidates");
-  require(cands && cands->t == json::Value::T::Array && !cands->arr().empty(), Errc::ConfigError,
-          "auto strategy needs a non-empty 'candidates' list");
   const std::string key = spec + "|rows=" + std::to_string(rows());
   auto hit = auto_choice_.find(key);
   if (hit != auto_choice_.end()) return hit->second;
-  require(!dry_, Errc::EngineStopped, "auto strategy selection needs a device session");
-  const int reps = v.get("reps") ? static_cast<int>(v.get("reps")->as_i64()) : 5;
-  // serialise candidate specs back to text (they are plain objects of scalars / arrays)
-  std::function<std::string(const json::Value&)> dump = [&](const json::Value& x) -> std::string {
-    switch (x.t) {
-      case json::Value::T::Null: return "null";
-      case json::Value::T::Bool: return x.b ? "true" : "false";
-      case json::Value::T::Int: return x.is_neg ? std::to_string(x.i) : std::to_string(x.u);
-      case json::Value::T::Double: {
-        char b[64];
-        std::snprintf(b, sizeof b, "%.17g", x.d);
-        return b;
-      }
-      case json::Value::T::String: return json::quote(x.s);
-      case json::Value::T::Array: {
-        std::string o = "[";
-        for (std::size_t i = 0; i < x.a->size(); ++i) o += (i ? "," : "") + dump((*x.a)[i]);
-        return o + "]";
-      }
-      case json::Value::T::Object: {
-        std::string o = "{";
-        for (std::size_t i = 0; i < x.o->size(); ++i)
-          o += (i ? "," : "") + json::quote((*x.o)[i].first) + ":" + dump((*x.o)[i].second);
-        return o + "}";
+  // Calibrated form: {"name":"auto","table":[{"min_rows":R,"strategy":{...}},...]}
+  // — a rows -> strategy decision table fitted offline from device timings
+  // (selector.py): the entry with the largest min_rows <= rows
+  // wins, no timing at run time, one cached CUDA graph per decision.
+  if (const json::Value* table = v.get("table")) {
+    require(table->t == json::Value::T::Array && !table->arr().empty(), Errc::ConfigError,
+            "auto table must be a non-empty list");
+    const json::Value* pick = nullptr;
+    int64_t pick_min = -1;
+    for (const json::Value& e : table->arr()) {
+      const json::Value* mr = e.get("min_rows");
+      const json::Value* st = e.get("strategy");
+      require(mr && st && st->t == json::Value::T::Object, Errc::ConfigError,
+              "auto table entries need 'min_rows' and a 'strategy' object");
+      const int64_t m = mr->as_i64();
+      require(m >= 0, Errc::ConfigError, "auto table: min_rows must be >= 0");
+      if (m <= rows() && m > pick_min) {
+        pick = st;
+        pick_min = m;
       }
     }
-    return "null";
-  };
+    require(pick != nullptr, Errc::ConfigError,
+            "auto table has no entry for rows=" + std::to_string(rows()) + " (add min_rows 0)");
+    const std::string chosen = dump_json(*pick);
+    auto_choice_[key] = chosen;
+    auto_times_[key] = {};
+    return chosen;
+  }
+  const json::Value* cands = v.get("candidates");
+  require(cands && cands->t == json::Value::T::Array && !cands->arr().empty(), Errc::ConfigError,
+          "auto strategy needs a non-empty 'candidates' list (or a 'table')");
+  require(!dry_, Errc::EngineStopped, "auto strategy selection needs a device session");
+  const int reps = v.get("reps") ? static_cast<int>(v.get("reps")->as_i64()) : 5;
+  const auto dump = dump_json;
   cudaEvent_t e0, e1;
   OPF_CUDA(cudaEventCreate(&e0));
   OPF_CUDA(cudaEventCreate(&e1));
