@@ -156,6 +156,9 @@ opf_status opf_comm_window_open(opf_comm* c, const uint8_t* handles);
 /* `world` virtual ranks sharing one device (tests of the peer-memory protocol). */
 opf_status opf_comm_create_virtual(int32_t world, int32_t device, size_t stage_bytes, opf_comm** outs);
 opf_status opf_comm_window_error(opf_comm* c, uint32_t* err);
+/* Fused GEMM -> all-reduce calls that ran the peer-memory push protocol on
+ * this rank (matmul_allreduce_add_rmsnorm; 0 = every call took the fallback). */
+opf_status opf_comm_push_calls(opf_comm* c, uint32_t* calls);
 
 /* ---------------------------------------------------------------- sessions */
 typedef struct opf_session opf_session;

@@ -86,6 +86,7 @@ _SIGS = {
     "opf_comm_window_open": (C.c_int32, [C.c_void_p, C.POINTER(C.c_uint8)]),
     "opf_comm_create_virtual": (C.c_int32, [C.c_int32, C.c_int32, C.c_size_t, C.POINTER(C.c_void_p)]),
     "opf_comm_window_error": (C.c_int32, [C.c_void_p, C.POINTER(C.c_uint32)]),
+    "opf_comm_push_calls": (C.c_int32, [C.c_void_p, C.POINTER(C.c_uint32)]),
     "opf_launch_comm": (C.c_int32, [C.c_char_p, C.POINTER(opf_view), C.c_int32, C.POINTER(opf_view),
                                     C.c_int32, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p]),
     "opf_session_create": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_void_p,

@@ -399,6 +399,13 @@ opf_status opf_comm_window_error(opf_comm* c, uint32_t* err) {
   });
 }
 
+opf_status opf_comm_push_calls(opf_comm* c, uint32_t* calls) {
+  return guard([&] {
+    need(c, "comm");
+    *calls = comm_push_calls(c);
+  });
+}
+
 // ------------------------------------------------------------------ sessions
 opf_status opf_session_create(const opf_graph* g, const opf_plan* p, const char* config,
                               opf_comm* comm, opf_session** out) {

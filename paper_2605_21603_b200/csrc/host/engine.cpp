@@ -553,6 +553,12 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
               "replacement '" + d.replace_fn + "' takes " + std::to_string(e->n_in) + "->" +
                   std::to_string(e->n_out) + " tensors, fused subgraphs expose " +
                   std::to_string(l.in.size()) + "->" + std::to_string(l.out.size()));
+      if (e->prepack_input >= 0 && e->prepack_input < static_cast<int>(b_in.size()) &&
+          g_.tensors[b_in[e->prepack_input]].role == TensorRole::kWeight &&
+          g_.tensors[b_in[e->prepack_input]].dtype == Dtype::kBF16) {
+        l.prepacked = b_in[e->prepack_input];  // e.g. the GEMM weight of matmul_allreduce_add_rmsnorm
+        l.prepack_mode = e->prepack_mode;
+      }
       pd.launches.push_back(std::move(l));
       plan_ws(pd.launches.back());
     } else {
@@ -1071,6 +1077,7 @@ std::string Session::schedule_json() const {
       s += "{\"name\":" + json::quote(l.name) + ",\"op\":" + std::to_string(l.op) +
            ",\"copy\":" + (l.is_copy ? "true" : "false") + ",\"rows\":" + std::to_string(l.rows) +
            ",\"ws_off\":" + std::to_string(l.ws_off) + ",\"ws_bytes\":" + std::to_string(l.ws_bytes) +
+           ",\"prepacked\":" + std::to_string(l.prepacked) +
            ",\"in\":" + views(l.in) + ",\"out\":" + views(l.out) + "}";
     }
     s += "]}";

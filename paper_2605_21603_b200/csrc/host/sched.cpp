@@ -228,6 +228,7 @@ struct StrategyParams {
   std::string replace_fn;         // fuse_norm_comm replacement name ("" = auto)
   std::vector<std::string> merged_labels = {"*.attn"};  // dbo: executed merged
   std::vector<int> lane_budget;   // per-lane SM budgets
+  bool fuse_gemm = false;         // fuse_norm_comm: fold the producing row-parallel MatMul in too
   std::string raw;
 };
 
@@ -257,6 +258,7 @@ StrategyParams parse_spec(const std::string& text) {
     if (const json::Value* c = x->get("network")) p.lane_of[2] = static_cast<int32_t>(c->as_i64());
   }
   if (const json::Value* x = v.get("replace_fn")) p.replace_fn = x->str();
+  if (const json::Value* x = v.get("fuse_gemm")) p.fuse_gemm = x->t == json::Value::T::Bool ? x->b : x->as_i64() != 0;
   if (const json::Value* x = v.get("lane_sm_budget"))
     for (const json::Value& e : x->arr()) p.lane_budget.push_back(static_cast<int>(e.as_i64()));
   if (const json::Value* x = v.get("merged")) {
@@ -427,6 +429,25 @@ class FuseNormComm final : public Scheduler {
     std::vector<bool> is_second(plan.size(), false);
     for (int32_t s = 0; s < static_cast<int32_t>(plan.size()); ++s)
       if (pair[s] >= 0) is_second[pair[s]] = true;
+    // fuse_gemm: a single-MatMul subgraph whose only successor is the AllReduce
+    // of an (AllReduce, add_rmsnorm) pair joins it — the row-parallel GEMM's
+    // epilogue then pushes its partial to the owner ranks while later tiles
+    // compute (matmul_allreduce_add_rmsnorm).  Isolate those MatMuls with
+    // rules, e.g. by_module("layer*.attn.o"), by_module("layer*.mlp.down").
+    std::vector<int32_t> gemm_of(plan.size(), -1);  // AR subgraph -> its MatMul subgraph
+    std::vector<int32_t> ar_of(plan.size(), -1);    // MatMul subgraph -> its AR subgraph
+    if (p_.fuse_gemm)
+      for (int32_t s = 0; s < static_cast<int32_t>(plan.size()); ++s) {
+        if (pair[s] < 0 || fn[s] != "allreduce_add_rmsnorm" || plan.sg_pred[s].size() != 1) continue;
+        const int32_t m = plan.sg_pred[s][0];
+        const Subgraph& ms = plan.subgraphs[m];
+        if (ms.ops.size() != 1 || plan.sg_succ[m].size() != 1) continue;
+        const OperatorNode& mop = g.ops[ms.ops[0]];
+        if (mop.kind != OperatorKind::kMatMul || g.ops[plan.subgraphs[s].ops[0]].inputs[0] != mop.outputs[0]) continue;
+        gemm_of[s] = m;
+        ar_of[m] = s;
+        fn[s] = p_.replace_fn.empty() ? "matmul_allreduce_add_rmsnorm" : p_.replace_fn;
+      }
     const bool split = !(ctx.rows() < p_.threshold || ctx.rows() < 2 * p_.align);
     if (split) {
       StrategyParams two = p_;
@@ -439,7 +460,12 @@ class FuseNormComm final : public Scheduler {
       for (int32_t u = 0; u < U; ++u) {
         for (const OpHandle& h : ctx.get_ready_ops(u)) {
           if (is_second[h.subgraph]) continue;  // dispatched with its AllReduce
-          if (pair[h.subgraph] >= 0) {
+          if (ar_of[h.subgraph] >= 0) {         // MatMul -> AllReduce -> add_rmsnorm as one op
+            const int32_t a = ar_of[h.subgraph];
+            ctx.execute({h, ctx.handle(a, u), ctx.handle(pair[a], u)}, net, fn[a]);
+          } else if (gemm_of[h.subgraph] >= 0) {
+            continue;  // dispatched with its MatMul
+          } else if (pair[h.subgraph] >= 0) {
             ctx.execute({h, ctx.handle(pair[h.subgraph], u)}, net, fn[h.subgraph]);
           } else {
             ctx.execute({h}, lane_for(p_, ctx, h.subgraph, u));

@@ -135,6 +135,18 @@ struct GemmArgs {
   size_t ws_bytes;
 };
 void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s);
+// Push epilogue (row-parallel GEMM -> all-reduce over peer memory): output row
+// r of this rank's partial belongs to owner q = r / blk; the 32-row slab is
+// stored at dst[q] + (r - q*blk) * N (this rank's slot in q's window) and
+// counted in q's cnt[(r - q*blk) / 32] (red.release.sys) once written.
+struct PushArgs {
+  void* dst[8];
+  uint32_t* cnt[8];
+  uint32_t* epoch;  // my call epoch (CTA 0 bumps it; the reduce kernel reads it)
+  int64_t blk;
+  int world;
+};
+void gemm_bf16_push(const GemmArgs& g, const PushArgs& p, cudaStream_t s);
 // K splits the 2-CTA kernel uses for an (m, n, k) launch on `max_ctas` SMs
 // (1 = none) and the workspace they need (fp32 partials + tile semaphores).
 int gemm_splitk_splits(int64_t m, int64_t n, int64_t k, int max_ctas);

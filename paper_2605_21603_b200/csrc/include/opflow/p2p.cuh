@@ -29,11 +29,24 @@ struct PeerPtrs {
   uint32_t* flags[kMaxWorld];  // flag array of each rank [kMaxCtas][kMaxWorld]
 };
 
+// GEMM -> all-reduce push protocol (gemm_ar_push: the row-parallel GEMM's
+// epilogue stores each 32-row slab of its partial straight into the owner
+// rank's window): per-slab arrival counters, per-slab publish epochs and one
+// call epoch, after the error flag.
+constexpr int kMaxSlabs = 4096;  // 32-row slabs per owner block (blk <= 131072 rows)
+
 inline size_t window_layout(size_t stage_bytes, size_t* flags_off, size_t* epoch_off) {
   const size_t s = (stage_bytes + 255) / 256 * 256;
   *flags_off = s;
   *epoch_off = s + sizeof(uint32_t) * kMaxCtas * kMaxWorld;
-  return *epoch_off + sizeof(uint32_t) * kMaxCtas + sizeof(uint32_t) /*error flag*/;
+  return *epoch_off + sizeof(uint32_t) * kMaxCtas + sizeof(uint32_t) /*error flag*/ +
+         sizeof(uint32_t) * (2 * kMaxSlabs + 1) /*push counters, publish epochs, call epoch*/;
+}
+// offset of the push area: [cnt kMaxSlabs | pub kMaxSlabs | call epoch]
+inline size_t window_push_off(size_t stage_bytes) {
+  size_t fo, eo;
+  window_layout(stage_bytes, &fo, &eo);
+  return eo + sizeof(uint32_t) * kMaxCtas + sizeof(uint32_t);
 }
 
 // Host: peer pointers + my epochs / error flag of a windowed communicator.

@@ -26,6 +26,8 @@ namespace opflow {
 bool ar_add_rmsnorm_p2p(const opf_comm* c, const opf_view& o, const opf_view& x, const opf_view& g,
                         opf_view& x_out, opf_view& y, int64_t rows, float eps, int max_ctas, int mode,
                         cudaStream_t s);
+bool gemm_ar_add_rmsnorm_push(const opf_comm* c, const GemmArgs& g, const opf_view& x, const opf_view& gam,
+                              opf_view& x_out, opf_view& y, float eps, cudaStream_t s);
 
 namespace {
 
@@ -233,11 +235,66 @@ opf_status op_ar_add_rmsnorm(const opf_op_ctx* c, const opf_view* in, int32_t n_
   return op_error(Errc::ShapeMismatch, "allreduce_add_rmsnorm: dtype");
 }
 
+// matmul_allreduce_add_rmsnorm (a, w, x, g) -> (x1, y): the row-parallel
+// projection (o_proj / down) + its AllReduce + the residual add + RMSNorm as
+// ONE op (the fuse_norm_comm strategy with "fuse_gemm": 1).  With a peer
+// window the GEMM epilogue pushes partial slabs to their owner ranks over
+// NVLink while later tiles compute, and one kernel reduces, normalises and
+// gathers (gemm_ar_add_rmsnorm_p2p in comm_p2p.cu).  Otherwise: GEMM into the
+// workspace, then the allreduce_add_rmsnorm path on it.
+size_t ws_mm_ar(const opf_op_ctx& c, const opf_view* in, int n_in, const opf_view* out, int n_out, int64_t rows) {
+  if (n_in != 4 || n_out != 2) return 0;
+  const size_t o_bytes = (static_cast<size_t>(rows * view_row_elems(out[0]) * 2) + 255) / 256 * 256;
+  opf_view o = out[0];
+  return o_bytes + ws_ar(c, &o, 1, nullptr, 0, rows);
+}
+
+opf_status op_mm_ar_add_rmsnorm(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out,
+                                int32_t n_out, int64_t rows, void* stream) {
+  if (n_in != 4 || n_out != 2)
+    return op_error(Errc::SignatureMismatch, "matmul_allreduce_add_rmsnorm takes (a, w, x, g) -> (x1, y)");
+  if (rows == 0) return 0;
+  auto s = static_cast<cudaStream_t>(stream);
+  const int64_t K = view_row_elems(in[0]), N = view_row_elems(out[0]);
+  if (in[0].dtype != OPF_BF16 || in[1].dtype != OPF_BF16 || in[1].shape[0] != K || in[1].shape[1] != N)
+    return op_error(Errc::ShapeMismatch, "matmul_allreduce_add_rmsnorm: bf16 a [rows,K] and w [K,N]");
+  if (!c->aux) return op_error(Errc::ShapeMismatch, "matmul_allreduce_add_rmsnorm needs the packed weight");
+  const opf_comm* comm = static_cast<const opf_comm*>(c->comm);
+  const float eps = static_cast<float>(ctx_param(*c, "eps", 1e-5));
+  GemmArgs g{};
+  g.a = view_ptr(in[0]);
+  g.bt = c->aux;
+  g.m = rows;
+  g.n = N;
+  g.k = K;
+  g.lda = K;
+  g.ldc = N;
+  g.max_ctas = c->max_ctas;
+  if (comm && comm->world > 1 && !comm->peer_buf.empty() && ctx_param(*c, "push", 1.0) != 0.0 &&
+      gemm_ar_add_rmsnorm_push(comm, g, in[2], in[3], out[0], out[1], eps, s))
+    return launch_status("matmul_allreduce_add_rmsnorm_push");
+  // unfused fallback: partial product in the workspace, then the fused AR + add + norm
+  const size_t o_bytes = (static_cast<size_t>(rows * N * 2) + 255) / 256 * 256;
+  if (!c->workspace || c->workspace_bytes < o_bytes)
+    return op_error(Errc::ShapeMismatch, "matmul_allreduce_add_rmsnorm: workspace too small");
+  g.c = c->workspace;
+  gemm_bf16_tc(g, s);
+  opf_view o = make_view(c->workspace, 0, Dtype::kBF16, {rows, N}, true);
+  opf_op_ctx c2 = *c;
+  c2.workspace = static_cast<char*>(c->workspace) + o_bytes;
+  c2.workspace_bytes = c->workspace_bytes - o_bytes;
+  opf_view ins[3] = {o, in[2], in[3]};
+  return op_ar_add_rmsnorm(&c2, ins, 3, out, 2, rows, stream);
+}
+
 }  // namespace
 
 void register_comm_ops(OpRegistry& r) {
   r.add({"allreduce_rowscale", op_ar_rowscale, ResourceClass::kNetwork, 1, 1, ws_ar});
   r.add({"allreduce_add_rmsnorm", op_ar_add_rmsnorm, ResourceClass::kNetwork, 3, 2, ws_ar});
+  OpEntry mm{"matmul_allreduce_add_rmsnorm", op_mm_ar_add_rmsnorm, ResourceClass::kNetwork, 4, 2, ws_mm_ar};
+  mm.prepack_input = 1;  // [K,N] weight -> K-major [N,K] (tcgen05 B operand)
+  r.add(mm);
 }
 
 }  // namespace opflow

@@ -229,6 +229,164 @@ __global__ void __launch_bounds__(kThreads) allreduce_p2p_kernel(
 }
 
 
+// GEMM -> all-reduce -> residual add -> RMSNorm with the transfer inside the
+// GEMM (gemm_ar_add_rmsnorm_push).  The row-parallel GEMM of every rank pushed
+// its partial rows into the owner's window (rank q owns rows [q*blk,(q+1)*blk),
+// slot p = rank p's partial) and counted each 32-row slab in the owner's
+// cnt[slab]; this kernel, on every rank:
+//   1. per slab of MY block: wait cnt == world x n_tiles, sum the world slots
+//      (local HBM), add the residual, write x1 (local output + my window's x1
+//      plane) and h = rmsnorm(x1) * g; reset cnt, publish pub[slab] = epoch;
+//   2. per 8-row quarter of every OTHER owner's slab: wait that owner's
+//      pub[slab] >= epoch, pull x1 over NVLink, normalise locally.
+// NVLink bytes per rank: (W-1)/W of the partial pushed during the GEMM plus
+// (W-1)/W of x1 pulled here — one all-reduce's worth, the first half hidden
+// under the GEMM's math.  Flow control needs no extra barrier: a rank pushes
+// call k+1's partials only after its call-k kernel finished gathering from
+// every owner, i.e. after every owner reset its counters and published.
+__global__ void __launch_bounds__(kThreads) push_reduce_norm_kernel(
+    PeerPtrs pp, int world, int rank, unsigned long long push_off, const __nv_bfloat16* __restrict__ resid,
+    const __nv_bfloat16* __restrict__ gamma, __nv_bfloat16* __restrict__ x_out, __nv_bfloat16* __restrict__ y,
+    int64_t rows, int64_t H, float eps, int n_tiles, uint32_t* err) {
+  extern __shared__ float rowbuf[];
+  __shared__ float red[kThreads / 32];
+  __shared__ uint32_t ok;
+  const int64_t n8 = H / 8;
+  const int64_t blk = rows / world, slabs = blk / 32, plane = rows * H;
+  char* mine = const_cast<char*>(static_cast<const char*>(pp.buf[rank]));
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(mine + push_off);
+  uint32_t* pub = cnt + kMaxSlabs;
+  const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(cnt + 2 * kMaxSlabs);
+  const __nv_bfloat16* part = reinterpret_cast<const __nv_bfloat16*>(mine);
+  __nv_bfloat16* x1w = reinterpret_cast<__nv_bfloat16*>(mine) + plane;
+  // one row: v[c] = x1 (bf16-rounded) from `src8` (+ partial slots when reducing); y = rmsnorm(v) * g
+  auto norm_row = [&](int64_t r) {
+    float ss = 0.0f;
+    for (int64_t c = threadIdx.x; c < n8; c += kThreads) {
+      const float* v = rowbuf + c * 8;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss += v[e] * v[e];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = ss;
+    __syncthreads();
+    float tot = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) tot += red[w];
+    const float inv = rsqrtf(tot / static_cast<float>(H) + eps);
+    for (int64_t c = threadIdx.x; c < n8; c += kThreads) {
+      const uint4 gu = reinterpret_cast<const uint4*>(gamma)[c];
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gu);
+      uint4 o;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 gf = __bfloat1622float2(g2[e]);
+        o2[e] = __floats2bfloat162_rn(rowbuf[c * 8 + 2 * e] * inv * gf.x, rowbuf[c * 8 + 2 * e + 1] * inv * gf.y);
+      }
+      reinterpret_cast<uint4*>(y + r * H)[c] = o;
+    }
+    __syncthreads();  // rowbuf / red reused by the next row
+  };
+  // 1. reduce my block
+  for (int64_t s = blockIdx.x; s < slabs; s += gridDim.x) {
+    if (threadIdx.x == 0) {
+      ok = 1;
+      const uint32_t need = static_cast<uint32_t>(world * n_tiles);
+      int64_t spins = 0;
+      while (ld_acquire_sys(cnt + s) < need)
+        if (++spins > kSpinLimit) {
+          atomicExch(err, 1u);
+          ok = 0;
+          break;
+        }
+    }
+    __syncthreads();
+    if (!ok) return;
+    for (int rr = 0; rr < 32; ++rr) {
+      const int64_t lr = s * 32 + rr, r = rank * blk + lr;
+      for (int64_t c = threadIdx.x; c < n8; c += kThreads) {
+        float acc[8];
+        const uint4 u = reinterpret_cast<const uint4*>(resid + r * H)[c];
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h2[e]);
+          acc[2 * e] = f.x;
+          acc[2 * e + 1] = f.y;
+        }
+        for (int p = 0; p < world; ++p) {
+          const uint4 pu = reinterpret_cast<const uint4*>(part + (p * blk + lr) * H)[c];
+          const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&pu);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(p2[e]);
+            acc[2 * e] += f.x;
+            acc[2 * e + 1] += f.y;
+          }
+        }
+        uint4 o;
+        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          o2[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+          const float2 f = __bfloat1622float2(o2[e]);
+          rowbuf[c * 8 + 2 * e] = f.x;
+          rowbuf[c * 8 + 2 * e + 1] = f.y;
+        }
+        reinterpret_cast<uint4*>(x_out + r * H)[c] = o;
+        reinterpret_cast<uint4*>(x1w + r * H)[c] = o;
+      }
+      norm_row(r);
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      cnt[s] = 0;  // every partial of this slab is consumed
+      __threadfence_system();
+      st_release_sys(pub + s, epoch);
+    }
+  }
+  // 2. gather the other owners' x1 rows (8-row quarters of their slabs)
+  const int64_t units = static_cast<int64_t>(world - 1) * slabs * 4;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int qi = static_cast<int>(u / (slabs * 4));
+    const int q = qi < rank ? qi : qi + 1;
+    const int64_t s = (u % (slabs * 4)) / 4, qu = u % 4;
+    const char* theirs = static_cast<const char*>(pp.buf[q]);
+    if (threadIdx.x == 0) {
+      ok = 1;
+      const uint32_t* qpub = reinterpret_cast<const uint32_t*>(theirs + push_off) + kMaxSlabs;
+      int64_t spins = 0;
+      while (static_cast<int32_t>(ld_acquire_sys(qpub + s) - epoch) < 0)
+        if (++spins > kSpinLimit) {
+          atomicExch(err, 1u);
+          ok = 0;
+          break;
+        }
+    }
+    __syncthreads();
+    if (!ok) return;
+    const __nv_bfloat16* qx1 = reinterpret_cast<const __nv_bfloat16*>(theirs) + plane;
+    for (int rr = 0; rr < 8; ++rr) {
+      const int64_t r = q * blk + s * 32 + qu * 8 + rr;
+      for (int64_t c = threadIdx.x; c < n8; c += kThreads) {
+        const uint4 u4 = reinterpret_cast<const uint4*>(qx1 + r * H)[c];
+        reinterpret_cast<uint4*>(x_out + r * H)[c] = u4;
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u4);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h2[e]);
+          rowbuf[c * 8 + 2 * e] = f.x;
+          rowbuf[c * 8 + 2 * e + 1] = f.y;
+        }
+      }
+      norm_row(r);
+    }
+  }
+}
+
 }  // namespace
 
 // ----------------------------------------------------------------- window API
@@ -288,6 +446,15 @@ uint32_t comm_window_error(const opf_comm* c) {
   window_layout(c->peer_bytes, &fo, &eo);
   uint32_t e = 0;
   OPF_CUDA(cudaMemcpy(&e, static_cast<char*>(c->window_base) + eo + sizeof(uint32_t) * kMaxCtas,
+                      sizeof(e), cudaMemcpyDeviceToHost));
+  return e;
+}
+
+uint32_t comm_push_calls(const opf_comm* c) {
+  if (!c || !c->window_base) return 0;
+  uint32_t e = 0;
+  OPF_CUDA(cudaMemcpy(&e, static_cast<char*>(c->window_base) + window_push_off(c->peer_bytes) +
+                              sizeof(uint32_t) * 2 * kMaxSlabs,
                       sizeof(e), cudaMemcpyDeviceToHost));
   return e;
 }
@@ -356,6 +523,41 @@ bool allreduce_p2p(const opf_comm* c, const opf_view& in, opf_view& out, int64_t
       pp, c->world, c->rank, vptr<__nv_bfloat16>(in), reinterpret_cast<__nv_bfloat16*>(base),
       reinterpret_cast<uint32_t*>(base + eo), vptr<__nv_bfloat16>(out), rows, H,
       reinterpret_cast<uint32_t*>(base + eo + sizeof(uint32_t) * kMaxCtas));
+  return true;
+}
+
+bool gemm_ar_add_rmsnorm_push(const opf_comm* c, const GemmArgs& g, const opf_view& x, const opf_view& gam,
+                              opf_view& x_out, opf_view& y, float eps, cudaStream_t s) {
+  if (!c || c->peer_buf.empty() || c->world < 2) return false;
+  const int W = c->world;
+  const int64_t rows = g.m, H = g.n;
+  if (rows % (32 * W) || H % 256 || rows <= 128 || H * 4 > 48 * 1024 || x.dtype != OPF_BF16) return false;
+  if (static_cast<size_t>(2 * rows * H * 2) > c->peer_bytes) return false;  // partials + x1 planes
+  const int64_t blk = rows / W;
+  if (blk / 32 > kMaxSlabs) return false;
+  const size_t push_off = window_push_off(c->peer_bytes);
+  PushArgs p{};
+  PeerPtrs pp{};
+  for (int q = 0; q < W; ++q) {
+    char* base = static_cast<char*>(c->peer_buf[q]);
+    p.dst[q] = base + static_cast<size_t>(c->rank) * blk * H * 2;
+    p.cnt[q] = reinterpret_cast<uint32_t*>(base + push_off);
+    pp.buf[q] = base;
+    pp.flags[q] = c->peer_flag[q];
+  }
+  p.epoch = reinterpret_cast<uint32_t*>(static_cast<char*>(c->window_base) + push_off) + 2 * kMaxSlabs;
+  p.blk = blk;
+  p.world = W;
+  gemm_bf16_push(g, p, s);
+  size_t fo, eo;
+  window_layout(c->peer_bytes, &fo, &eo);
+  const int64_t slabs = blk / 32;
+  int grid = g.max_ctas > 0 ? g.max_ctas : num_sms();
+  grid = static_cast<int>(std::min<int64_t>(grid, std::max<int64_t>(slabs, (W - 1) * slabs * 4)));
+  push_reduce_norm_kernel<<<std::max(grid, 1), kThreads, H * sizeof(float), s>>>(
+      pp, W, c->rank, static_cast<unsigned long long>(push_off), vptr<__nv_bfloat16>(x), vptr<__nv_bfloat16>(gam),
+      vptr<__nv_bfloat16>(x_out), vptr<__nv_bfloat16>(y), rows, H, eps, static_cast<int>(H / 256),
+      reinterpret_cast<uint32_t*>(static_cast<char*>(c->window_base) + eo + sizeof(uint32_t) * kMaxCtas));
   return true;
 }
 

@@ -721,13 +721,62 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
 // expert) x n_tiles] with 256-row tiles; N is the per-expert width, expert e's
 // B rows start at e * N; rows of a tile past row_end belong to the next
 // expert's tile (computed, never stored).
+// Push epilogue (EPI 3): the 32-row slab of this warp goes straight into the
+// owner rank's window (row r -> owner r / blk, this rank's slot there), 64
+// columns at a time through the swizzled staging buffer so every store
+// instruction writes 4 rows x 128 contiguous bytes (NVLink-friendly), then one
+// system-scope release increment of the owner's slab counter per tile.  Never
+// waits on a peer: the reduce side does all the waiting.
+template <int TN, typename Release>
+__device__ __forceinline__ void store_tile_push(uint32_t tmem_col0, uint8_t* sbuf, int lane, int64_t nb, int64_t row0,
+                                                int64_t M, int64_t N, const PushArgs& pa, Release&& release) {
+  const int q = static_cast<int>(row0 / pa.blk);
+  const int64_t lr = row0 - q * pa.blk;
+  __nv_bfloat16* dst = row0 < M ? static_cast<__nv_bfloat16*>(pa.dst[q]) + lr * N + nb * TN : nullptr;
+#pragma unroll 1
+  for (int chunk = 0; chunk < TN / 64; ++chunk) {
+    uint32_t v0[32], v1[32];
+    const uint32_t taddr = tmem_col0 + static_cast<uint32_t>(chunk * 64);
+    tmem_ld32(taddr, v0);
+    tmem_ld32(taddr + 32, v1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (chunk == TN / 64 - 1) release();  // accumulator fully read
+    __syncwarp();  // the previous chunk's read-back of sbuf is done
+    const int r = lane;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t* src = j < 4 ? &v0[8 * j] : &v1[8 * (j - 4)];
+      uint4 u;
+      u.x = pack_bf16(src[0], src[1]);
+      u.y = pack_bf16(src[2], src[3]);
+      u.z = pack_bf16(src[4], src[5]);
+      u.w = pack_bf16(src[6], src[7]);
+      *reinterpret_cast<uint4*>(sbuf + r * 128 + ((j ^ (r & 7)) * 16)) = u;
+    }
+    __syncwarp();
+    if (dst) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int row = i * 4 + lane / 8, j = lane % 8;
+        const uint4 u = *reinterpret_cast<const uint4*>(sbuf + row * 128 + ((j ^ (row & 7)) * 16));
+        *reinterpret_cast<uint4*>(dst + row * N + chunk * 64 + j * 8) = u;
+      }
+    }
+  }
+  if (!dst) return;
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0)
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(pa.cnt[q] + lr / 32), "r"(1u) : "memory");
+}
+
 template <int EPI, int TN, bool SPLIT = false, bool GROUPED = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K, int splits,
                     float4* __restrict__ ws, int* __restrict__ sem, RopeArgs rope,
-                    const int32_t* __restrict__ gtab = nullptr, __nv_bfloat16* __restrict__ c_out = nullptr,
-                    int64_t ldc = 0) {
+                    const int32_t* __restrict__ gtab, __nv_bfloat16* __restrict__ c_out,
+                    int64_t ldc, PushArgs push) {
   using C = Tc2Cfg<TN, SPLIT>;
   constexpr int kStages2 = C::kStages;
   constexpr uint32_t kStageBytes2 = C::kStageBytes;
@@ -777,6 +826,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
   pdl_wait();     // inputs of the previous kernel on this stream are visible from here
   pdl_trigger();  // persistent grid: let the next kernel stage its prologue on freed SMs
   if constexpr (GROUPED) m_blocks = *reinterpret_cast<const volatile int32_t*>(gtab);  // routing kernel output
+  if constexpr (EPI == 3)  // one new push call: the reduce kernel that follows waits for this epoch's publishes
+    if (blockIdx.x == 0 && threadIdx.x == 0) *push.epoch += 1;
   const int64_t tiles = m_blocks * n_blocks;
   const int64_t units = tiles * splits;  // unit u = split (u % splits) of tile (u / splits)
 
@@ -877,6 +928,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
         else
           store_tile_direct<EPI>(tcol, c_out, ldc, row0 + lane, row_end, nb);
         release();
+      } else if constexpr (EPI == 3) {
+        store_tile_push<TN>(tcol, stg[0], lane, nb, row0, M, N, push, release);
       } else if constexpr (SPLIT && TN == 256) {
         store_tile_splitk<EPI>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, static_cast<int>(rank) * 8 + ew, t,
                                static_cast<int>(u % splits), splits, ws, sem, release);
@@ -1015,6 +1068,7 @@ size_t gemm_splitk_workspace(int64_t m, int64_t n, int64_t k, int max_ctas) {
 
 constexpr const int32_t* kNoGtab = nullptr;
 constexpr __nv_bfloat16* kNoOut = nullptr;
+constexpr PushArgs kNoPush{};
 
 void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
   require(g.k % 8 == 0 && g.lda % 8 == 0 && g.ldc % 8 == 0, Errc::ShapeMismatch,
@@ -1075,25 +1129,25 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     const dim3 blocks(2u * static_cast<unsigned>(std::max(clusters, 1)));
     if (splits > 1 && g.epi == 1)
       launch_pdl(gemm_tc2_kernel<1, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
-                 g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
+                 g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
     else if (splits > 1)
       launch_pdl(gemm_tc2_kernel<0, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
-                 g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
+                 g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
     else if (g.epi == 2)
       launch_pdl(gemm_tc2_kernel<2, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb,
-                 mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
+                 mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
     else if (g.epi == 1)
       launch_pdl(gemm_tc2_kernel<1, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
+                 g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
     else if (tn == 256)
       launch_pdl(gemm_tc2_kernel<0, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
+                 g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
     else if (tn == 192)
       launch_pdl(gemm_tc2_kernel<0, 192>, blocks, dim3(Tc2Cfg<192, false>::kThreads), Tc2Cfg<192, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
+                 g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
     else
       launch_pdl(gemm_tc2_kernel<0, 128>, blocks, dim3(Tc2Cfg<128, false>::kThreads), Tc2Cfg<128, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0});
+                 g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
     return;
   }
   const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN);
@@ -1108,6 +1162,29 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
   else
     launch_pdl(gemm_tc_kernel<0>, dim3(grid), dim3(kThreads), kSmemBytes, s, ma, mb, mc, g.m, g.n, g.k,
                static_cast<const int32_t*>(nullptr), static_cast<__nv_bfloat16*>(nullptr), int64_t{0}, rope);
+}
+
+// Row-parallel GEMM whose epilogue pushes each 32-row slab of the partial
+// product into its owner rank's peer window (EPI 3, store_tile_push).  2-CTA
+// 256x256 tiles only; the caller checks m % (32 * world) == 0 and n % 256 == 0.
+void gemm_bf16_push(const GemmArgs& g, const PushArgs& p, cudaStream_t s) {
+  require(g.k % 8 == 0 && g.lda % 8 == 0 && g.n % 256 == 0 && p.blk % 32 == 0 && g.m > BM, Errc::ShapeMismatch,
+          "push GEMM needs K % 8, N % 256, 32-row owner blocks and M > 128");
+  gemm_bf16_tc_init();
+  static std::once_flag once;
+  std::call_once(once, [] {
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<3, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
+  });
+  const CUtensorMap ma = make_map(g.a, g.k, g.m, g.lda, BK, BM);
+  const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, 128);
+  int grid = num_sms();
+  if (g.max_ctas > 0 && g.max_ctas < grid) grid = g.max_ctas;
+  const int64_t tiles = ((g.m + 2 * BM - 1) / (2 * BM)) * (g.n / 256);
+  const int clusters = static_cast<int>(std::min<int64_t>(tiles, std::max(grid / 2, 1)));
+  launch_pdl(gemm_tc2_kernel<3, 256>, dim3(2u * static_cast<unsigned>(std::max(clusters, 1))),
+             dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, ma, g.m, g.n, g.k, 1,
+             static_cast<float4*>(nullptr), static_cast<int*>(nullptr), RopeArgs{}, kNoGtab, kNoOut, int64_t{0}, p);
 }
 
 // Grouped (per-expert) GEMM: rows of `a` are expert-sorted segments, gtab the
@@ -1142,11 +1219,11 @@ void gemm_bf16_grouped(const GemmArgs& g, const int32_t* gtab, int64_t max_mtile
     if (g.epi == 1)
       launch_pdl(gemm_tc2_kernel<1, 256, false, true>, blocks, dim3(Tc2Cfg<256, false>::kThreads),
                  Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m, group_n, g.k, 1, static_cast<float4*>(nullptr),
-                 static_cast<int*>(nullptr), RopeArgs{}, gtab, c, g.ldc);
+                 static_cast<int*>(nullptr), RopeArgs{}, gtab, c, g.ldc, kNoPush);
     else
       launch_pdl(gemm_tc2_kernel<0, 256, false, true>, blocks, dim3(Tc2Cfg<256, false>::kThreads),
                  Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m, group_n, g.k, 1, static_cast<float4*>(nullptr),
-                 static_cast<int*>(nullptr), RopeArgs{}, gtab, c, g.ldc);
+                 static_cast<int*>(nullptr), RopeArgs{}, gtab, c, g.ldc, kNoPush);
     return;
   }
   const CUtensorMap mb = make_map(g.bt, g.k, group_n * n_groups, g.k, BK, BN);

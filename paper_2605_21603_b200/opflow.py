@@ -546,6 +546,12 @@ class Comm:
         check(lib().opf_comm_window_error(self._h, C.byref(e)))
         return e.value
 
+    def push_calls(self) -> int:
+        """Fused GEMM -> all-reduce calls that used the peer-memory push path."""
+        e = C.c_uint32()
+        check(lib().opf_comm_push_calls(self._h, C.byref(e)))
+        return e.value
+
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value:
             lib().opf_comm_free(self._h)

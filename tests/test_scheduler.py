@@ -260,3 +260,35 @@ def test_schedules_are_race_free():
                   {"name": "fuse_norm_comm", "align": 256}, {"name": "split_overlap", "align": 256}]:
         sched, _ = of.dry_run(g, p, strat)
         assert not find_races(sched)
+
+
+def test_fuse_gemm_folds_row_parallel_matmul_into_the_allreduce():
+    """fuse_norm_comm + fuse_gemm: an isolated o_proj / down MatMul subgraph joins
+    its (AllReduce, add_rmsnorm) pair as ONE matmul_allreduce_add_rmsnorm
+    dispatch (inputs a, w, x, g -> outputs x1, h) on the network lane; without
+    the isolating rules the plan keeps the plain pairs."""
+    desc = of.llama_graph(layers=2, tokens=512, seq_len=128, hidden=1024, heads=16, kv_heads=4, head_dim=64,
+                          inter=2048, tp=2, dtype="bf16")
+    g = of.build_graph(desc)
+    rules = [R.by_module("layer*.attn.o"), R.by_module("layer*.mlp.down"), R.by_func("AllReduce"),
+             R.by_func("add_rmsnorm")]
+    p = of.partition(g, rules)
+    sched, _ = of.dry_run(g, p, {"name": "fuse_norm_comm", "fuse_gemm": 1, "threshold": 1 << 20})
+    fused = [d for d in sched["dispatches"] if d["replace_fn"] == "matmul_allreduce_add_rmsnorm"]
+    assert [[g.ops[o].name for s in d["subgraphs"] for o in p.subgraphs[s].ops] for d in fused] == [
+        ["layer0.o_proj", "layer0.o_allreduce", "layer0.attn_resid_norm"],
+        ["layer0.down", "layer0.down_allreduce", "layer0.mlp_resid_norm"],
+        ["layer1.o_proj", "layer1.o_allreduce", "layer1.attn_resid_norm"]]
+    for d in fused:
+        (l,) = d["launches"]
+        names = [g.tensors[v["tensor"]].name for v in l["in"]]
+        assert names[1].endswith((".o.w", ".down.w")) and names[3].endswith("norm.w"), names
+        assert l["prepacked"] == l["in"][1]["tensor"]  # packed once per binding: K-major tcgen05 B operand
+        assert len(l["out"]) == 2 and d["lane"] == 2
+    # the last layer's down feeds an ElemAdd: plain AllReduce stays
+    assert any(d["replace_fn"] == "" and [g.ops[o].name for s in d["subgraphs"] for o in p.subgraphs[s].ops]
+               == ["layer1.down_allreduce"] for d in sched["dispatches"])
+    # without isolating rules the MatMuls sit inside fillers: pairs only
+    p2 = of.partition(g, [R.by_func("AllReduce"), R.by_func("add_rmsnorm")])
+    s2, _ = of.dry_run(g, p2, {"name": "fuse_norm_comm", "fuse_gemm": 1})
+    assert {d["replace_fn"] for d in s2["dispatches"]} == {"", "allreduce_add_rmsnorm"}
