@@ -325,7 +325,11 @@ def run_ours(args):
     tp = world
     T, S, L = args.tokens, args.seq_len, args.layers
     desc = of.llama_graph(layers=L, tokens=T, seq_len=S, tp=tp, dtype="bf16", **LLAMA)
-    rules = [of.PartitionRule.by_func("AllReduce"), of.PartitionRule.by_func("add_rmsnorm")] if tp > 1 else []
+    # TP: AllReduce / add_rmsnorm subgraphs for TokenWeave, and the row-parallel
+    # o_proj / down MatMuls isolated so fuse_gemm can fold them into the collective
+    R_ = of.PartitionRule
+    rules = [R_.by_module("layer*.attn.o"), R_.by_module("layer*.mlp.down"), R_.by_func("AllReduce"),
+             R_.by_func("add_rmsnorm")] if tp > 1 else []
     g, plan, sess, bufs = build_session(of, desc, rules, dev, comm, seed=1234 + rank)
     pos = (torch.arange(T, device=dev) % S).to(torch.int64)
     bufs["positions"] = pos
@@ -338,6 +342,8 @@ def run_ours(args):
         cands["nanoflow_class"] = {"name": "split_overlap", "n_microbatches": 2, "align": S}
         if tp > 1:
             cands["tokenweave"] = {"name": "fuse_norm_comm", "align": S}
+            if comm_window_ok:  # GEMM epilogue pushes partials to owner ranks (peer window needed)
+                cands["tokenweave_gemm"] = {"name": "fuse_norm_comm", "align": S, "fuse_gemm": 1}
     else:
         for s in args.strategies.split(","):
             cands[s] = json.loads(s) if s.startswith("{") else {"name": s, "align": S}
