@@ -584,6 +584,10 @@ __global__ void __launch_bounds__(128 + NP * 128, 1)
 // covers PV_t,{j-1} (in-order tcgen05 completion), so the softmax may rescale
 // O_t without a separate PV tracker.
 constexpr int kPPThreads = 384;                  // 4 role warps + 2 softmax warpgroups
+#ifndef FA_PP_TURNS
+#define FA_PP_TURNS 1
+#endif
+constexpr bool kPPTurns = FA_PP_TURNS != 0;      // heads alternate the exp phase
 constexpr uint32_t kPPQ = 0;                     // Q0, Q1
 constexpr uint32_t kPPK = 2 * kTile;             // [2 stages]
 constexpr uint32_t kPPV = kPPK + 2 * kTile;      // [2 stages]
@@ -648,7 +652,12 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     hp = static_cast<int>(r % pairs);
     seq = static_cast<int>(r / pairs);
   };
-
+  // Register split (warpgroup granularity): the role warpgroup (TMA, MMA)
+  // shrinks to 56, the two softmax warpgroups grow to 224 so a thread holds
+  // its whole 128-column S row (one TMEM pass, no spills).
+  // 128 x 56 + 256 x 224 = 384 x 168.
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
   if (warp == 0) {
     if (lane == 0) {  // ---------------------------------------------- TMA: Q pair, K tiles
       int stage = 0;
@@ -779,8 +788,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         first_item = false;
       }
     }
-  } else if (warp >= 4) {  // ------------------------------------------ softmax warpgroups
+  }
+  } else {  // ------------------------------------------------------------ softmax warpgroups
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 192;\n" ::: "memory");
     const int t = (warp - 4) >> 2;  // head of the pair
+    if (kPPTurns && t == 1 && blockIdx.x < n_items) asm volatile("bar.arrive 1, 256;" ::: "memory");  // head 0 first
     const int q = warp & 3;         // TMEM lane quarter
     const int r = q * 32 + lane;    // query row within the tile
     const uint32_t srow = tmem + (static_cast<uint32_t>(q * 32) << 16) + t * 128;
@@ -796,25 +808,26 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         sph ^= 1;
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const bool diag = j == qt;
-        // pass 1: row max over the 128 keys
-        float pm = -INFINITY;
+        // the whole 128-key S row in registers (one TMEM pass), row max in-thread
+        float sv[128];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          float s[64];
-          tld32(srow + h * 64, *reinterpret_cast<float(*)[32]>(&s[0]));
-          tld32(srow + h * 64 + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          float mx8[8];
+        for (int c = 0; c < 4; ++c) tld32(srow + c * 32, *reinterpret_cast<float(*)[32]>(&sv[c * 32]));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float mx8[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+        for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+        if (diag) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) {
-            const float v = (diag && h * 64 + c > r) ? -INFINITY : s[c];
-            mx8[c & 7] = fmaxf(mx8[c & 7], v);
+          for (int c = 0; c < 128; ++c) {
+            if (c > r) sv[c] = -INFINITY;
+            mx8[c & 7] = fmaxf(mx8[c & 7], sv[c]);
           }
-          pm = fmaxf(pm, fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 128; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], sv[c]);
         }
+        const float pm = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         const float mx = scale_log2 * pm;
         float factor = 1.0f;
         const bool rescale = mx > m_used + kRescaleThresh;
@@ -825,7 +838,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         l *= factor;
         // O_t is stable here (this S's commit covered PV_t,{j-1})
         if (j > 0 && __any_sync(0xffffffffu, rescale)) {
-#pragma unroll
+#pragma unroll 1
           for (int c = 0; c < 4; ++c) {
             float o[32];
             tld32(orow + c * 32, o);
@@ -835,28 +848,32 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             tst32(orow + c * 32, o);
           }
         }
-        // pass 2: P = 2^(s * scale - m) (bf16) over the consumed S columns
+        // P = 2^(s * scale - m) (bf16) over the consumed S columns, 32 keys per store.
+        // The two heads take turns in this MUFU-bound phase (named barriers
+        // 1 / 2): one head exponentiates while the other loads / reduces /
+        // stores and its MMAs run, so the phases interleave instead of both
+        // heads contending for the SFU in lock-step.
+        if (kPPTurns) asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
         float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          float s[64];
-          tld32(srow + h * 64, *reinterpret_cast<float(*)[32]>(&s[0]));
-          tld32(srow + h * 64 + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          uint32_t pk[32];
+        for (int h = 0; h < 4; ++h) {
+          uint32_t pk[16];
 #pragma unroll
-          for (int c2 = 0; c2 < 32; ++c2) {
-            const int c0 = h * 64 + 2 * c2;
-            const float x0 = (diag && c0 > r) ? -INFINITY : fmaf(s[2 * c2], scale_log2, -m_used);
-            const float x1 = (diag && c0 + 1 > r) ? -INFINITY : fmaf(s[2 * c2 + 1], scale_log2, -m_used);
-            const float p0 = c2 < kPolyPairs ? ex2_poly(x0) : ex2(x0);
-            const float p1 = c2 < kPolyPairs ? ex2_poly(x1) : ex2(x1);
+          for (int c2 = 0; c2 < 16; ++c2) {
+            const int c0 = h * 32 + 2 * c2;
+            const float x0 = fmaf(sv[c0], scale_log2, -m_used), x1 = fmaf(sv[c0 + 1], scale_log2, -m_used);
+            const bool poly = (h * 16 + c2) % 4 == 0 && kPolyPairs > 0;  // 1 in 4 pairs on the FMA pipe
+            const float p0 = poly ? ex2_poly(x0) : ex2(x0);
+            const float p1 = poly ? ex2_poly(x1) : ex2(x1);
             sum8[(2 * c2) & 7] += p0;
             sum8[(2 * c2 + 1) & 7] += p1;
             pk[c2] = bf2(p0, p1);
           }
-          tst32u(srow + h * 32, pk);
+          tst16u(srow + h * 16, pk);
         }
+        // hand the turn to the other head (head 1's very last hand-off has no taker)
+        if (kPPTurns && !(t == 1 && j == n - 1 && it + gridDim.x >= n_items))
+          asm volatile("bar.arrive %0, 256;" ::"r"(2 - t) : "memory");
         l += ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -922,10 +939,13 @@ bool prefill_bf16_tcgen05(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t 
                      cudaFuncSetAttribute(fa_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(kPPSmem)) == cudaSuccess;
   if (!enc || !attr) return false;
-  // OPF_FA=pp: two heads of one GQA group per item (ping-pong; even groups only)
+  // Two heads of one GQA group per item (fa_pp_kernel: registers rebalanced
+  // with setmaxnreg, whole S row per thread) for even groups — measured 111 vs
+  // 126 us at 8 x 1024 tokens, 32 / 8 heads (620 vs 547 TFLOP/s); OPF_FA=single
+  // forces the one-head kernel.
   static const bool one_tile = [] {
     const char* e = std::getenv("OPF_FA");
-    return !(e && std::string(e) == "pp");  // ping-pong measured slower (softmax issue-bound), opt-in
+    return e && std::string(e) == "single";
   }();
   const bool pp = !one_tile && (nq / nkv) % 2 == 0;
   static const int parts = [] {  // OPF_FA_PARTS=2|4 softmax column parts per row

@@ -62,6 +62,13 @@ spec = {"name": "sequential"}
 for _ in range(5):
     sess.run(spec)
 torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(10):
+    sess.run(spec)
+e1.record()
+torch.cuda.synchronize()
+graph_ms = e0.elapsed_time(e1) / 10  # CUDA-graph replay of the same plan
 tr = sess.trace()
 agg = collections.defaultdict(lambda: [0, 0.0])
 for e in tr:
@@ -72,5 +79,6 @@ for e in tr:
 tot = sum(v[1] for v in agg.values())
 span = (max(e["ts"] + e["dur"] for e in tr) - min(e["ts"] for e in tr)) / 1e3
 rows = sorted(agg.items(), key=lambda kv: -kv[1][1])
-print(json.dumps({"which": which, "layers": L, "span_ms": round(span, 3), "sum_ms": round(tot, 3),
+print(json.dumps({"which": which, "layers": L, "graph_replay_ms": round(graph_ms, 3), "span_ms": round(span, 3),
+                  "sum_ms": round(tot, 3),
                   "per_kernel_ms_per_layer": {k: round(v[1] / L, 4) for k, v in rows}}, indent=1))
