@@ -798,6 +798,40 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     const uint32_t srow = tmem + (static_cast<uint32_t>(q * 32) << 16) + t * 128;
     const uint32_t orow = tmem + (static_cast<uint32_t>(q * 32) << 16) + kColO + t * 128;
     uint32_t sph = 0, oph = 0;
+    // Epilogue of an item (O_t / l -> bf16 -> global), deferred until the next
+    // item's first P is stored: that softmax overlaps the last PV of this item
+    // instead of waiting behind it (the next PV needs O free anyway).
+    struct Done {
+      int64_t row0;  // first output row of the item's q tile
+      int head;
+      float l;
+    } prev{0, 0, 0.0f};
+    bool pending = false;
+    auto epilogue = [&](const Done& d) {
+      bar_wait(&o_full[t], oph);
+      oph ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const float inv = d.l > 0.0f ? 1.0f / d.l : 0.0f;
+      __nv_bfloat16* op = out + (d.row0 + r) * (static_cast<int64_t>(nq) * HD) + static_cast<int64_t>(d.head) * HD;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float o[32];
+        tld32(orow + c * 32, o);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 u;
+          u.x = bf2(o[v * 8 + 0] * inv, o[v * 8 + 1] * inv);
+          u.y = bf2(o[v * 8 + 2] * inv, o[v * 8 + 3] * inv);
+          u.z = bf2(o[v * 8 + 4] * inv, o[v * 8 + 5] * inv);
+          u.w = bf2(o[v * 8 + 6] * inv, o[v * 8 + 7] * inv);
+          *reinterpret_cast<uint4*>(op + c * 32 + v * 8) = u;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) bar_arrive(&o_free[t]);
+    };
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
       int qt, hp, seq;
       decode_item(it, qt, hp, seq);
@@ -879,33 +913,15 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) bar_arrive(&p_full[t]);
-      }
-      // ---- epilogue: O_t / l -> bf16 -> global
-      bar_wait(&o_full[t], oph);
-      oph ^= 1;
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const float inv = l > 0.0f ? 1.0f / l : 0.0f;
-      __nv_bfloat16* op = out + (static_cast<int64_t>(seq) * S + qt * BQ + r) * (static_cast<int64_t>(nq) * HD) +
-                          static_cast<int64_t>(2 * hp + t) * HD;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float o[32];
-        tld32(orow + c * 32, o);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          uint4 u;
-          u.x = bf2(o[v * 8 + 0] * inv, o[v * 8 + 1] * inv);
-          u.y = bf2(o[v * 8 + 2] * inv, o[v * 8 + 3] * inv);
-          u.z = bf2(o[v * 8 + 4] * inv, o[v * 8 + 5] * inv);
-          u.w = bf2(o[v * 8 + 6] * inv, o[v * 8 + 7] * inv);
-          *reinterpret_cast<uint4*>(op + c * 32 + v * 8) = u;
+        if (j == 0 && pending) {
+          epilogue(prev);
+          pending = false;
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) bar_arrive(&o_free[t]);
+      prev = Done{static_cast<int64_t>(seq) * S + static_cast<int64_t>(qt) * BQ, 2 * hp + t, l};
+      pending = true;
     }
+    if (pending) epilogue(prev);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
