@@ -159,11 +159,11 @@ def barrier(world):
 
 
 # ------------------------------------------------------------------ our engine
-def build_session(of, desc, rules, dev, comm, seed):
+def build_session(of, desc, rules, dev, comm, seed, extra_cfg=None):
     import torch
     g = of.build_graph(desc)
     plan = of.partition(g, rules)
-    sess = of.Session(g, plan, {"lanes": 3, "device": dev.index}, comm)
+    sess = of.Session(g, plan, dict({"lanes": 3, "device": dev.index}, **(extra_cfg or {})), comm)
     gen = torch.Generator(device=dev).manual_seed(seed)
     bufs = {}
     for t in g.description["tensors"]:

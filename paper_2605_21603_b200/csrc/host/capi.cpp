@@ -94,6 +94,7 @@ SessionConfig parse_config(const char* text) {
   if (const json::Value* x = v.get("device")) c.device = static_cast<int>(x->as_i64());
   if (const json::Value* x = v.get("gemm_sm_budget")) c.gemm_sm_budget = static_cast<int>(x->as_i64());
   if (const json::Value* x = v.get("fuse")) c.fuse = x->b;
+  if (const json::Value* x = v.get("fuse_addnorm")) c.fuse_addnorm = x->b;
   if (const json::Value* x = v.get("world")) c.world = static_cast<int>(x->as_i64());
   if (const json::Value* x = v.get("lane_sm_budget"))
     for (const json::Value& e : x->arr()) c.lane_sm_budget.push_back(static_cast<int>(e.as_i64()));

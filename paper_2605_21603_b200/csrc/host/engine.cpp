@@ -570,6 +570,8 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
       std::set<int32_t> skip;
       if (cfg_.fuse) {
         const std::set<int32_t> in_dispatch(ops.begin(), ops.end());
+        std::map<int32_t, int32_t> pos_of;  // op -> position in this dispatch
+        for (int32_t k = 0; k < static_cast<int32_t>(ops.size()); ++k) pos_of[ops[k]] = k;
         for (int32_t op : ops) {
           const OperatorNode& node = g_.ops[op];
           if (node.kind != OperatorKind::kMatMul) continue;
@@ -587,7 +589,17 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
           const auto hd = act.attrs.params.find("head_dim");
           const bool rope = act.attrs.custom_name == "rope" && act.inputs.size() == 2 && act.inputs[0] == t &&
                             hd != act.attrs.params.end() && hd->second == 128.0;
-          if (!silu && !rope) continue;
+          // residual add + RMSNorm: the MatMul output is add_rmsnorm's second
+          // input; the residual and gamma must exist by the MatMul's position
+          bool addnorm = cfg_.fuse_addnorm && act.attrs.custom_name == "add_rmsnorm" && act.inputs.size() == 3 &&
+                         act.outputs.size() == 2 && act.inputs[1] == t && act.inputs[0] != t &&
+                         g_.tensors[act.inputs[0]].dtype == Dtype::kBF16;
+          for (int32_t u : {act.inputs.size() == 3 ? act.inputs[0] : -1, act.inputs.size() == 3 ? act.inputs[2] : -1})
+            if (addnorm && u >= 0) {
+              const int32_t p = g_.tensors[u].producer;
+              if (p >= 0 && in_dispatch.count(p) && pos_of[p] > pos_of[op]) addnorm = false;
+            }
+          if (!silu && !rope && !addnorm) continue;
           fused_act[op] = cons[0];
           skip.insert(cons[0]);
         }
@@ -614,29 +626,35 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
         auto fa = fused_act.find(op);
         if (fa != fused_act.end()) {
           const OperatorNode& act = g_.ops[fa->second];
-          const int32_t a_out = act.outputs[0];
-          if (!view_of.count(a_out)) {
-            const int32_t blk = pl.alloc(tensor_bytes_rows(g_.tensors[a_out], nrows), di);
-            scratch.push_back(blk);
-            int_blk[a_out] = blk;
-            view_of[a_out] = arena_view(blk, a_out, 0, nrows);
-          }
+          for (int32_t a_out : act.outputs)
+            if (!view_of.count(a_out)) {
+              const int32_t blk = pl.alloc(tensor_bytes_rows(g_.tensors[a_out], nrows), di);
+              scratch.push_back(blk);
+              int_blk[a_out] = blk;
+              view_of[a_out] = arena_view(blk, a_out, 0, nrows);
+            }
           const bool rope = act.attrs.custom_name == "rope";
+          const bool addnorm = act.attrs.custom_name == "add_rmsnorm";
           PlannedLaunch l;
           l.op = op;
           l.kind = OperatorKind::kMatMul;
           l.attrs = node.attrs;
-          if (rope)
+          if (rope || addnorm)
             for (const auto& kv : act.attrs.params) l.attrs.params[kv.first] = kv.second;
-          l.attrs.params["epi"] = rope ? 2.0 : 1.0;
+          l.attrs.params["epi"] = rope ? 2.0 : (addnorm ? 4.0 : 1.0);
           l.name = node.name + "+" + act.name;
           l.rows = nrows;
           l.in.push_back(view_of.at(node.inputs[0]));
           l.in.push_back(weight_view(node.inputs[1], node));
           if (rope) l.in.push_back(view_of.at(act.inputs[1]));  // positions
-          l.out.push_back(view_of.at(a_out));
+          if (addnorm) {                                         // residual x, gamma
+            l.in.push_back(view_of.at(act.inputs[0]));
+            l.in.push_back(g_.tensors[act.inputs[2]].role == TensorRole::kWeight ? weight_view(act.inputs[2], act)
+                                                                                 : view_of.at(act.inputs[2]));
+          }
+          for (int32_t o : act.outputs) l.out.push_back(view_of.at(o));
           l.prepacked = node.inputs[1];
-          l.prepack_mode = rope ? 0 : 1;
+          l.prepack_mode = (rope || addnorm) ? 0 : 1;
           pd.launches.push_back(std::move(l));
           plan_ws(pd.launches.back());
           // only inputs whose last consumer is this MatMul retire here (an input

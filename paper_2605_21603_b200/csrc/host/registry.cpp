@@ -105,6 +105,8 @@ size_t kind_workspace(const opf_op_ctx& c, const opf_view* in, int n_in, const o
       in[0].dtype == OPF_BF16) {
     const int epi = static_cast<int>(ctx_param(c, "epi", 0.0));
     if (epi == 2) return 0;  // RoPE epilogue runs unsplit
+    if (epi == 4)            // residual-norm epilogue: per-row, per-column-tile sums of squares
+      return (static_cast<size_t>(rows * (out[0].shape[1] / 256)) * sizeof(float) + 255) / 256 * 256;
     const int64_t N = out[0].shape[1] * (epi == 1 ? 2 : 1);
     return gemm_splitk_workspace(rows, N, in[0].shape[1], c.max_ctas);
   }
@@ -123,9 +125,12 @@ opf_status launch_kind(const opf_op_ctx& c, const opf_view* in, int n_in, opf_vi
   try {
     switch (kind) {
       case OperatorKind::kMatMul: {
-        const int epi = static_cast<int>(ctx_param(c, "epi", 0.0));  // 1: fused SiLU-mul, 2: fused RoPE
-        if (n_in != (epi == 2 ? 3 : 2))
-          return op_error(Errc::ShapeMismatch, epi == 2 ? "MatMul+RoPE takes (x, w, positions)" : "MatMul takes 2 inputs");
+        // 1: fused SiLU-mul, 2: fused RoPE, 4: fused residual add + RMSNorm (add_rmsnorm)
+        const int epi = static_cast<int>(ctx_param(c, "epi", 0.0));
+        if (n_in != (epi == 2 ? 3 : epi == 4 ? 4 : 2) || n_out != (epi == 4 ? 2 : 1))
+          return op_error(Errc::ShapeMismatch, epi == 2   ? "MatMul+RoPE takes (x, w, positions)"
+                                               : epi == 4 ? "MatMul+add_rmsnorm takes (a, w, x, g) -> (x1, y)"
+                                                          : "MatMul takes 2 inputs");
         const int64_t K = in[0].shape[1];
         const int64_t N = out[0].shape[1] * (epi == 1 ? 2 : 1);
         if (in[1].shape[0] != K || in[1].shape[1] != N)
@@ -154,6 +159,22 @@ opf_status launch_kind(const opf_op_ctx& c, const opf_view* in, int n_in, opf_vi
             g.pos = vptr<const int64_t>(in[2]);
             g.rot_heads = nq + nkv;
             g.log2_theta = static_cast<float>(std::log2(ctx_param(c, "theta", 10000.0)));
+          }
+          if (epi == 4) {  // C = x + A W, row statistics into the workspace, then the norm pass
+            if (view_row_elems(in[2]) != N || view_numel(in[3]) != N || N % 256 != 0)
+              return op_error(Errc::ShapeMismatch, "MatMul+add_rmsnorm: residual [rows,N], gamma [N], N % 256 == 0");
+            const size_t need = static_cast<size_t>(rows * (N / 256)) * sizeof(float);
+            if (!c.workspace || c.workspace_bytes < need)
+              return op_error(Errc::ShapeMismatch, "MatMul+add_rmsnorm: workspace too small");
+            g.resid = view_ptr(in[2]);
+            g.ssq = static_cast<float*>(c.workspace);
+            g.ws = nullptr;
+            g.ws_bytes = 0;
+            g.bt = c.aux;
+            gemm_bf16_tc(g, s);
+            rmsnorm_from_stats(view_ptr(out[0]), g.ssq, N / 256, view_ptr(in[3]), view_ptr(out[1]), rows, N,
+                               static_cast<float>(ctx_param(c, "eps", 1e-5)), s);
+            return launch_status("MatMul+add_rmsnorm");
           }
           if (c.aux) {  // pre-packed [N,K] weight -> tcgen05 path
             g.bt = c.aux;

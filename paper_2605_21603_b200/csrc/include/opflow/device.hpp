@@ -133,8 +133,16 @@ struct GemmArgs {
   float log2_theta;    // epi 2
   void* ws;        // split-K workspace (gemm_splitk_workspace bytes), nullptr = no split
   size_t ws_bytes;
+  // epi 4: C = x + A B^T (x = resid [M,N]) and per-row, per-256-column-tile sums
+  // of squares of the rounded C in ssq [M, N/256] (input of rmsnorm_from_stats)
+  const void* resid;
+  float* ssq;
 };
 void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s);
+// y = x1 * rsqrt(sum(ssq[row, :]) / H + eps) * g  (the norm half of a MatMul
+// fused with add_rmsnorm: x1 and ssq come from the epi-4 GEMM)
+void rmsnorm_from_stats(const void* x1, const float* ssq, int64_t n_tiles, const void* gamma, void* y, int64_t rows,
+                        int64_t H, float eps, cudaStream_t s);
 // Push epilogue (row-parallel GEMM -> all-reduce over peer memory): output row
 // r of this rank's partial belongs to owner q = r / blk; the 32-row slab is
 // stored at dst[q] + (r - q*blk) * N (this rank's slot in q's window) and

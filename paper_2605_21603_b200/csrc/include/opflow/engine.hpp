@@ -141,6 +141,7 @@ struct SessionConfig {
   bool prealloc = true;       // Algorithm-1 zero-copy merge buffers; false = copying fallback
   bool cuda_graph = true;     // capture + replay; false = eager launches every run
   bool fuse = true;           // GEMM epilogue fusion (MatMul -> silu_mul) inside a dispatch
+  bool fuse_addnorm = true;   // ... and MatMul -> add_rmsnorm (residual add in the epilogue)
   int device = 0;
   int gemm_sm_budget = 0;     // max CTAs for tensor-core GEMMs on lane 0 when overlapping
   std::vector<int> lane_sm_budget;  // per-lane SM budget defaults (strategy may override)

@@ -74,10 +74,17 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const __nv_bfloat16* __r
 // ------------------------------------------------------------------ tcgen05 path
 constexpr int BM = 128, BN = 256, BK = 64;
 // EPI 2 (RoPE epilogue): a 256-column tile holds two 128-wide heads.
+// EPI 4 (residual add + RMSNorm statistics): out = x + A B^T (the add_rmsnorm
+// residual output) and this tile's per-row sum of squares of the rounded
+// result in ssq[row * ssq_ld + n_tile] (one writer per entry: deterministic).
 struct RopeArgs {
   const int64_t* pos;
   int rot_heads;
   float log2_theta;
+  const __nv_bfloat16* resid = nullptr;  // EPI 4: x [M, N]
+  float* ssq = nullptr;                  // EPI 4: [M, ssq_ld] partial sums of squares
+  int64_t ssq_ld = 0;                    // EPI 4: N / 256 (column tiles)
+  int64_t resid_ld = 0;                  // EPI 4: row stride of x (= N)
 };
 constexpr int kStages = 4;
 constexpr int kAccStages = 2;
@@ -211,9 +218,19 @@ __device__ __forceinline__ void store_tile(const CUtensorMap* map_c, uint32_t tm
   }
   // EPI 1 needs TN = 256 (gate | up halves of 128); chunks are 64 output columns
   constexpr int kChunks = EPI == 1 ? 2 : TN / 64;
+  float ss = 0.0f;  // EPI 4: this lane's row, this warp's columns of the tile
 #pragma unroll 1
   for (int chunk = first; chunk < kChunks; chunk += step) {
     uint32_t v0[32], v1[32];
+    uint4 xres[EPI == 4 ? 8 : 1];
+    if constexpr (EPI == 4) {  // residual row segment, loads in flight under the TMEM loads
+      const int64_t row = row0 + lane;
+      if (row < M) {
+        const uint4* xr = reinterpret_cast<const uint4*>(rope->resid + row * rope->resid_ld + nb * TN + chunk * 64);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xres[j] = __ldcs(xr + j);
+      }
+    }
     const uint32_t taddr = tmem_col0 + static_cast<uint32_t>(chunk * 64);
     tmem_ld32(taddr, v0);
     tmem_ld32(taddr + 32, v1);
@@ -230,6 +247,25 @@ __device__ __forceinline__ void store_tile(const CUtensorMap* map_c, uint32_t tm
       }
     } else {
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    }
+    if constexpr (EPI == 4) {  // + residual row (128 B of this lane's row), sum of squares of the rounded sum
+      if (row0 + lane < M) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 u = xres[j];
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+          uint32_t* dst = j < 4 ? &v0[8 * j] : &v1[8 * (j - 4)];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h2[e]);
+            const float a = __bfloat162float(__float2bfloat16(__uint_as_float(dst[2 * e]) + f.x));
+            const float b = __bfloat162float(__float2bfloat16(__uint_as_float(dst[2 * e + 1]) + f.y));
+            ss += a * a + b * b;
+            dst[2 * e] = __float_as_uint(a);
+            dst[2 * e + 1] = __float_as_uint(b);
+          }
+        }
+      }
     }
     // staging buffer reuse: the TMA store issued two chunks ago must have read it
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -254,6 +290,10 @@ __device__ __forceinline__ void store_tile(const CUtensorMap* map_c, uint32_t tm
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
     buf ^= 1;
+  }
+  if constexpr (EPI == 4) {
+    static_assert(EPI != 4 || TN == 256, "EPI 4 partials assume whole 256-column tiles per warp");
+    if (row0 + lane < M) rope->ssq[(row0 + lane) * rope->ssq_ld + nb] = ss;
   }
 }
 
@@ -1014,6 +1054,8 @@ void gemm_bf16_tc_init() {
                                   static_cast<int>(Tc2Cfg<128, false>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<4, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tc2Cfg<256, true>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1079,7 +1121,10 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
   require(g.epi == 0 || g.n % BN == 0, Errc::ShapeMismatch,
           "SiLU-mul / RoPE epilogues need N to be a multiple of 256");
   require(g.epi != 2 || g.pos != nullptr, Errc::ShapeMismatch, "RoPE epilogue needs positions");
-  const RopeArgs rope{g.pos, g.rot_heads, g.log2_theta};
+  require(g.epi != 4 || (g.n % 256 == 0 && g.resid && g.ssq), Errc::ShapeMismatch,
+          "residual-norm epilogue needs N % 256 == 0, the residual and the statistics buffer");
+  const RopeArgs rope{g.pos, g.rot_heads, g.log2_theta, static_cast<const __nv_bfloat16*>(g.resid), g.ssq,
+                      g.n / 256, g.n};
   gemm_bf16_tc_init();
   static const int mode = [] {  // OPF_GEMM=1sm|2sm|auto
     const char* e = std::getenv("OPF_GEMM");
@@ -1087,7 +1132,7 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     if (e && std::string(e) == "2sm") return 2;
     return 0;
   }();
-  const bool pair = mode == 2 || (mode == 0 && g.m > BM);
+  const bool pair = mode == 2 || (mode == 0 && g.m > BM) || g.epi == 4;  // EPI 4 lives in the 2-CTA kernel
   const int64_t n_out = g.epi == 1 ? g.n / 2 : g.n;
   const CUtensorMap ma = make_map(g.a, g.k, g.m, g.lda, BK, BM);
   const CUtensorMap mc = make_map(g.c, n_out, g.m, g.ldc, 64, 32);
@@ -1111,7 +1156,7 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     }
     const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, static_cast<uint32_t>(tn / 2));
     const int64_t tiles = mt * ((g.n + tn - 1) / tn);
-    int splits = tn == 256 && g.epi != 2 ? gemm_splitk_splits(g.m, g.n, g.k, g.max_ctas) : 1;
+    int splits = tn == 256 && g.epi != 2 && g.epi != 4 ? gemm_splitk_splits(g.m, g.n, g.k, g.max_ctas) : 1;
     float4* ws = nullptr;
     int* sem = nullptr;
     if (splits > 1) {
@@ -1133,6 +1178,9 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     else if (splits > 1)
       launch_pdl(gemm_tc2_kernel<0, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
                  g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
+    else if (g.epi == 4)
+      launch_pdl(gemm_tc2_kernel<4, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb,
+                 mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
     else if (g.epi == 2)
       launch_pdl(gemm_tc2_kernel<2, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb,
                  mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);

@@ -114,6 +114,42 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const T* __restrict__
   }
 }
 
+// Norm half of a MatMul fused with add_rmsnorm: the epi-4 GEMM stored
+// x1 = x + A W and per-(row, 256-column tile) sums of squares; one warp per
+// row sums those (fixed order: deterministic) and writes y = x1 * rsqrt(ms + eps) * g.
+__global__ void __launch_bounds__(256) rmsnorm_stats_kernel(const __nv_bfloat16* __restrict__ x1,
+                                                            const float* __restrict__ ssq, int64_t n_tiles,
+                                                            const __nv_bfloat16* __restrict__ g,
+                                                            __nv_bfloat16* __restrict__ y, int64_t rows, int64_t H,
+                                                            float eps) {
+  pdl_wait();
+  pdl_trigger();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+  if (row >= rows) return;
+  float t = 0.0f;
+  for (int64_t i = lane; i < n_tiles; i += 32) t += ssq[row * n_tiles + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  const float inv = rsqrtf(t / static_cast<float>(H) + eps);
+  const uint4* xr = reinterpret_cast<const uint4*>(x1 + row * H);
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+  uint4* yr = reinterpret_cast<uint4*>(y + row * H);
+  for (int64_t c = lane; c < H / 8; c += 32) {
+    const uint4 u = xr[c], gu = gr[c];
+    const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&u);
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&gu);
+    uint4 o;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 fa = __bfloat1622float2(a[e]), fb = __bfloat1622float2(b[e]);
+      o2[e] = __floats2bfloat162_rn(fa.x * inv * fb.x, fa.y * inv * fb.y);
+    }
+    yr[c] = o;
+  }
+}
+
 // HF rotate-half rope on the q and k heads of a fused qkv row; v is copied.
 template <typename T>
 __global__ void __launch_bounds__(256) rope_kernel(const T* __restrict__ qkv,
@@ -358,6 +394,13 @@ opf_status op_qk_norm_rope(const opf_op_ctx* c, const opf_view* in, int32_t n_in
 }
 
 }  // namespace
+
+void rmsnorm_from_stats(const void* x1, const float* ssq, int64_t n_tiles, const void* gamma, void* y, int64_t rows,
+                        int64_t H, float eps, cudaStream_t s) {
+  launch_pdl(rmsnorm_stats_kernel, dim3(static_cast<unsigned>((rows + 7) / 8)), dim3(256), 0, s,
+             static_cast<const __nv_bfloat16*>(x1), ssq, n_tiles, static_cast<const __nv_bfloat16*>(gamma),
+             static_cast<__nv_bfloat16*>(y), rows, H, eps);
+}
 
 void register_llama_ops(OpRegistry& r) {
   r.add({"rmsnorm", op_rmsnorm, ResourceClass::kMemory, 2, 1, {}});

@@ -222,7 +222,7 @@ class Graph:
         return self.tensor_index[name]
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value:
+        if getattr(self, "_h", None) and self._h.value and lib is not None:  # None at interpreter exit
             lib().opf_graph_free(self._h)
             self._h = C.c_void_p()
 
@@ -296,7 +296,7 @@ class PartitionPlan:
         return None
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value:
+        if getattr(self, "_h", None) and self._h.value and lib is not None:  # None at interpreter exit
             lib().opf_plan_free(self._h)
             self._h = C.c_void_p()
 
@@ -553,7 +553,7 @@ class Comm:
         return e.value
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value:
+        if getattr(self, "_h", None) and self._h.value and lib is not None:  # None at interpreter exit
             lib().opf_comm_free(self._h)
             self._h = C.c_void_p()
 
@@ -631,7 +631,7 @@ class Session:
         return json.loads(take_string(p))
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value:
+        if getattr(self, "_h", None) and self._h.value and lib is not None:  # None at interpreter exit
             lib().opf_session_free(self._h)
             self._h = C.c_void_p()
 

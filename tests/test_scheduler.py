@@ -292,3 +292,24 @@ def test_fuse_gemm_folds_row_parallel_matmul_into_the_allreduce():
     p2 = of.partition(g, [R.by_func("AllReduce"), R.by_func("add_rmsnorm")])
     s2, _ = of.dry_run(g, p2, {"name": "fuse_norm_comm", "fuse_gemm": 1})
     assert {d["replace_fn"] for d in s2["dispatches"]} == {"", "allreduce_add_rmsnorm"}
+
+
+def test_residual_norm_epilogue_fusion_plan():
+    """Peephole fusion plans MatMul -> add_rmsnorm as one epi-4 MatMul launch
+    (inputs a, w, residual, gamma; outputs x1, h) when the residual is available
+    at the MatMul's position; fuse_addnorm=false keeps them apart."""
+    desc = of.llama_graph(layers=2, tokens=512, seq_len=128, hidden=512, heads=4, kv_heads=2, head_dim=128,
+                          inter=1024, dtype="bf16")
+    g = of.build_graph(desc)
+    p = of.partition(g, [])
+    sched, _ = of.dry_run(g, p, {"name": "sequential"})
+    ls = [l for d in sched["dispatches"] for l in d["launches"]]
+    fused = [l for l in ls if "resid_norm" in l["name"] and "+" in l["name"]]
+    assert [l["name"] for l in fused] == ["layer0.o_proj+layer0.attn_resid_norm",
+                                          "layer0.down+layer0.mlp_resid_norm",
+                                          "layer1.o_proj+layer1.attn_resid_norm"]
+    for l in fused:
+        assert len(l["in"]) == 4 and len(l["out"]) == 2 and l["ws_bytes"] >= 512 * 2 * 4
+    plain, _ = of.dry_run(g, p, {"name": "sequential"}, config={"fuse_addnorm": False})
+    assert not any("resid_norm" in l["name"] and "+" in l["name"]
+                   for d in plain["dispatches"] for l in d["launches"])

@@ -15,12 +15,13 @@ L = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 T, S = 8192, 1024
 dev = torch.device("cuda:0")
 desc = of.llama_graph(layers=L, tokens=T, seq_len=S, tp=1, dtype="bf16", **bench.LLAMA)
-g, plan, sess, bufs = bench.build_session(of, desc, [], dev, None, seed=1234)
+extra = json.loads(os.environ.get("SESSION_CFG", "{}"))  # e.g. {"fuse_addnorm": false}
+g, plan, sess, bufs = bench.build_session(of, desc, [], dev, None, seed=1234, extra_cfg=extra)
 pos = (torch.arange(T, device=dev) % S).to(torch.int64)
 sess.bind("positions", pos)
 cands = {"sequential": {"name": "sequential"},
          "nanoflow_u2": {"name": "split_overlap", "n_microbatches": 2, "align": S, "lane_mode": "ubatch"}}
 res = bench.time_candidates(torch, sess, cands, 5, 3, torch.cuda.current_stream(dev), 1)
-print(json.dumps({"lib": os.environ.get("OPF_LIB", "default"), "layers": L,
+print(json.dumps({"lib": os.environ.get("OPF_LIB", "default"), "cfg": extra, "layers": L,
                   "ms_per_layer": {k: round(v / L, 4) for k, v in res.items()},
                   "launches": sess.stats()["last"]["launches"]}))
