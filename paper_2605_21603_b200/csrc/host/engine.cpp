@@ -594,6 +594,12 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
           bool addnorm = cfg_.fuse_addnorm && act.attrs.custom_name == "add_rmsnorm" && act.inputs.size() == 3 &&
                          act.outputs.size() == 2 && act.inputs[1] == t && act.inputs[0] != t &&
                          g_.tensors[act.inputs[0]].dtype == Dtype::kBF16;
+          if (addnorm) {  // only where the plain GEMM would not split K (decode-size rows keep split-K)
+            int mc = 0;
+            if (cfg_.gemm_sm_budget > 0 && d.lane == 0) mc = cfg_.gemm_sm_budget;
+            if (d.lane < static_cast<int>(budgets.size()) && budgets[d.lane] > 0) mc = budgets[d.lane];
+            addnorm = gemm_splitk_splits(nrows, w.shape[1], w.shape[0], mc) <= 1;
+          }
           for (int32_t u : {act.inputs.size() == 3 ? act.inputs[0] : -1, act.inputs.size() == 3 ? act.inputs[2] : -1})
             if (addnorm && u >= 0) {
               const int32_t p = g_.tensors[u].producer;
