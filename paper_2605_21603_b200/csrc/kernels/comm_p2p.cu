@@ -103,6 +103,87 @@ __global__ void __launch_bounds__(kThreads) ar_add_rmsnorm_p2p_kernel(
   cta_barrier(pp, my_epoch, world, rank, err);
 }
 
+// One-shot, push form ("writes to peer buffers"): every rank STORES its
+// partial rows into slot `rank` of every peer's window ([world][rows][H]), so
+// the NVLink traffic is posted writes; after the barrier each rank sums the
+// world slots from its own HBM.  Same bytes as the pull form, no remote-read
+// round trips.  Needs world x rows x H x 2 bytes of window.
+template <bool NORM>
+__global__ void __launch_bounds__(kThreads) ar_push_kernel(
+    PeerPtrs pp, int world, int rank, const __nv_bfloat16* __restrict__ partial, uint32_t* my_epoch,
+    const __nv_bfloat16* __restrict__ resid, const __nv_bfloat16* __restrict__ gamma,
+    __nv_bfloat16* __restrict__ x_out, __nv_bfloat16* __restrict__ y, int64_t rows, int64_t H, float eps,
+    uint32_t* err) {
+  extern __shared__ float rowbuf[];
+  __shared__ float red[kThreads / 32];
+  const int64_t n8 = H / 8;
+  // 1. push my partial rows into every rank's slot `rank`
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x)
+    for (int64_t c = threadIdx.x; c < n8; c += kThreads) {
+      const uint4 v = reinterpret_cast<const uint4*>(partial + r * H)[c];
+      for (int p = 0; p < world; ++p)
+        reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(static_cast<const __nv_bfloat16*>(pp.buf[p])) +
+                                 (static_cast<int64_t>(rank) * rows + r) * H)[c] = v;
+    }
+  __threadfence_system();
+  if (!cta_barrier(pp, my_epoch, world, rank, err)) return;
+  // 2. reduce my world slots (local HBM) [+ residual + norm]
+  const __nv_bfloat16* mine = static_cast<const __nv_bfloat16*>(pp.buf[rank]);
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    float ss = 0.0f;
+    for (int64_t c = threadIdx.x; c < n8; c += kThreads) {
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if constexpr (NORM) {
+        const uint4 u = reinterpret_cast<const uint4*>(resid + r * H)[c];
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h2[e]);
+          acc[2 * e] = f.x;
+          acc[2 * e + 1] = f.y;
+        }
+      }
+      for (int p = 0; p < world; ++p) {
+        const uint4 u = reinterpret_cast<const uint4*>(mine + (static_cast<int64_t>(p) * rows + r) * H)[c];
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h2[e]);
+          acc[2 * e] += f.x;
+          acc[2 * e + 1] += f.y;
+        }
+      }
+      uint4 o;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        o2[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+        if constexpr (NORM) {
+          rowbuf[c * 8 + 2 * e] = acc[2 * e];
+          rowbuf[c * 8 + 2 * e + 1] = acc[2 * e + 1];
+          ss += acc[2 * e] * acc[2 * e] + acc[2 * e + 1] * acc[2 * e + 1];
+        }
+      }
+      reinterpret_cast<uint4*>(x_out + r * H)[c] = o;
+    }
+    if constexpr (NORM) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = ss;
+      __syncthreads();
+      float tot = 0.0f;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) tot += red[w];
+      const float inv = rsqrtf(tot / static_cast<float>(H) + eps);
+      for (int64_t c = threadIdx.x; c < H; c += kThreads)
+        y[r * H + c] = __float2bfloat16(rowbuf[c] * inv * __bfloat162float(gamma[c]));
+      __syncthreads();
+    }
+  }
+  // 3. every rank has read its slots before anyone pushes the next call's rows
+  cta_barrier(pp, my_epoch, world, rank, err);
+}
+
 // Two-shot variant (reduce-scatter -> residual add + RMSNorm -> all-gather)
 // for large messages at W >= 4: rank q reduces and normalises only row block
 // q (rows [q*B, (q+1)*B)), publishes x1 / h of its block in its window, and
@@ -241,13 +322,17 @@ __global__ void __launch_bounds__(kThreads) allreduce_p2p_kernel(
 //      pub[slab] >= epoch, pull x1 over NVLink, normalise locally.
 // NVLink bytes per rank: (W-1)/W of the partial pushed during the GEMM plus
 // (W-1)/W of x1 pulled here — one all-reduce's worth, the first half hidden
-// under the GEMM's math.  Flow control needs no extra barrier: a rank pushes
-// call k+1's partials only after its call-k kernel finished gathering from
-// every owner, i.e. after every owner reset its counters and published.
+// under the GEMM's math.  Between two push calls no extra barrier is needed
+// (a rank pushes call k+1 only after its call-k kernel gathered from every
+// owner, i.e. after every owner reset its counters and published); the final
+// barrier keeps the window invariant shared by all collectives here: each
+// ends after its last window access on every rank, so whichever collective
+// comes next may write into any peer's window (e.g. a one-shot push into the
+// region this call's x1 plane occupied).
 __global__ void __launch_bounds__(kThreads) push_reduce_norm_kernel(
     PeerPtrs pp, int world, int rank, unsigned long long push_off, const __nv_bfloat16* __restrict__ resid,
     const __nv_bfloat16* __restrict__ gamma, __nv_bfloat16* __restrict__ x_out, __nv_bfloat16* __restrict__ y,
-    int64_t rows, int64_t H, float eps, int n_tiles, uint32_t* err) {
+    int64_t rows, int64_t H, float eps, int n_tiles, uint32_t* my_epoch, uint32_t* err) {
   extern __shared__ float rowbuf[];
   __shared__ float red[kThreads / 32];
   __shared__ uint32_t ok;
@@ -385,6 +470,9 @@ __global__ void __launch_bounds__(kThreads) push_reduce_norm_kernel(
       norm_row(r);
     }
   }
+  // 3. every window collective ends with a barrier after its last window
+  //    access, so the next one (of any kind) may write into any peer's window
+  cta_barrier(pp, my_epoch, world, rank, err);
 }
 
 }  // namespace
@@ -478,13 +566,23 @@ bool ar_add_rmsnorm_p2p(const opf_comm* c, const opf_view& o, const opf_view& x,
   // NVLink) when the window holds partials + x1 + h; OPF_AR=oneshot|twoshot forces
   static const int ar_mode = [] {
     const char* e = std::getenv("OPF_AR");
-    if (e && std::string(e) == "oneshot") return 1;
+    if (e && std::string(e) == "oneshot") return 1;  // pull form
     if (e && std::string(e) == "twoshot") return 2;
+    if (e && std::string(e) == "push") return 3;
     return 0;
   }();
   const bool fits2 = static_cast<size_t>(3 * rows * H * 2) <= c->peer_bytes;
+  const bool fits_push = static_cast<size_t>(c->world) * rows * H * 2 <= c->peer_bytes;
   const int m = mode ? mode : ar_mode;
   const bool two = fits2 && (m == 2 || (m == 0 && c->world >= 4 && rows * H * 2 >= (1 << 20)));
+  if (!two && fits_push && (m == 0 || m == 3)) {  // one-shot, push form (default when the window holds W planes)
+    grid = static_cast<int>(std::min<int64_t>(std::min(grid, kBarrierSlot), rows));
+    ar_push_kernel<true><<<std::max(grid, 1), kThreads, H * sizeof(float), s>>>(
+        pp, c->world, c->rank, vptr<__nv_bfloat16>(o), reinterpret_cast<uint32_t*>(base + eo),
+        vptr<__nv_bfloat16>(x), vptr<__nv_bfloat16>(g), vptr<__nv_bfloat16>(x_out), vptr<__nv_bfloat16>(y), rows,
+        H, eps, reinterpret_cast<uint32_t*>(base + eo + sizeof(uint32_t) * kMaxCtas));
+    return true;
+  }
   if (two) {
     const int64_t blk = (rows + c->world - 1) / c->world;
     grid = static_cast<int>(std::min<int64_t>(std::min(grid, kBarrierSlot), blk));
@@ -519,6 +617,17 @@ bool allreduce_p2p(const opf_comm* c, const opf_view& in, opf_view& out, int64_t
   char* base = static_cast<char*>(c->window_base);
   int grid = max_ctas > 0 ? max_ctas : num_sms();
   grid = static_cast<int>(std::min<int64_t>(std::min(grid, kBarrierSlot), rows));
+  static const bool pull = [] {
+    const char* e = std::getenv("OPF_AR");
+    return e && std::string(e) == "oneshot";
+  }();
+  if (!pull && static_cast<size_t>(c->world) * rows * H * 2 <= c->peer_bytes) {  // push form
+    ar_push_kernel<false><<<std::max(grid, 1), kThreads, 0, s>>>(
+        pp, c->world, c->rank, vptr<__nv_bfloat16>(in), reinterpret_cast<uint32_t*>(base + eo), nullptr, nullptr,
+        vptr<__nv_bfloat16>(out), nullptr, rows, H, 0.0f,
+        reinterpret_cast<uint32_t*>(base + eo + sizeof(uint32_t) * kMaxCtas));
+    return true;
+  }
   allreduce_p2p_kernel<<<std::max(grid, 1), kThreads, 0, s>>>(
       pp, c->world, c->rank, vptr<__nv_bfloat16>(in), reinterpret_cast<__nv_bfloat16*>(base),
       reinterpret_cast<uint32_t*>(base + eo), vptr<__nv_bfloat16>(out), rows, H,
@@ -553,10 +662,12 @@ bool gemm_ar_add_rmsnorm_push(const opf_comm* c, const GemmArgs& g, const opf_vi
   window_layout(c->peer_bytes, &fo, &eo);
   const int64_t slabs = blk / 32;
   int grid = g.max_ctas > 0 ? g.max_ctas : num_sms();
-  grid = static_cast<int>(std::min<int64_t>(grid, std::max<int64_t>(slabs, (W - 1) * slabs * 4)));
+  grid = static_cast<int>(std::min<int64_t>(std::min(grid, kBarrierSlot),
+                                             std::max<int64_t>(slabs, (W - 1) * slabs * 4)));
   push_reduce_norm_kernel<<<std::max(grid, 1), kThreads, H * sizeof(float), s>>>(
       pp, W, c->rank, static_cast<unsigned long long>(push_off), vptr<__nv_bfloat16>(x), vptr<__nv_bfloat16>(gam),
       vptr<__nv_bfloat16>(x_out), vptr<__nv_bfloat16>(y), rows, H, eps, static_cast<int>(H / 256),
+      reinterpret_cast<uint32_t*>(static_cast<char*>(c->window_base) + eo),
       reinterpret_cast<uint32_t*>(static_cast<char*>(c->window_base) + eo + sizeof(uint32_t) * kMaxCtas));
   return true;
 }

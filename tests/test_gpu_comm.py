@@ -14,14 +14,16 @@ pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("built")]
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
-@pytest.mark.parametrize("ar_mode,rows", [(1, 64), (2, 64), (2, 61)])
+@pytest.mark.parametrize("ar_mode,rows", [(0, 64), (1, 64), (2, 64), (2, 61), (3, 64), (3, 61)])
 def test_fused_allreduce_add_rmsnorm_virtual_ranks(cuda, world, ar_mode, rows):
-    """ar_mode 1: one-shot (every rank reduces every row); 2: two-shot
-    (reduce-scatter by row blocks -> add + norm -> all-gather), incl. a row
-    count that does not divide by the world size."""
+    """ar_mode 1: one-shot, pull form (every rank reads every rank's rows);
+    3: one-shot, push form (every rank writes its rows into every peer's
+    window; the default when the window holds world planes, else mode 1);
+    2: two-shot (reduce-scatter by row blocks -> add + norm -> all-gather);
+    0: automatic.  Includes a row count that does not divide by the world size."""
     import torch
     H = 4096
-    comms = of.Comm.virtual(world, 0, 3 * rows * H * 2)
+    comms = of.Comm.virtual(world, 0, max(3, world if ar_mode == 3 else 3) * rows * H * 2)
     rng = np.random.default_rng(world)
     tb = lambda a: torch.from_numpy(a.astype(np.float32)).cuda().to(torch.bfloat16)
     x = tb(rng.uniform(-1, 1, (rows, H)))
