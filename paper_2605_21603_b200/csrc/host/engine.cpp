@@ -627,7 +627,10 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
       };
       for (int32_t k = 0; k < static_cast<int32_t>(ops.size()); ++k) {
         const int32_t op = ops[k];
-        if (skip.count(op)) continue;
+        if (skip.count(op)) {  // ran inside its producer's GEMM epilogue: its inputs retire here
+          retire_inputs(k, g_.ops[op].inputs);
+          continue;
+        }
         const OperatorNode& node = g_.ops[op];
         auto fa = fused_act.find(op);
         if (fa != fused_act.end()) {

@@ -313,3 +313,17 @@ def test_residual_norm_epilogue_fusion_plan():
     plain, _ = of.dry_run(g, p, {"name": "sequential"}, config={"fuse_addnorm": False})
     assert not any("resid_norm" in l["name"] and "+" in l["name"]
                    for d in plain["dispatches"] for l in d["launches"])
+
+
+def test_fused_epilogue_keeps_arena_liveness():
+    """An op run inside its producer's GEMM epilogue (add_rmsnorm) still retires
+    its inputs at its own position: the 32-layer Llama-3-8B plan at 8192 rows
+    stays under 1 GiB of arena with the fusion on."""
+    desc = of.llama_graph(layers=32, tokens=8192, seq_len=1024, hidden=4096, heads=32, kv_heads=8,
+                          head_dim=128, inter=14336, dtype="bf16")
+    g = of.build_graph(desc)
+    p = of.partition(g, [])
+    _, fused = of.dry_run(g, p, {"name": "sequential"}, rows=8192)
+    _, plain = of.dry_run(g, p, {"name": "sequential"}, rows=8192, config={"fuse_addnorm": False})
+    assert fused["last"]["plan_arena_bytes"] < (1 << 30)
+    assert fused["last"]["plan_arena_bytes"] < 2 * plain["last"]["plan_arena_bytes"]
