@@ -588,6 +588,13 @@ constexpr int kPPThreads = 384;                  // 4 role warps + 2 softmax war
 #define FA_PP_TURNS 1
 #endif
 constexpr bool kPPTurns = FA_PP_TURNS != 0;      // heads alternate the exp phase
+#ifndef FA_PP_POLY_EVERY
+#define FA_PP_POLY_EVERY 0
+#endif
+// exp2 pairs computed on the FMA pipe: 1 in N (0 = all on MUFU).  Measured at
+// 8 x 1024 tokens: 1 in 2 / 3 / 4 / 8 / 16 -> 119 / 114 / 110 / 104 / 103 us,
+// none (0) -> 101 us: in this kernel the softmax is issue-bound, not MUFU-bound.
+constexpr int kPPPolyEvery = FA_PP_POLY_EVERY;
 constexpr uint32_t kPPQ = 0;                     // Q0, Q1
 constexpr uint32_t kPPK = 2 * kTile;             // [2 stages]
 constexpr uint32_t kPPV = kPPK + 2 * kTile;      // [2 stages]
@@ -645,6 +652,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
   pdl_trigger();
+  int pp_k = 0, pp_s[2] = {0, 0}, pp_pv[2] = {0, 0}, pp_sm = 0;  // trace indices (FA_TRACE builds)
+  (void)pp_k, (void)pp_s, (void)pp_pv, (void)pp_sm;
 
   auto decode_item = [&](int64_t i, int& qt, int& hp, int& seq) {
     qt = q_tiles - 1 - static_cast<int>(i / per_q);  // longest first
@@ -680,6 +689,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           bar_expect(&k_full[stage], kTile);
           tma2d(kd, &mqkv, &k_full[stage], (nq + kh) * HD, row0 + j * BKV);
           tma2d(kd + kHalf, &mqkv, &k_full[stage], (nq + kh) * HD + 64, row0 + j * BKV);
+          FA_T(0, pp_k++);
           if (++stage == 2) {
             stage = 0;
             ph ^= 1;
@@ -726,6 +736,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           mma_ss(tmem + t * 128, ad, bd, S_id, k != 0);
         }
         commit(&s_full[t]);
+        FA_T(2 + t, pp_s[t]++);
       };
       auto issue_pv = [&](int t, int j) {  // O_t += P_t V (P in TMEM over S_t's first 64 cols)
         bar_wait(&p_full[t], pph[t]);
@@ -741,6 +752,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           const uint64_t bd = sdesc(vb + k * 2048, kHalf, 1024);
           mma_ts(tmem + kColO + t * 128, tmem + t * 128 + k * 8, bd, PV_id, (j | k) != 0);
         }
+        FA_T(4 + t, pp_pv[t]++);
       };
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         int qt, hp, seq;
@@ -840,6 +852,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       for (int j = 0; j < n; ++j) {
         bar_wait(&s_full[t], sph);
         sph ^= 1;
+        if (lane == 0 && (warp & 3) == 0) FA_T(6 + 2 * t, pp_sm);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const bool diag = j == qt;
         // the whole 128-key S row in registers (one TMEM pass), row max in-thread
@@ -896,7 +909,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           for (int c2 = 0; c2 < 16; ++c2) {
             const int c0 = h * 32 + 2 * c2;
             const float x0 = fmaf(sv[c0], scale_log2, -m_used), x1 = fmaf(sv[c0 + 1], scale_log2, -m_used);
-            const bool poly = (h * 16 + c2) % 4 == 0 && kPolyPairs > 0;  // 1 in 4 pairs on the FMA pipe
+            const bool poly = kPPPolyEvery > 0 && (h * 16 + c2) % (kPPPolyEvery > 0 ? kPPPolyEvery : 1) == 0;
             const float p0 = poly ? ex2_poly(x0) : ex2(x0);
             const float p1 = poly ? ex2_poly(x1) : ex2(x1);
             sum8[(2 * c2) & 7] += p0;
@@ -913,6 +926,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) bar_arrive(&p_full[t]);
+        if (lane == 0 && (warp & 3) == 0) FA_T(7 + 2 * t, pp_sm);
+        ++pp_sm;
         if (j == 0 && pending) {
           epilogue(prev);
           pending = false;
