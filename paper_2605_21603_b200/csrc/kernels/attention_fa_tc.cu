@@ -187,6 +187,22 @@ __device__ __forceinline__ float ex2_poly(float x) {
   float p = fmaf(fmaf(fmaf(0.0555041086648216f, f, 0.2402264923172690f), f, 0.6931471805599453f), f, 1.0f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+// packed fp32x2 FMA / add (sm_100 FFMA2 / FADD2): two softmax elements per instruction
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+        "l"(*reinterpret_cast<uint64_t*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  uint64_t r;
+  asm("add.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
 #ifndef FA_POLY
 #define FA_POLY 8
 #endif
@@ -901,23 +917,24 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         // stores and its MMAs run, so the phases interleave instead of both
         // heads contending for the SFU in lock-step.
         if (kPPTurns) asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
-        float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        float2 sum4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_used, -m_used);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           uint32_t pk[16];
 #pragma unroll
           for (int c2 = 0; c2 < 16; ++c2) {
             const int c0 = h * 32 + 2 * c2;
-            const float x0 = fmaf(sv[c0], scale_log2, -m_used), x1 = fmaf(sv[c0 + 1], scale_log2, -m_used);
+            const float2 xv = ffma2(make_float2(sv[c0], sv[c0 + 1]), sc2, nm2);
             const bool poly = kPPPolyEvery > 0 && (h * 16 + c2) % (kPPPolyEvery > 0 ? kPPPolyEvery : 1) == 0;
-            const float p0 = poly ? ex2_poly(x0) : ex2(x0);
-            const float p1 = poly ? ex2_poly(x1) : ex2(x1);
-            sum8[(2 * c2) & 7] += p0;
-            sum8[(2 * c2 + 1) & 7] += p1;
+            const float p0 = poly ? ex2_poly(xv.x) : ex2(xv.x);
+            const float p1 = poly ? ex2_poly(xv.y) : ex2(xv.y);
+            sum4[c2 & 3] = fadd2(sum4[c2 & 3], make_float2(p0, p1));
             pk[c2] = bf2(p0, p1);
           }
           tst16u(srow + h * 16, pk);
         }
+        float sum8[8] = {sum4[0].x, sum4[0].y, sum4[1].x, sum4[1].y, sum4[2].x, sum4[2].y, sum4[3].x, sum4[3].y};
         // hand the turn to the other head (head 1's very last hand-off has no taker)
         if (kPPTurns && !(t == 1 && j == n - 1 && it + gridDim.x >= n_items))
           asm volatile("bar.arrive %0, 256;" ::"r"(2 - t) : "memory");
