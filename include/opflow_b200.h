@@ -147,6 +147,11 @@ typedef struct opf_comm opf_comm;
 opf_status opf_comm_unique_id(uint8_t id_out[128]);
 opf_status opf_comm_init(const uint8_t id[128], int32_t world, int32_t rank, int32_t device,
                          opf_comm** out);
+/* Peer-window-only communicator (no NCCL): every collective runs over the
+ * CUDA-IPC window (opf_comm_window_alloc / _open), at any message size.  For
+ * ranks that cannot form an NCCL communicator (two processes sharing one GPU)
+ * or that want NCCL-free collectives. */
+opf_status opf_comm_init_peer(int32_t world, int32_t rank, int32_t device, opf_comm** out);
 void opf_comm_free(opf_comm* c);
 /* Symmetric peer window for the fused all-reduce+RMSNorm kernel: allocate my
  * window (returns its 64-byte CUDA-IPC handle), exchange handles out of band,
@@ -156,6 +161,10 @@ opf_status opf_comm_window_open(opf_comm* c, const uint8_t* handles);
 /* `world` virtual ranks sharing one device (tests of the peer-memory protocol). */
 opf_status opf_comm_create_virtual(int32_t world, int32_t device, size_t stage_bytes, opf_comm** outs);
 opf_status opf_comm_window_error(opf_comm* c, uint32_t* err);
+/* Test hook: set every barrier epoch / flag / publish epoch of my window to
+ * `value` (all ranks the same, before any collective) — e.g. near 2^32 to
+ * exercise the wrap-safe barrier comparisons. */
+opf_status opf_comm_window_set_epochs(opf_comm* c, uint32_t value);
 /* Fused GEMM -> all-reduce calls that ran the peer-memory push protocol on
  * this rank (matmul_allreduce_add_rmsnorm; 0 = every call took the fallback). */
 opf_status opf_comm_push_calls(opf_comm* c, uint32_t* calls);
@@ -197,6 +206,10 @@ opf_status opf_session_prepare(opf_session* s, const char* strategy, void* strea
 typedef opf_status (*opf_schedule_fn)(opf_sched_ctx* ctx, void* user);
 opf_status opf_session_run_custom(opf_session* s, const char* cache_key, opf_schedule_fn fn,
                                   void* user, void* stream);
+/* Wait for the last run and fail with SchedulerError if any peer-window
+ * barrier of the runs so far timed out (a peer never arrived; the outputs are
+ * invalid).  opf_session_run also raises it for earlier runs it finds done. */
+opf_status opf_session_check(opf_session* s);
 opf_status opf_session_output(opf_session* s, const char* tensor, opf_view* out);
 /* Metrics JSON: plan-cache hits/misses, analysis ops, dispatches, launches,
  * copied elements, arena bytes, last-run trace summary. */

@@ -82,6 +82,9 @@ _SIGS = {
     "opf_comm_init": (C.c_int32, [C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32,
                                   C.POINTER(C.c_void_p)]),
     "opf_comm_free": (None, [C.c_void_p]),
+    "opf_comm_window_set_epochs": (C.c_int32, [C.c_void_p, C.c_uint32]),
+    "opf_comm_init_peer": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "opf_session_check": (C.c_int32, [C.c_void_p]),
     "opf_comm_window_alloc": (C.c_int32, [C.c_void_p, C.c_size_t, C.POINTER(C.c_uint8)]),
     "opf_comm_window_open": (C.c_int32, [C.c_void_p, C.POINTER(C.c_uint8)]),
     "opf_comm_create_virtual": (C.c_int32, [C.c_int32, C.c_int32, C.c_size_t, C.POINTER(C.c_void_p)]),

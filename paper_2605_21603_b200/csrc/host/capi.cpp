@@ -350,6 +350,19 @@ opf_status opf_comm_init(const uint8_t id[128], int32_t world, int32_t rank, int
   });
 }
 
+opf_status opf_comm_init_peer(int32_t world, int32_t rank, int32_t device, opf_comm** out) {
+  return guard([&] {
+    require(world >= 1 && world <= 8 && rank >= 0 && rank < world, Errc::ConfigError,
+            "peer communicator: need 1 <= world <= 8 and 0 <= rank < world");
+    auto c = std::make_unique<opf_comm>();
+    c->world = world;
+    c->rank = rank;
+    c->device = device;
+    OPF_CUDA(cudaSetDevice(device));
+    *out = c.release();
+  });
+}
+
 void opf_comm_free(opf_comm* c) {
   if (!c) return;
   if (c->nccl) nccl().CommDestroy(c->nccl);
@@ -397,6 +410,14 @@ opf_status opf_comm_window_error(opf_comm* c, uint32_t* err) {
   return guard([&] {
     need(c, "comm");
     *err = comm_window_error(c);
+  });
+}
+
+opf_status opf_comm_window_set_epochs(opf_comm* c, uint32_t value) {
+  return guard([&] {
+    need(c, "comm");
+    require(c->window_base != nullptr, Errc::ConfigError, "communicator has no window");
+    comm_window_set_epochs(c, value);
   });
 }
 
@@ -484,6 +505,13 @@ opf_status opf_session_run(opf_session* s, const char* strategy, void* stream) {
     auto cs = s->s->choose(spec, static_cast<cudaStream_t>(stream));
     auto strat = make_strategy(cs);
     s->s->run(*strat, "builtin:" + cs, static_cast<cudaStream_t>(stream));
+  });
+}
+
+opf_status opf_session_check(opf_session* s) {
+  return guard([&] {
+    need(s, "session");
+    s->s->check_window(true);
   });
 }
 

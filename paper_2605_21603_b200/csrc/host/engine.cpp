@@ -9,6 +9,7 @@
 #include <numeric>
 
 #include "opflow/comm.hpp"
+#include "opflow/p2p.cuh"
 #include "opflow/json.hpp"
 
 namespace opflow {
@@ -126,6 +127,38 @@ Session::~Session() {
     if (p) cudaFree(p);
   for (auto& kv : perms_) cudaFree(kv.second);
   if (arena_) cudaFree(arena_);
+  if (win_err_ev_) cudaEventDestroy(win_err_ev_);
+  if (win_err_host_) cudaFreeHost(win_err_host_);
+}
+
+void Session::check_window(bool wait) {
+  if (!win_err_pending_) return;
+  if (wait) {
+    OPF_CUDA(cudaEventSynchronize(win_err_ev_));
+  } else {
+    const cudaError_t q = cudaEventQuery(win_err_ev_);
+    if (q == cudaErrorNotReady) return;
+    OPF_CUDA(q);
+  }
+  win_err_pending_ = false;
+  if (*win_err_host_ != 0)
+    fail(Errc::SchedulerError,
+         "peer-window barrier timed out on rank " + std::to_string(comm_->rank) + " of " +
+             std::to_string(comm_->world) +
+             " (a peer never arrived): the outputs of that run are invalid and the window is poisoned");
+}
+
+void Session::note_window(cudaStream_t stream) {
+  WindowView w;
+  if (!window_view(comm_, &w)) return;
+  if (!win_err_host_) {
+    OPF_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&win_err_host_), sizeof(uint32_t), cudaHostAllocDefault));
+    *win_err_host_ = 0;
+    OPF_CUDA(cudaEventCreateWithFlags(&win_err_ev_, cudaEventDisableTiming));
+  }
+  OPF_CUDA(cudaMemcpyAsync(win_err_host_, w.err, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+  OPF_CUDA(cudaEventRecord(win_err_ev_, stream));
+  win_err_pending_ = true;
 }
 
 void Session::bind(const std::string& name, const opf_view& v) {
@@ -972,14 +1005,16 @@ std::string Session::choose(const std::string& spec, cudaStream_t stream) {
 }
 
 void Session::run(Scheduler& strat, const std::string& key_in, cudaStream_t stream) {
+  check_window(false);
   CompiledPlan* cp = prepare(strat, key_in, stream);
   last_ = cp;
   if (!cfg_.cuda_graph) {
     launch_plan(*cp, stream, false);
     OPF_CUDA(cudaGetLastError());
-    return;
+  } else {
+    OPF_CUDA(cudaGraphLaunch(cp->exec, stream));
   }
-  OPF_CUDA(cudaGraphLaunch(cp->exec, stream));
+  note_window(stream);
 }
 
 CompiledPlan* Session::prepare(Scheduler& strat, const std::string& key_in, cudaStream_t stream) {

@@ -202,9 +202,14 @@ opf_status launch_kind(const opf_op_ctx& c, const opf_view* in, int n_in, opf_vi
         // (prefill) ones go to NCCL's bandwidth-optimal algorithms, whose
         // per-rank NVLink traffic is 2(W-1)/W instead of (W-1) row-planes
         const int64_t msg = view_numel(in[0]) * (in[0].dtype == OPF_F32 ? 4 : in[0].dtype == OPF_I64 ? 8 : 2);
+        // a peer-only communicator (no NCCL) takes the peer path at every size
         if (comm && comm->world > 1 && !comm->peer_buf.empty() && comm->world == c.world_size &&
-            msg <= (int64_t{4} << 20) && allreduce_p2p(comm, in[0], out[0], rows, c.max_ctas, s))
+            (msg <= (int64_t{4} << 20) || !comm->nccl) &&
+            allreduce_p2p(comm, in[0], out[0], rows, c.max_ctas, s))
           return launch_status("AllReduce(p2p)");
+        if (comm && comm->world > 1 && !comm->nccl)
+          return op_error(Errc::ConfigError, "AllReduce: peer-only communicator and the message does not "
+                                             "fit its window (or is not bf16)");
         if (comm && comm->world > 1) {
           if (comm->world != c.world_size)
             return op_error(Errc::ConfigError, "AllReduce world_size " +

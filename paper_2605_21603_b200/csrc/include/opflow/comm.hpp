@@ -42,5 +42,6 @@ void comm_window_open(opf_comm* c, const void* handles);
 void comm_window_link_local(opf_comm* const* comms, int world);
 uint32_t comm_window_error(const opf_comm* c);
 uint32_t comm_push_calls(const opf_comm* c);
+void comm_window_set_epochs(opf_comm* c, uint32_t v);
 struct opf_view_fwd;
 }  // namespace opflow

@@ -237,6 +237,12 @@ class Session {
   void* export_arena(int64_t bytes);
   void set_peer_arenas(const std::vector<void*>& bases);
   opf_comm* comm() const { return comm_; }
+  // Peer-window health: every replay that may touch the communicator's window
+  // copies its sticky barrier-timeout word to pinned host memory behind the
+  // replay.  run() raises SchedulerError for an earlier replay whose copy has
+  // landed; check_window() waits for the last one.  A timed-out barrier means
+  // a peer never arrived, so that replay's activations are invalid.
+  void check_window(bool wait);
 
  private:
   std::unique_ptr<CompiledPlan> compile(const SchedContext& ctx, const std::string& key,
@@ -270,6 +276,10 @@ class Session {
   std::map<std::string, std::vector<double>> auto_times_;  // (auto spec | rows) -> ms per candidate
   bool dry_ = false;
   int64_t dry_rows_ = 0;
+  uint32_t* win_err_host_ = nullptr;   // pinned copy of the window's error word
+  cudaEvent_t win_err_ev_ = nullptr;   // recorded behind that copy
+  bool win_err_pending_ = false;
+  void note_window(cudaStream_t stream);
   CompiledPlan* lookup_or_build(Scheduler& strat, const std::string& key);
   std::vector<std::string> names_;  // storage for opf_op_ctx param names
 };

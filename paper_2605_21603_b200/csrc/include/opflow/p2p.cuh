@@ -22,7 +22,9 @@ namespace opflow {
 constexpr int kMaxWorld = 8;
 constexpr int kMaxCtas = 1024;
 constexpr int kBarrierSlot = kMaxCtas - 1;  // rank-wide barriers (EP dispatch / combine)
-constexpr int64_t kSpinLimit = 1ll << 24;   // ~seconds: error flag instead of a hung GPU
+// spin bound: a barrier that waits longer than this raises the window's error
+// flag instead of hanging the GPU (generous: ranks sharing one GPU time-slice)
+constexpr uint64_t kSpinTimeoutNs = 10ull * 1000 * 1000 * 1000;
 
 struct PeerPtrs {
   const void* buf[kMaxWorld];  // staging region of each rank
@@ -82,6 +84,28 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spin until *p reaches `target` in wrap-safe serial-number order (epochs and
+// counters are u32 that grow forever in device memory).  Returns false, after
+// setting *err, when kSpinTimeoutNs passes first.
+__device__ __forceinline__ bool spin_until_reached(const uint32_t* p, uint32_t target, uint32_t* err) {
+  if (static_cast<int32_t>(ld_acquire_sys(p) - target) >= 0) return true;
+  const uint64_t t0 = global_ns();
+  uint32_t n = 0;
+  while (static_cast<int32_t>(ld_acquire_sys(p) - target) < 0) {
+    if ((++n & 255u) == 0 && global_ns() - t0 > kSpinTimeoutNs) {
+      atomicExch(err, 1u);
+      return false;
+    }
+  }
+  return true;
+}
+
 // Barrier of CTA slot `slot` across all ranks; called by every thread of the CTA.
 __device__ __forceinline__ bool slot_barrier(const PeerPtrs& pp, uint32_t* my_epoch, int slot, int world, int rank,
                                              uint32_t* err) {
@@ -92,16 +116,11 @@ __device__ __forceinline__ bool slot_barrier(const PeerPtrs& pp, uint32_t* my_ep
     const uint32_t e = ++my_epoch[slot];
     __threadfence_system();
     for (int p = 0; p < world; ++p) st_release_sys(pp.flags[p] + slot * kMaxWorld + rank, e);
-    for (int p = 0; p < world; ++p) {
-      int64_t spins = 0;
-      while (ld_acquire_sys(pp.flags[rank] + slot * kMaxWorld + p) < e) {
-        if (++spins > kSpinLimit) {
-          atomicExch(err, 1u);
-          ok = 0;
-          break;
-        }
+    for (int p = 0; p < world; ++p)
+      if (!spin_until_reached(pp.flags[rank] + slot * kMaxWorld + p, e, err)) {
+        ok = 0;
+        break;
       }
-    }
   }
   __syncthreads();
   return ok != 0;

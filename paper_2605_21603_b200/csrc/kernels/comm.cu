@@ -151,6 +151,9 @@ opf_status launch_ar_norm(const opf_comm* comm, const opf_view& o, const opf_vie
   if (smem > 48 * 1024) return op_error(Errc::ShapeMismatch, "fused norm: row too wide");
   const T* src = vptr<T>(o);
   float scale = static_cast<float>(ws);
+  if (comm && comm->world > 1 && !comm->nccl)
+    return op_error(Errc::ConfigError, "allreduce_norm: peer-only communicator and the message does not "
+                                       "fit its window");
   if (comm && comm->world > 1) {
     // NCCL all-reduce into the workspace, then one fused add+norm pass.
     T* red = static_cast<T*>(workspace);

@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "opflow/comm.hpp"
 #include "opflow/device.hpp"
@@ -379,13 +380,7 @@ __global__ void __launch_bounds__(kThreads) push_reduce_norm_kernel(
     if (threadIdx.x == 0) {
       ok = 1;
       const uint32_t need = static_cast<uint32_t>(world * n_tiles);
-      int64_t spins = 0;
-      while (ld_acquire_sys(cnt + s) < need)
-        if (++spins > kSpinLimit) {
-          atomicExch(err, 1u);
-          ok = 0;
-          break;
-        }
+      if (!spin_until_reached(cnt + s, need, err)) ok = 0;
     }
     __syncthreads();
     if (!ok) return;
@@ -443,13 +438,7 @@ __global__ void __launch_bounds__(kThreads) push_reduce_norm_kernel(
     if (threadIdx.x == 0) {
       ok = 1;
       const uint32_t* qpub = reinterpret_cast<const uint32_t*>(theirs + push_off) + kMaxSlabs;
-      int64_t spins = 0;
-      while (static_cast<int32_t>(ld_acquire_sys(qpub + s) - epoch) < 0)
-        if (++spins > kSpinLimit) {
-          atomicExch(err, 1u);
-          ok = 0;
-          break;
-        }
+      if (!spin_until_reached(qpub + s, epoch, err)) ok = 0;
     }
     __syncthreads();
     if (!ok) return;
@@ -536,6 +525,19 @@ uint32_t comm_window_error(const opf_comm* c) {
   OPF_CUDA(cudaMemcpy(&e, static_cast<char*>(c->window_base) + eo + sizeof(uint32_t) * kMaxCtas,
                       sizeof(e), cudaMemcpyDeviceToHost));
   return e;
+}
+
+void comm_window_set_epochs(opf_comm* c, uint32_t v) {
+  size_t fo, eo;
+  window_layout(c->peer_bytes, &fo, &eo);
+  char* base = static_cast<char*>(c->window_base);
+  const std::vector<uint32_t> flags(static_cast<size_t>(kMaxCtas) * kMaxWorld, v);
+  OPF_CUDA(cudaMemcpy(base + fo, flags.data(), flags.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  OPF_CUDA(cudaMemcpy(base + eo, flags.data(), kMaxCtas * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  // push protocol: publish epochs [kMaxSlabs] + the call epoch (arrival counters stay 0)
+  char* push = base + window_push_off(c->peer_bytes);
+  OPF_CUDA(cudaMemcpy(push + sizeof(uint32_t) * kMaxSlabs, flags.data(), (kMaxSlabs + 1) * sizeof(uint32_t),
+                      cudaMemcpyHostToDevice));
 }
 
 uint32_t comm_push_calls(const opf_comm* c) {

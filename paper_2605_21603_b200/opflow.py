@@ -513,6 +513,19 @@ class Comm:
         self._h = h
 
     @staticmethod
+    def peer(world: int, rank: int, device: int) -> "Comm":
+        """Peer-window-only communicator (no NCCL): every collective runs over
+        the CUDA-IPC window at any message size.  Call enable_window() next.
+        Works for ranks that cannot form an NCCL communicator, e.g. two
+        processes sharing one GPU."""
+        c = Comm.__new__(Comm)
+        c.world, c.rank = world, rank
+        h = C.c_void_p()
+        check(lib().opf_comm_init_peer(world, rank, device, C.byref(h)))
+        c._h = h
+        return c
+
+    @staticmethod
     def unique_id() -> bytes:
         arr = (C.c_uint8 * 128)()
         check(lib().opf_comm_unique_id(arr))
@@ -545,6 +558,10 @@ class Comm:
         e = C.c_uint32()
         check(lib().opf_comm_window_error(self._h, C.byref(e)))
         return e.value
+
+    def set_epochs(self, value: int) -> None:
+        """Test hook: seed every barrier epoch / flag of this rank's window."""
+        check(lib().opf_comm_window_set_epochs(self._h, value & 0xFFFFFFFF))
 
     def push_calls(self) -> int:
         """Fused GEMM -> all-reduce calls that used the peer-memory push path."""
@@ -590,6 +607,11 @@ class Session:
             return
         spec = json.dumps(strategy if strategy is not None else {"name": "sequential"})
         check(lib().opf_session_run(self._h, spec.encode(), s))
+
+    def check(self) -> None:
+        """Wait for the last run; raise SchedulerError if a peer-window barrier
+        of any run so far timed out (its outputs are invalid)."""
+        check(lib().opf_session_check(self._h))
 
     def prepare(self, strategy: Any = None, stream=None) -> None:
         """Plan + prepack + capture without launching (virtual peer ranks on one

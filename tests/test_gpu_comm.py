@@ -57,3 +57,36 @@ def test_fused_allreduce_add_rmsnorm_virtual_ranks(cuda, world, ar_mode, rows):
     want = sum(p.float().cpu().numpy() for p in parts)
     for r in range(world):
         assert rel_err(outs[r].float().cpu().numpy(), want) < 1e-2
+
+
+@pytest.mark.parametrize("ar_mode", [1, 2, 3])
+def test_barrier_epochs_wrap_around(cuda, ar_mode):
+    """Epochs and flags are u32 that grow forever in device memory; seeded just
+    below 2^32, twenty calls cross the wrap.  The barrier compares in serial-
+    number order, so every call still waits for its peers (right results, no
+    timeout) — an unsigned `<` would let a rank run ahead after the wrap."""
+    import torch
+    world, rows, H = 2, 64, 4096
+    comms = of.Comm.virtual(world, 0, 3 * rows * H * 2)
+    for c in comms:
+        c.set_epochs(0xFFFFFFFF - 6)
+    rng = np.random.default_rng(5)
+    tb = lambda a: torch.from_numpy(a.astype(np.float32)).cuda().to(torch.bfloat16)
+    x = tb(rng.uniform(-1, 1, (rows, H)))
+    g = tb(1 + 0.1 * rng.uniform(-1, 1, H))
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    op = {"name": "f", "kind": "Custom", "inputs": [], "outputs": [],
+          "attrs": {"custom_name": "allreduce_add_rmsnorm", "world_size": world,
+                    "params": {"eps": 1e-5, "ar_mode": ar_mode}}}
+    for it in range(20):
+        parts = [tb(rng.uniform(-1, 1, (rows, H))) for _ in range(world)]
+        outs = [(torch.empty_like(x), torch.empty_like(x)) for _ in range(world)]
+        torch.cuda.synchronize()
+        for r in range(world):
+            of.launch(op, [parts[r], x, g], list(outs[r]), rows, streams[r], comm=comms[r], max_ctas=8)
+        torch.cuda.synchronize()
+        s = x.float().cpu().numpy() + sum(p.float().cpu().numpy() for p in parts)
+        for r in range(world):
+            assert rel_err(outs[r][0].float().cpu().numpy(), s) < 1e-2, (it, r)
+    for c in comms:
+        assert c.window_error() == 0

@@ -1,0 +1,94 @@
+"""GPU: the peer-memory collectives across real processes.
+
+Two ranks = two processes = two CUDA contexts, both on cuda:0 (gpurun leases
+one GPU; on a multi-GPU box the same worker runs one rank per device).  Each
+rank maps the other's window and session arena through CUDA IPC handles
+exchanged over gloo, so the protocol the virtual-rank tests cannot reach runs
+for real: IPC mapping, system-scope release/acquire flag barriers between
+contexts (which time-slice on one GPU), device epochs across replays, the
+GEMM epilogue pushing into another process's memory, and the engine's
+barrier-timeout check.  Every rank's outputs must match the unsharded oracle
+(bf16 normwise rel err <= 2e-2, BASELINE north_star)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("built")]
+ROOT = Path(__file__).resolve().parent.parent
+TOL = 2e-2
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def run_ranks(case: str, world: int = 2, timeout: float = 240.0):
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    procs = [subprocess.Popen([sys.executable, str(ROOT / "tests" / "mp_worker.py"), "--rank", str(r),
+                               "--world", str(world), "--case", case],
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, env=env, cwd=ROOT)
+             for r in range(world)]
+    outs = []
+    try:
+        for p in procs:
+            out, err = p.communicate(timeout=timeout)
+            outs.append((p.returncode, out, err))
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    res = []
+    for rc, out, err in outs:
+        assert rc == 0, f"rank failed rc={rc}\n{out[-2000:]}\n{err[-4000:]}"
+        line = [l for l in out.splitlines() if l.startswith("RESULT ")]
+        assert line, out[-2000:] + err[-2000:]
+        res.append(json.loads(line[-1][7:]))
+    return res
+
+
+def _check_errors(res):
+    for r in res:
+        assert r["window_error"] == 0, r
+        bad = {k: v for k, v in r["errors"].items() if not v < TOL}
+        assert not bad, (r["rank"], bad)
+
+
+def test_multiproc_allreduce_forms():
+    res = run_ranks("ar")
+    _check_errors(res)
+    assert {"pull_r64_h", "twoshot_r61_h", "push_r61_x1", "auto_r64_h", "allreduce_r1024"} <= set(res[0]["errors"])
+
+
+def test_multiproc_tp_llama_layers():
+    res = run_ranks("tp")
+    _check_errors(res)
+    # replicated activations are bit-identical across the two processes
+    assert res[0]["digest"] == res[1]["digest"]
+
+
+def test_multiproc_gemm_push_allreduce():
+    res = run_ranks("tp_fuse")
+    _check_errors(res)
+    assert res[0]["digest"] == res[1]["digest"]
+    # 3 replays x (unsplit: o, down, o, down = 4? the builder's 2 layers) -- the
+    # push path must have run on every eligible call, not fallen back
+    assert res[0]["push_calls"] > 0 and res[0]["push_calls"] == res[1]["push_calls"]
+
+
+def test_multiproc_expert_parallel_all_to_all():
+    res = run_ranks("ep")
+    _check_errors(res)
+    assert all(r["copied_elements"] == 0 for r in res)
+
+
+def test_multiproc_barrier_timeout_raises():
+    res = run_ranks("timeout", timeout=120)
+    assert res[0]["raised"] == "SchedulerError", res[0]
+    assert res[0]["window_error"] == 1
