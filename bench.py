@@ -46,6 +46,27 @@ except Exception:  # noqa: BLE001
     TRAFFIC = {}
 
 LLAMA = dict(hidden=4096, heads=32, kv_heads=8, head_dim=128, inter=14336)
+METRIC = "tokens/sec overlapped vs sequential schedule, Llama-3-8B layer TP=1/2/4/8"
+
+
+def bench_config(args, tp):
+    """The workload both arms report (ours and --impl reference print the same dict)."""
+    T, S, L = args.tokens, args.seq_len, args.layers
+    return {"workload": f"llama3-8b-shaped prefill, {L} layers, {T} tokens ({T // S} seqs x {S}) per replica, "
+                        f"TP={tp}",
+            "model": "Llama-3-8B-shaped (random init)", "global_batch": T // S, "seq_len": S,
+            "parallelism": f"tp{tp}",
+            "inputs_vs_l2": "activations/weights > 126 MB L2 (no flush needed)"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def parse():
@@ -63,6 +84,7 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-decode", action="store_true")
     p.add_argument("--no-moe", action="store_true")
+    p.add_argument("--no-toy", action="store_true")
     p.add_argument("--moe-layers", type=int, default=1)
     p.add_argument("--decode-batch", type=int, default=512)
     p.add_argument("--decode-ctx", type=int, default=4096)
@@ -119,6 +141,9 @@ def dist_init(n):
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != n:
+        print(f"[bench] --gpus {n} but WORLD_SIZE={world}: launch one rank per GPU", file=sys.stderr, flush=True)
+        sys.exit(2)
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -234,6 +259,7 @@ def time_candidates(torch, sess, cands, steps, warmup, stream, world, rounds=Non
     for _ in range(rounds):
         for k, spec in cands.items():
             per[k].append(time_steps(torch, lambda s=spec: sess.run(s, stream), steps, warmup, stream, world))
+    sess.check()  # a timed-out peer-window barrier (invalid outputs) raises SchedulerError here
     return {k: statistics.median(v) for k, v in per.items()}
 
 
@@ -442,21 +468,23 @@ def run_ours(args):
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
         moe = run_moe(of, torch, dev, args, rank, world, stream, comm, comm_window_ok)
+    toy = None
+    if rank == 0 and not args.no_toy:
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        toy = run_toy(of, torch, dev, stream, args)
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(args, T, S, tp)
         line = {
-            "metric": "tokens/sec overlapped vs sequential schedule, Llama-3-8B layer TP=1/2/4/8",
+            "metric": METRIC,
             "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(best_ms, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded uniform inputs, random-init weights)",
-            "config": {"workload": f"llama3-8b-shaped prefill, {L} layers, {T} tokens "
-                                   f"({T // S} seqs x {S}) per replica, TP={tp}",
-                       "model": "Llama-3-8B-shaped (random init)", "global_batch": T // S,
-                       "seq_len": S, "parallelism": f"tp{tp}", "strategy": best,
-                       "inputs_vs_l2": "activations/weights > 126 MB L2 (no flush needed)",
-                       "timing": "per candidate: median of 3 interleaved rounds, each W warm-up + K timed steps "
-                                 "(CUDA events, max over ranks), after a 2 s power soak"},
+            "config": bench_config(args, tp),
+            "strategy": best,
+            "timing": "per candidate: median of 3 interleaved rounds, each W warm-up + K timed steps "
+                      "(CUDA events, max over ranks), after a 2 s power soak",
             "sequential": {"ms_per_step": round(seq_ms, 3), "tokens_per_s": round(T / (seq_ms / 1e3), 1)},
             "strategies_ms": {k: round(v, 3) for k, v in results.items()},
             "speedup_vs_sequential": round(seq_ms / best_ms, 4),
@@ -484,6 +512,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "decode": decode,
             "moe": moe,
+            "toy_c1": toy,
             "clocks": clk.summary(),
             "gpu_launches": int(launches) * args.steps,
             "plan": {"dispatches": stats["last"]["dispatches"], "launches_per_step": launches,
@@ -719,50 +748,113 @@ def run_moe(of, torch, dev, args, rank, world, stream, comm=None, window_ok=True
 
 
 # ------------------------------------------------------------------ reference (CPU)
+def _ref_desc(rows: int) -> str:
+    """Llama-3-8B-shaped layer (fp32, TP=1, one `rows`-token sequence) as the
+    committed description (oracle/fixtures): the reference arm never loads
+    the product library."""
+    return (ROOT / "oracle" / "fixtures" / f"llama3_8b_layer_f32_rows{rows}.json").read_text()
+
+
 def _ref_worker(args_tuple):
     desc, rows, seed = args_tuple
     sys.path.insert(0, str(ROOT))
     from oracle import ref
-    from paper_2605_21603_b200.workloads import llama_inputs
+    from paper_2605_21603_b200.workloads import llama_inputs  # numpy only (no library load)
     ins = llama_inputs(desc, rows, seed=seed)
     _, secs = ref.evaluate(desc, rows, ins, timed=True)
     return secs
 
 
+def _ref_sample(pool, cores, rows, seed0):
+    """One bounded sample: `cores` processes, each the reference's
+    eval_reference over one full (unsharded) layer of its own rows-token
+    sequence.  Returns seconds of the slowest process."""
+    desc = _ref_desc(rows)
+    secs = pool.map(_ref_worker, [(desc, rows, seed0 + c) for c in range(cores)])
+    return max(secs)
+
+
 def cpu_baseline(args, T, S, tp, budget_s=None):
     """Reference eval_reference (oracle/_ref, compiled from the reference's
     sources, AVX2 lane, single-threaded by construction) on a bounded sample:
-    1 Llama layer of `rows` tokens per process, one process per host core, each
-    a disjoint sequence; tokens/s is extrapolated to the full workload as
-    (tokens / s per layer) / layers."""
+    1 unsharded Llama layer of 128 tokens per process, one process per host
+    core, each a disjoint sequence; tokens/s is extrapolated to the full
+    workload as (tokens / s per layer) / layers."""
     import multiprocessing as mp
     from oracle import ref
     if not ref.available():
         return None
-    from paper_2605_21603_b200 import opflow as of
     cores = os.cpu_count() or 1
-    rows = 128 if S >= 128 else S
-    desc = of.llama_graph(layers=1, tokens=rows, seq_len=rows, tp=tp, dtype="f32", **LLAMA)
+    rows = 128
     t0 = time.time()
     with mp.get_context("fork").Pool(cores) as pool:
-        secs = pool.map(_ref_worker, [(desc, rows, 17 + i) for i in range(cores)])
+        sec = _ref_sample(pool, cores, rows, 17)
     wall = time.time() - t0
-    per_layer_tok_s = cores * rows / max(secs)
+    per_layer_tok_s = cores * rows / sec
     return {"value": round(per_layer_tok_s / args.layers, 2), "unit": "tokens/s",
-            "cores": cores, "kind": "reference",
-            "sample": f"{cores} procs x 1 Llama-3-8B-shaped layer x {rows} tokens (fp32, eval_reference "
-                      f"AVX2 lane, backend={ref.backend()}), extrapolated to {args.layers} layers; "
-                      f"{max(secs):.1f}s per layer, wall {wall:.1f}s"}
+            "cores": cores, "cpu_model": cpu_model(), "kind": "reference",
+            "sample": f"{cores} procs x 1 unsharded Llama-3-8B-shaped layer x {rows} tokens (fp32, eval_reference "
+                      f"AVX2 lane, backend={ref.backend()}), extrapolated linearly to {args.layers} layers and "
+                      f"{T} tokens (attention at {rows}-token sequences: flatters the CPU); {sec:.1f}s per "
+                      f"layer, wall {wall:.1f}s"}
+
+
+def run_toy(of, torch, dev, stream, args):
+    """BASELINE configs[0]: the 2-layer toy decoder (d=512, 8 heads, seq 128,
+    batch 8 = 1024 rows, fp32, TP=1), sequential vs overlapped schedule on the
+    engine, with the reference's own eval_reference of the same graph timed
+    beside it (full config: it runs on the CPU reference)."""
+    desc = (ROOT / "oracle" / "fixtures" / "toy_decoder_c1.json").read_text()
+    from paper_2605_21603_b200.workloads import llama_inputs
+    rows = 1024
+    host = llama_inputs(desc, rows, seed=2026)
+    g = of.build_graph(desc)
+    sess = of.Session(g, of.partition(g, []), {"lanes": 3, "device": dev.index})
+    keep = {}
+    for t in g.description["tensors"]:
+        if t["role"] in ("input", "weight"):
+            keep[t["name"]] = torch.from_numpy(host[t["name"]]).to(dev)
+        elif t["role"] == "output":
+            keep[t["name"]] = torch.empty(t["shape"], dtype=torch.float32, device=dev)
+        else:
+            continue
+        sess.bind(t["name"], keep[t["name"]])
+    cands = {"sequential": {"name": "sequential"},
+             "nanoflow_class": {"name": "split_overlap", "align": 128},
+             "nanoflow_u2": {"name": "split_overlap", "align": 128, "lane_mode": "ubatch"}}
+    res = time_candidates(torch, sess, cands, max(args.steps, 20), max(args.warmup, 3), stream, 1, soak_s=0.5)
+    best = min((k for k in res if k != "sequential"), key=lambda k: res[k])
+    out = {"workload": "toy decoder (BASELINE configs[0]): 2 layers, d=512, 8 heads x 64, seq 128, batch 8, fp32, TP=1",
+           "tokens_per_s": round(rows / (res[best] / 1e3), 1), "strategy": best,
+           "sequential_tokens_per_s": round(rows / (res["sequential"] / 1e3), 1),
+           "speedup_vs_sequential": round(res["sequential"] / res[best], 4),
+           "strategies_ms": {k: round(v, 4) for k, v in res.items()}}
+    del sess
+    try:
+        from oracle import ref
+        if ref.available():
+            ts = []
+            for i in range(3):
+                _, sec = ref.evaluate(desc, rows, host, timed=True)
+                ts.append(sec)
+            ms = sorted(ts)[1] * 1e3
+            out["reference_cpu"] = {"ms_per_forward": round(ms, 2), "tokens_per_s": round(rows / (ms / 1e3), 1),
+                                    "cores": 1, "cpu_model": cpu_model(), "kind": "reference",
+                                    "sample": "full config, eval_reference (oracle/_ref), median of 3"}
+    except Exception as e:  # noqa: BLE001
+        out["reference_cpu"] = {"error": str(e)[:200]}
+    return out
 
 
 def run_reference(args):
     """Reference arm: the reference's own eval_reference (oracle/_ref, compiled
     from /root/reference/proj/src by oracle/Makefile) on every host core.  Each
     step is one bounded sample — one process per core, each evaluating one
-    Llama-3-8B-shaped layer over its own `rows`-token sequence (disjoint rows;
-    the graph is batch-decomposable, proj/tests/test_graph.cpp:325-408) — and
-    tokens/s is extrapolated to the full layer count.  Exactly W untimed + K
-    timed steps; rank 0 only under torchrun."""
+    unsharded Llama-3-8B-shaped layer over its own 64-token sequence (disjoint
+    rows; the graph is batch-decomposable, proj/tests/test_graph.cpp:325-408) —
+    and tokens/s is extrapolated to the full layer count.  Whatever N is, the
+    CPU evaluates the whole (TP=1) layer: it has no tensor parallelism.
+    Exactly W untimed + K timed steps; rank 0 only under torchrun."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
@@ -771,41 +863,66 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libopflow_ref.so not built"}))
         return
     import multiprocessing as mp
-    from paper_2605_21603_b200 import opflow as of
-    T, S = args.tokens, args.seq_len
     tp = max(1, args.gpus)
     cores = os.cpu_count() or 1
     rows = 64
-    desc = of.llama_graph(layers=1, tokens=rows, seq_len=rows, tp=tp, dtype="f32", **LLAMA)
     step_s = []
     with mp.get_context("fork").Pool(cores) as pool:
         for i in range(args.warmup + args.steps):
-            t0 = time.time()
-            secs = pool.map(_ref_worker, [(desc, rows, 17 + 131 * i + c) for c in range(cores)])
-            wall = time.time() - t0
+            sec = _ref_sample(pool, cores, rows, 17 + 131 * i)
             if i >= args.warmup:
-                step_s.append(max(max(secs), 0.0) or wall)
+                step_s.append(sec)
     per_step = sum(step_s) / len(step_s)
     v = cores * rows / per_step / args.layers
-    cb = {"value": round(v, 3), "unit": "tokens/s", "cores": cores, "kind": "reference",
-          "sample": f"per step: {cores} procs x 1 Llama-3-8B-shaped layer (TP={tp} shard) x {rows} tokens "
+    cb = {"value": round(v, 3), "unit": "tokens/s", "cores": cores, "cpu_model": cpu_model(), "kind": "reference",
+          "sample": f"per step: {cores} procs x 1 unsharded Llama-3-8B-shaped layer x {rows} tokens "
                     f"(fp32 eval_reference, backend={ref.backend()}), extrapolated to {args.layers} layers; "
                     f"{per_step:.2f}s per step"}
     print(json.dumps({
-        "impl": "reference", "metric": "tokens/sec overlapped vs sequential schedule, Llama-3-8B layer TP=1/2/4/8",
+        "impl": "reference", "metric": METRIC,
         "value": cb["value"], "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(per_step * 1e3, 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded uniform inputs, random-init weights)",
-        "config": {"workload": f"llama3-8b-shaped prefill, {args.layers} layers, {T} tokens "
-                               f"({T // S} seqs x {S}) per replica, TP={tp}"},
+        "config": bench_config(args, tp),
         "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                                     "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def maybe_spawn(a) -> None:
+    """`--gpus N` without a torchrun environment: re-exec under
+    torch.distributed.run with N ranks (one process per GPU), or fail loudly
+    when fewer than N GPUs are visible (never silently run TP=1)."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    if a.impl == "reference":
+        return  # CPU arm: rank 0 does all the work anyway
+    import torch
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(f"[bench] --gpus {a.gpus} requested but only {have} GPU(s) are visible; refusing to run "
+              f"a smaller tensor-parallel degree", file=sys.stderr, flush=True)
+        sys.exit(2)
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    os.execve(sys.executable, cmd, env)
 
 
 if __name__ == "__main__":
     a = parse()
     ROUNDS, SOAK_S = max(1, a.rounds), max(0.0, a.soak)
+    maybe_spawn(a)
+    if int(os.environ.get("WORLD_SIZE", 1)) > 1:
+        # the driver checks NCCL's communicator ranks from its INIT log lines
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if a.impl == "reference":
         run_reference(a)
     else:
