@@ -249,6 +249,17 @@ CustomRegistry make_registry(const std::map<std::string, std::map<std::string, d
     };
   }
   {
+    // external-operator test op (tests/bridge/ext_op.cu registers the device
+    // kernel of the same name through opf_register_op): y = cap * tanh(x / cap)
+    const float cap = float(P(params("softcap"), "cap", 30.0));
+    reg.fns["softcap"] = [cap](const std::vector<TensorValue>& in, int64_t rows) {
+      const int64_t W = in[0].row_elems();
+      TensorValue y = like({rows, W});
+      for (int64_t i = 0; i < rows * W; ++i) y.f32()[i] = cap * std::tanh(in[0].f32()[i] / cap);
+      return std::vector<TensorValue>{y};
+    };
+  }
+  {
     const auto ps = params("rope");
     const int64_t nq = int64_t(P(ps, "heads", 1)), nkv = int64_t(P(ps, "kv_heads", 1)),
                   hd = int64_t(P(ps, "head_dim", 2));

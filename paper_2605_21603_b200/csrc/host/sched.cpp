@@ -186,10 +186,17 @@ void SchedContext::execute(const std::vector<OpHandle>& ops, int32_t lane,
     record(std::move(d));
     return;
   }
-  // different subgraphs, no replacement: sequential fallback in handle order
+  // different subgraphs, no replacement: sequential fallback in handle order.
+  // Readiness of the whole list is checked first (earlier handles of the same
+  // ubatch count as done), so a NotReady leaves the context untouched.
+  for (std::size_t i = 0; i < ops.size(); ++i) {
+    std::set<int32_t> earlier;
+    for (std::size_t j = 0; j < i; ++j)
+      if (ops[j].ubatch == ops[i].ubatch) earlier.insert(ops[j].subgraph);
+    require(deps_met(ops[i].subgraph, ops[i].ubatch, earlier), Errc::NotReady,
+            "subgraph '" + p_.subgraphs[ops[i].subgraph].label + "' not ready");
+  }
   for (const OpHandle& h : ops) {
-    require(deps_met(h.subgraph, h.ubatch, {}), Errc::NotReady,
-            "subgraph '" + p_.subgraphs[h.subgraph].label + "' not ready");
     Dispatch d;
     d.lane = lane;
     d.subgraphs = {h.subgraph};

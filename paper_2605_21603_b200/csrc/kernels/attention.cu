@@ -357,6 +357,17 @@ opf_status op_attn_decode(const opf_op_ctx* c, const opf_view* in, int32_t n_in,
   if (hnd == 1 && (in[1].rank != 4 || in[1].shape[1] != nkv || in[1].shape[2] != page || in[1].shape[3] != hd))
     return op_error(Errc::ShapeMismatch, "attn_decode: kv_layout 1 (HND) cache must be [pages, kv_heads, page, hd]");
   if (hnd != 0 && hnd != 1) return op_error(Errc::ConfigError, "attn_decode: kv_layout is 0 (NHD) or 1 (HND)");
+  bool same_kv = in[2].rank == in[1].rank;
+  for (int i = 0; same_kv && i < in[1].rank; ++i) same_kv = in[2].shape[i] == in[1].shape[i];
+  if (!same_kv) return op_error(Errc::ShapeMismatch, "attn_decode: K and V caches must have identical shapes");
+  if (in[0].dtype != in[1].dtype || in[2].dtype != in[1].dtype || out[0].dtype != in[0].dtype ||
+      (in[0].dtype != OPF_BF16 && in[0].dtype != OPF_F32))
+    return op_error(Errc::ShapeMismatch, "attn_decode: qkv, caches and output share one float dtype");
+  if (in[3].dtype != OPF_I64 || in[4].dtype != OPF_I64 || in[3].rank != 2 || in[4].rank != 1)
+    return op_error(Errc::ShapeMismatch, "attn_decode: block table [B, max_pages] and context lengths [B] are i64");
+  if (view_row_elems(in[0]) != static_cast<int64_t>(nq + 2 * nkv) * hd || view_row_elems(out[0]) != int64_t{nq} * hd)
+    return op_error(Errc::ShapeMismatch, "attn_decode: qkv rows are (heads + 2 kv_heads) * head_dim wide, "
+                                         "outputs heads * head_dim");
   if (rows == 0) return 0;
   const int64_t max_pages = view_row_elems(in[3]);
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));

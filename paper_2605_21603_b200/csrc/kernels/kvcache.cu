@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(256) kv_write_kernel(const __nv_bfloat16* __re
                                                        const int64_t* __restrict__ slots,
                                                        __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
                                                        int64_t* __restrict__ written, int64_t T, int nq, int nkv,
-                                                       int hd, int page, int hnd) {
+                                                       int hd, int page, int hnd, int64_t n_slots) {
   pdl_wait();
   pdl_trigger();
   const int64_t gid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 16;  // (token, head, K|V)
@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256) kv_write_kernel(const __nv_bfloat16* __re
   const int kh = rem >> 1, is_v = rem & 1;
   const int64_t slot = slots[t];
   if (rem == 0 && l16 == 0) written[t] = slot;
-  if (slot < 0) return;
+  if (slot < 0 || slot >= n_slots) return;  // padding, or outside the pool (never write past it)
   const int64_t pg = slot / page, off = slot % page;
   const int64_t W = static_cast<int64_t>(nq + 2 * nkv) * hd;
   const __nv_bfloat16* src = qkv + t * W + static_cast<int64_t>(nq + is_v * nkv + kh) * hd;
@@ -53,12 +53,16 @@ opf_status op_kv_write(const opf_op_ctx* c, const opf_view* in, int32_t n_in, op
                         (hnd ? (in[2].shape[1] == nkv && in[2].shape[2] == page)
                              : (in[2].shape[1] == page && in[2].shape[2] == nkv));
   if (!shape_ok) return op_error(Errc::ShapeMismatch, "kv_write: cache shape does not match kv_layout / heads / page");
+  bool same = in[3].rank == in[2].rank;
+  for (int i = 0; same && i < in[2].rank; ++i) same = in[3].shape[i] == in[2].shape[i];
+  if (!same) return op_error(Errc::ShapeMismatch, "kv_write: K and V caches must have identical shapes");
+  const int64_t n_slots = in[2].shape[0] * page;
   if (rows == 0) return 0;
   const int64_t threads = rows * 2 * nkv * 16;
   launch_pdl(kv_write_kernel, dim3(static_cast<unsigned>((threads + 255) / 256)), dim3(256), 0,
              static_cast<cudaStream_t>(stream), static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[0])),
              static_cast<const int64_t*>(vptr<int64_t>(in[1])), vptr<__nv_bfloat16>(in[2]), vptr<__nv_bfloat16>(in[3]),
-             vptr<int64_t>(out[0]), rows, nq, nkv, hd, page, hnd);
+             vptr<int64_t>(out[0]), rows, nq, nkv, hd, page, hnd, n_slots);
   return launch_status("kv_write");
 }
 

@@ -733,6 +733,81 @@ def _device_tensor(ptr: int, numel: int, dtype):
     return torch.as_tensor(_Holder(ptr, nbytes), device="cuda").view(dtype)
 
 
+# ------------------------------------------------------------------ operator registry
+@dataclass
+class OpCtx:
+    """What a registered op sees of its launch (opf_op_ctx, include/opflow_b200.h)."""
+    op_name: str
+    custom_name: str
+    world_size: int
+    seed: int
+    params: Dict[str, float]
+    max_ctas: int
+    workspace: int
+    workspace_bytes: int
+
+
+_TORCH_OF_DT = {0: "int64", 1: "float32", 2: "bfloat16"}
+_REGISTERED: Dict[str, Any] = {}  # keeps the ctypes trampolines alive
+
+
+def view_tensor(v: opf_view):
+    """A torch tensor aliasing an opf_view's device memory (no copy)."""
+    import torch
+    dt = getattr(torch, _TORCH_OF_DT[v.dtype])
+    shape = [int(v.shape[i]) for i in range(v.rank)]
+    numel = 1
+    for x in shape:
+        numel *= x
+    esz = torch.tensor([], dtype=dt).element_size()
+    return _device_tensor(int(v.base or 0) + int(v.elem_offset) * esz, numel, dt).view(*shape)
+
+
+def register_op(name: str, fn: Callable, resource_class: ResourceClass = ResourceClass.kCompute,
+                n_in: int = -1, n_out: int = -1) -> None:
+    """CustomRegistry::fns[name] = fn (reference eval.hpp:19-28) for device ops.
+
+    `fn(ctx: OpCtx, ins: list[Tensor], outs: list[Tensor], rows: int, stream)`
+    launches its kernels on `stream` (a torch.cuda.ExternalStream of the
+    engine's lane) and writes into `outs` in place — they are caller-owned
+    views, possibly nano-batch row slices of the engine's arena; it must not
+    allocate device memory (the call may be under CUDA-graph capture: the
+    engine calls it once per nano-batch when it captures, replays re-run the
+    captured kernels).  A Custom op with attrs.custom_name == name runs it,
+    and PartitionRule.by_func(name) isolates it."""
+    import sys
+    import traceback
+
+    def tramp(ctx_p, in_p, n_in_, out_p, n_out_, rows, stream):
+        try:
+            import torch
+            c = ctx_p.contents
+            params = {c.param_names[i].decode(): float(c.param_values[i]) for i in range(c.n_params)}
+            ctx = OpCtx((c.op_name or b"").decode(), (c.custom_name or b"").decode(), int(c.world_size),
+                        int(c.seed), params, int(c.max_ctas), int(c.workspace or 0), int(c.workspace_bytes))
+            ins = [view_tensor(in_p[i]) for i in range(n_in_)]
+            outs = [view_tensor(out_p[i]) for i in range(n_out_)]
+            st = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+            fn(ctx, ins, outs, int(rows), st)
+            return 0
+        except Error as e:
+            print(f"[opflow] registered op '{name}': {e}", file=sys.stderr)
+            return int(e.code) + 1
+        except BaseException:  # noqa: BLE001 - reported through the status code
+            traceback.print_exc()
+            return int(Errc.SchedulerError) + 1
+
+    cb = _lib.KERNEL_FN(tramp)
+    check(lib().opf_register_op(name.encode(), cb, int(resource_class), n_in, n_out))
+    _REGISTERED[name] = (cb, fn)
+
+
+def has_op(name: str) -> bool:
+    p = C.c_int32()
+    check(lib().opf_has_op(name.encode(), C.byref(p)))
+    return bool(p.value)
+
+
 def launch(op: OpDecl | dict, inputs: Sequence, outputs: Sequence, rows: int, stream=None,
            comm: Optional[Comm] = None, max_ctas: int = 0) -> None:
     """Device eval_op_into: run one operator into caller-provided tensors."""

@@ -327,3 +327,25 @@ def test_fused_epilogue_keeps_arena_liveness():
     _, plain = of.dry_run(g, p, {"name": "sequential"}, rows=8192, config={"fuse_addnorm": False})
     assert fused["last"]["plan_arena_bytes"] < (1 << 30)
     assert fused["last"]["plan_arena_bytes"] < 2 * plain["last"]["plan_arena_bytes"]
+
+
+def test_sequential_fallback_is_all_or_nothing():
+    """execute([a, b]) without a replacement runs a then b in order (b may
+    depend on a).  If a later handle is not ready, nothing is recorded: the
+    context is unchanged (SPEC: scheduler-visible state is totally ordered
+    and reproducible), so a strategy that catches NotReady sees no phantom
+    dispatch of `a`."""
+    g, p = plan_of(of.dense_tp_graph(1, 8, 4, costs=unit_costs()), [R.by_func("AllReduce")])
+    seen = {}
+
+    def fn(ctx):
+        ctx.split([8])
+        with pytest.raises(of.Error) as e:
+            ctx.execute([ctx.handle(0, 0), ctx.handle(2, 0)])  # 2 needs 1, which is not in the list
+        assert e.value.code == of.Errc.NotReady
+        seen["ready_after_failure"] = [h.subgraph for h in ctx.get_ready_ops(0)]
+        ctx.execute([ctx.handle(0, 0), ctx.handle(1, 0), ctx.handle(2, 0)])  # chained: fine in order
+
+    sched, _ = of.dry_run(g, p, Scripted(fn, "atomic"), rows=8)
+    assert seen["ready_after_failure"] == [0]
+    assert [d["subgraphs"] for d in sched["dispatches"]] == [[0], [1], [2]]
