@@ -106,8 +106,8 @@ def test_python_registered_op(cuda, ref):
     R, H = 256, 256
     desc = {"tensors": [{"name": "x", "shape": [R, H], "dtype": "f32", "role": "input"},
                         {"name": "w", "shape": [H, H], "batch": "replicated", "dtype": "f32", "role": "weight"},
-                        {"name": "mm", "shape": [R, H], "dtype": "f32"},
-                        {"name": "capped", "shape": [R, H], "dtype": "f32"},
+                        {"name": "mm", "shape": [R, H], "dtype": "f32", "role": "intermediate"},
+                        {"name": "capped", "shape": [R, H], "dtype": "f32", "role": "intermediate"},
                         {"name": "y", "shape": [R, H], "dtype": "f32", "role": "output"}],
             "operators": [{"name": "blk.proj", "kind": "MatMul", "inputs": ["x", "w"], "outputs": ["mm"],
                            "module_path": "blk.proj"},

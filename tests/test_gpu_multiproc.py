@@ -31,7 +31,9 @@ def _free_port() -> int:
 
 def run_ranks(case: str, world: int = 2, timeout: float = 240.0):
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
-    procs = [subprocess.Popen([sys.executable, str(ROOT / "tests" / "mp_worker.py"), "--rank", str(r),
+    # OPF_MP_WRAP="compute-sanitizer --tool memcheck" runs every rank under a tool
+    wrap = os.environ.get("OPF_MP_WRAP", "").split()
+    procs = [subprocess.Popen([*wrap, sys.executable, str(ROOT / "tests" / "mp_worker.py"), "--rank", str(r),
                                "--world", str(world), "--case", case],
                               stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, env=env, cwd=ROOT)
              for r in range(world)]
