@@ -113,6 +113,13 @@ __device__ __forceinline__ bool slot_barrier(const PeerPtrs& pp, uint32_t* my_ep
   __shared__ uint32_t ok;
   if (threadIdx.x == 0) {
     ok = 1;
+    if (*reinterpret_cast<volatile uint32_t*>(err)) {  // poisoned by an earlier timeout: fail fast
+      ok = 0;
+    }
+  }
+  __syncthreads();
+  if (!ok) return false;
+  if (threadIdx.x == 0) {
     const uint32_t e = ++my_epoch[slot];
     __threadfence_system();
     for (int p = 0; p < world; ++p) st_release_sys(pp.flags[p] + slot * kMaxWorld + rank, e);

@@ -330,8 +330,10 @@ __global__ void __launch_bounds__(256) ep_send_kernel(PeerArena pa, int64_t xr_o
                                                       const int64_t* __restrict__ slot_local,
                                                       const int32_t* __restrict__ off_local,
                                                       const int32_t* __restrict__ send_off, int64_t n, int k,
-                                                      int64_t H, int E, int El, int rank) {
+                                                      int64_t H, int E, int El, int rank, int64_t cap,
+                                                      const uint32_t* __restrict__ err) {
   pdl_wait();
+  if (*reinterpret_cast<const volatile uint32_t*>(err)) return;  // poisoned window: the counts are not valid
   const int lane = threadIdx.x % 32;
   for (int64_t s = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; s < n;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
@@ -339,6 +341,7 @@ __global__ void __launch_bounds__(256) ep_send_kernel(PeerArena pa, int64_t xr_o
     if (!valid_id(e, E)) continue;
     const int o = static_cast<int>(e / El);
     const int64_t dest = send_off[e] + (slot_local[s] - off_local[e]);
+    if (dest < 0 || dest >= cap) continue;  // never write outside the owner's receive tensor
     const uint4* src = reinterpret_cast<const uint4*>(x + (s / k) * H);
     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(pa.base[o] + xr_off) + dest * H);
     for (int64_t i = lane; i < H / 8; i += 32) dst[i] = src[i];
@@ -357,13 +360,15 @@ __global__ void ep_barrier_kernel(PeerPtrs pp, uint32_t* epochs, uint32_t* err, 
 __global__ void __launch_bounds__(256) ep_return_kernel(PeerArena pa, int64_t yc_off,
                                                         const __nv_bfloat16* __restrict__ yr,
                                                         const int64_t* __restrict__ rinfo, int El, int64_t n,
-                                                        int64_t H) {
+                                                        int64_t H, int W, int64_t cap,
+                                                        const uint32_t* __restrict__ err) {
   pdl_wait();
+  if (*reinterpret_cast<const volatile uint32_t*>(err)) return;  // poisoned window: rinfo is not valid
   __shared__ int64_t n_recv;
   if (threadIdx.x == 0) {
     int64_t t = 0;
     for (int el = 0; el < El; ++el) t += rinfo[el];
-    n_recv = t;
+    n_recv = t < cap ? t : cap;
   }
   __syncthreads();
   const int lane = threadIdx.x % 32;
@@ -372,6 +377,7 @@ __global__ void __launch_bounds__(256) ep_return_kernel(PeerArena pa, int64_t yc
     const int64_t code = rinfo[El + i];
     const int p = static_cast<int>(code / n);
     const int64_t s = code % n;
+    if (code < 0 || p >= W) continue;  // never follow a corrupt source code
     const uint4* src = reinterpret_cast<const uint4*>(yr + i * H);
     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(pa.base[p] + yc_off) + s * H);
     for (int64_t c = lane; c < H / 8; c += 32) dst[c] = src[c];
@@ -411,12 +417,14 @@ __global__ void __launch_bounds__(256) combine_slots_kernel(const __nv_bfloat16*
 
 // grouped-GEMM tile table from per-local-expert row counts (EP receive side)
 __global__ void tiles_from_counts_kernel(const int64_t* __restrict__ counts, int El, int32_t* __restrict__ gtab,
-                                         int tile_m) {
+                                         int tile_m, int64_t cap) {
   pdl_wait();
   if (threadIdx.x == 0) {
     int32_t row = 0, t = 0;
     for (int el = 0; el < El; ++el) {
-      const int32_t c = static_cast<int32_t>(counts[el]);
+      // clamp to the receive tensor's rows: tiles never address past it
+      const int64_t c64 = counts[el] < 0 ? 0 : counts[el];
+      const int32_t c = static_cast<int32_t>(c64 < cap - row ? c64 : cap - row);
       for (int32_t r = 0; r < c; r += tile_m, ++t) {
         gtab[1 + 3 * t] = row + r;
         gtab[2 + 3 * t] = row + c;
@@ -562,7 +570,7 @@ opf_status grouped(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_vi
   } else {
     gtab = reinterpret_cast<int32_t*>(ws);
     launch_pdl(tiles_from_counts_kernel, dim3(1), dim3(32), 0, s, static_cast<const int64_t*>(vptr<int64_t>(in[1])),
-               El, gtab, moe_tile_m());
+               El, gtab, moe_tile_m(), n);
   }
   GemmArgs g{};
   g.a = view_ptr(in[0]);
@@ -654,7 +662,8 @@ opf_status op_moe_ep_dispatch(const opf_op_ctx* c, const opf_view* in, int32_t n
   launch_pdl(ep_send_kernel, dim3(grid), dim3(256), 0, s, x.pa, xr_off, rinfo_off,
              static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[0])), ids,
              static_cast<const int64_t*>(slot_local), static_cast<const int32_t*>(off),
-             static_cast<const int32_t*>(send_off), n, k, H, E, El, x.rank);
+             static_cast<const int32_t*>(send_off), n, k, H, E, El, x.rank, n * ep,
+             static_cast<const uint32_t*>(x.w.err));
   launch_pdl(ep_barrier_kernel, dim3(1), dim3(32), 0, s, x.w.pp, x.w.epochs, x.w.err, ep, x.rank);
   return launch_status("moe_ep_dispatch");
 }
@@ -693,7 +702,8 @@ opf_status op_moe_ep_combine(const opf_op_ctx* c, const opf_view* in, int32_t n_
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n * ep * 32 + 255) / 256, num_sms() * 8LL)));
   launch_pdl(ep_return_kernel, dim3(grid), dim3(256), 0, s, x.pa, yc_off,
              static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[0])),
-             static_cast<const int64_t*>(vptr<int64_t>(in[1])), El, n, H);
+             static_cast<const int64_t*>(vptr<int64_t>(in[1])), El, n, H, ep, n * ep,
+             static_cast<const uint32_t*>(x.w.err));
   launch_pdl(ep_barrier_kernel, dim3(1), dim3(32), 0, s, x.w.pp, x.w.epochs, x.w.err, ep, x.rank);
   if (rows > 0)
     launch_pdl(combine_slots_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), 0, s,
