@@ -49,8 +49,8 @@ def run_ranks(case: str, world: int = 2, timeout: float = 240.0):
     if wrap and (ROOT / "gpurun_out").is_dir():  # keep each rank's tool report
         d = ROOT / "gpurun_out" / "san"
         d.mkdir(exist_ok=True)
-        for r, (_, _, err) in enumerate(outs):
-            (d / f"mp_{case}_rank{r}.log").write_text(err)
+        for r, (_, out, err) in enumerate(outs):
+            (d / f"mp_{case}_rank{r}.log").write_text(out + err)
     res = []
     for rc, out, err in outs:
         assert rc == 0, f"rank failed rc={rc}\n{out[-2000:]}\n{err[-4000:]}"
