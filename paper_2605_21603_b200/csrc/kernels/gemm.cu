@@ -708,16 +708,27 @@ __device__ __forceinline__ void store_tile_splitk(const CUtensorMap* map_c, uint
 // fixup) with a 5-stage ring.  8 warps did not speed up the whole-K epilogue
 // on short-K shapes (A/B in profiles/r01_gemm_ab_r0_vs_new.jsonl), so the
 // lighter 4-warp / 6-stage configuration stays there.
+//
+// TN = 384 (one-wave shapes, e.g. the TP=8 QKV 8192x768: 64 tiles of 256x384
+// on 74 clusters instead of 96 tiles of 256x256, a 1.3-wave tail): per k16 two
+// MMAs, N = 256 (TMEM columns 0..255, B rows 0..127 of each CTA's half) and
+// N = 128 (columns 256..383, B rows 128..191); one accumulator stage (384 of
+// the 512 TMEM columns), plain-store epilogue only.
 template <int TN, bool SPLIT>
 struct Tc2Cfg {
   static constexpr int kEpiW = SPLIT ? 8 : 4;
   static constexpr int kThreads = 64 + kEpiW * 32;
+  static constexpr int kAcc = TN == 384 ? 1 : 2;       // TMEM accumulator stages
+  static constexpr int kStg = TN == 384 ? 1 : 2;       // 4 KB staging buffers per epilogue warp
   static constexpr uint32_t kStageBytes = kABytes + (TN / 2) * BK * 2;
-  static constexpr uint32_t kFixed = 1024 + kEpiW * 2 * kEpiBytes + 512;
+  static constexpr uint32_t kFixed = 1024 + kEpiW * kStg * kEpiBytes + 512;
   static constexpr int kStages = ((232448 - kFixed) / kStageBytes) > 6 ? 6 : (232448 - kFixed) / kStageBytes;
   static constexpr uint32_t kSmemBytes = kFixed + kStages * kStageBytes;
-  static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(TN >> 3) << 17) |
-                                     (static_cast<uint32_t>(256 >> 4) << 24);
+  static constexpr uint32_t idesc(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(256 >> 4) << 24);
+  }
+  static constexpr uint32_t kIdesc = idesc(TN == 384 ? 256 : TN);
 };
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clear the CTA-rank bit: address the pair leader
 
@@ -755,6 +766,110 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask)
                : "memory");
+}
+// Accumulator hand-back: only the (already waited-for) TMEM loads must precede
+// it, so no release semantics — a .release arrive would first drain every
+// global store this thread issued (measured ~1.9k cycles per tile).
+__device__ __forceinline__ void mbar_arrive_leader_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask)
+               : "memory");
+}
+
+// Epilogue of one accumulator tile for one warp (32 rows) with plain global
+// stores: TMEM -> registers (-> SiLU-mul / residual add) -> bf16 -> a 4 KB
+// 128B-swizzled staging buffer (lane = row) -> read back so that 8 lanes
+// cover one 128-byte row segment (each store instruction writes 4 whole
+// rows x 128 B) -> st.global.  The accumulator is released as soon as its
+// last TMEM load lands, so the next tile's MMAs never wait for the stores, and
+// no TMA store shares the TMA unit with the operand loads (measured: the
+// TMA-store epilogue took 4-6k cycles per 128x256 tile and bounded every
+// short-K shape, tools/gemm_trace.py).
+template <int EPI, int TN, typename Release, typename Mark>
+__device__ __forceinline__ void store_tile_st(uint32_t tmem_col0, uint8_t* sbuf, int lane, int64_t nb, int64_t row0,
+                                              int64_t M, int64_t n_out, __nv_bfloat16* __restrict__ c, int64_t ldc,
+                                              const RopeArgs* rope, Release&& release, Mark&& mark) {
+  constexpr int kChunks = EPI == 1 ? 2 : TN / 64;
+  float ss = 0.0f;  // EPI 4: this lane's row, this tile's columns
+  const bool row_ok = row0 + lane < M;
+#pragma unroll 1
+  for (int chunk = 0; chunk < kChunks; ++chunk) {
+    uint32_t v0[32], v1[32];
+    uint4 xres[EPI == 4 ? 8 : 1];
+    if constexpr (EPI == 4) {  // residual row segment, in flight under the TMEM loads
+      if (row_ok) {
+        const uint4* xr =
+            reinterpret_cast<const uint4*>(rope->resid + (row0 + lane) * rope->resid_ld + nb * TN + chunk * 64);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xres[j] = __ldcs(xr + j);
+      }
+    }
+    const uint32_t taddr = tmem_col0 + static_cast<uint32_t>(chunk * 64);
+    tmem_ld32(taddr, v0);
+    tmem_ld32(taddr + 32, v1);
+    if constexpr (EPI == 1) {
+      uint32_t u0[32], u1[32];
+      tmem_ld32(taddr + 128, u0);
+      tmem_ld32(taddr + 160, u1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (chunk == kChunks - 1) release();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float g0 = __uint_as_float(v0[i]), g1 = __uint_as_float(v1[i]);
+        v0[i] = __float_as_uint(g0 / (1.0f + __expf(-g0)) * __uint_as_float(u0[i]));
+        v1[i] = __float_as_uint(g1 / (1.0f + __expf(-g1)) * __uint_as_float(u1[i]));
+      }
+    } else {
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      mark(4);
+      if (chunk == kChunks - 1) release();
+    }
+    if constexpr (EPI == 4) {  // + residual, sum of squares of the rounded sum
+      if (row_ok) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 u = xres[j];
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+          uint32_t* dst = j < 4 ? &v0[8 * j] : &v1[8 * (j - 4)];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h2[e]);
+            const float a = __bfloat162float(__float2bfloat16(__uint_as_float(dst[2 * e]) + f.x));
+            const float b = __bfloat162float(__float2bfloat16(__uint_as_float(dst[2 * e + 1]) + f.y));
+            ss += a * a + b * b;
+            dst[2 * e] = __float_as_uint(a);
+            dst[2 * e + 1] = __float_as_uint(b);
+          }
+        }
+      }
+    }
+    __syncwarp();  // the previous chunk's read-back of sbuf is done
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // 16-byte piece j = columns 8j..8j+7 of this lane's row
+      const uint32_t* src = j < 4 ? &v0[8 * j] : &v1[8 * (j - 4)];
+      uint4 q;
+      q.x = pack_bf16(src[0], src[1]);
+      q.y = pack_bf16(src[2], src[3]);
+      q.z = pack_bf16(src[4], src[5]);
+      q.w = pack_bf16(src[6], src[7]);
+      *reinterpret_cast<uint4*>(sbuf + lane * 128 + ((j ^ (lane & 7)) * 16)) = q;
+    }
+    __syncwarp();
+    const int64_t col0 = (EPI == 1 ? nb * (TN / 2) : nb * TN) + chunk * 64;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = i * 4 + lane / 8, j = lane % 8;
+      const int64_t col = col0 + j * 8;
+      if (row0 + row < M && col < n_out) {
+        const uint4 u = *reinterpret_cast<const uint4*>(sbuf + row * 128 + ((j ^ (row & 7)) * 16));
+        *reinterpret_cast<uint4*>(c + (row0 + row) * ldc + col) = u;
+      }
+    }
+    mark(5);
+  }
+  if constexpr (EPI == 4) {
+    static_assert(EPI != 4 || TN == 256, "EPI 4 partials assume whole 256-column tiles per warp");
+    if (row_ok) rope->ssq[(row0 + lane) * rope->ssq_ld + nb] = ss;
+  }
 }
 
 // GROUPED (MoE experts, TN = 256, unsplit): gtab = [n_tiles, (row0, row_end,
@@ -810,6 +925,34 @@ __device__ __forceinline__ void store_tile_push(uint32_t tmem_col0, uint8_t* sbu
     asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(pa.cnt[q] + lr / 32), "r"(1u) : "memory");
 }
 
+// Per-tile timeline of cluster 0's leader CTA (tools/gemm_trace.py), compiled
+// in only with -DOPF_GEMM_TRACE: role r (0 producer, 1 MMA, 2 epilogue warp
+// 2) appends (event, unit, clock64) records.
+#ifdef OPF_GEMM_TRACE
+__device__ unsigned long long g_gemm_trace[3][2048];
+__device__ int g_gemm_trace_n[3];
+// counters live in registers (a global read-modify-write per event would add
+// an L2 round trip to the timeline it measures)
+#define GTRACE(role, ev, unit)                                                                  \
+  do {                                                                                          \
+    if (blockIdx.x == 0 && gt_n < 2048)                                                         \
+      g_gemm_trace[role][gt_n++] = (static_cast<unsigned long long>(ev) << 56) |                \
+                                   (static_cast<unsigned long long>((unit) & 0xFFFF) << 40) |   \
+                                   (clock64() & 0xFFFFFFFFFFull);                               \
+  } while (0)
+#define GTRACE_END(role) \
+  do {                   \
+    if (blockIdx.x == 0) g_gemm_trace_n[role] = gt_n; \
+  } while (0)
+#else
+#define GTRACE(role, ev, unit) \
+  do {                         \
+  } while (0)
+#define GTRACE_END(role) \
+  do {                   \
+  } while (0)
+#endif
+
 template <int EPI, int TN, bool SPLIT = false, bool GROUPED = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -823,16 +966,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;
+  constexpr int kAcc = C::kAcc;
   uint8_t* epi_base = smem + kStages2 * kStageBytes2;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + C::kEpiW * 2 * kEpiBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + C::kEpiW * C::kStg * kEpiBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages2;
   uint64_t* tfull = bars + 2 * kStages2;
-  uint64_t* tempty = bars + 2 * kStages2 + kAccStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages2 + 2 * kAccStages);
+  uint64_t* tempty = bars + 2 * kStages2 + kAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages2 + 2 * kAcc);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
+#ifdef OPF_GEMM_TRACE
+  int gt_n = 0;
+#endif
   const bool leader = rank == 0;
   int64_t m_blocks = (M + 2 * BM - 1) / (2 * BM);
   const int64_t n_blocks = (N + TN - 1) / TN;
@@ -853,7 +1000,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < kAccStages; ++a) {
+    for (int a = 0; a < kAcc; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * C::kEpiW);
     }
@@ -887,18 +1034,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
           n0 += static_cast<int32_t>(gtab[3 + 3 * mb] * N);
         }
         const int kb0 = sp * k_blocks / splits, kb1 = (sp + 1) * k_blocks / splits;
+        GTRACE(0, 0, u);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (kb == kb0) GTRACE(0, 1, u);
           uint8_t* sa = stage_base + stage * kStageBytes2;
           if (leader) mbar_expect_tx(&full[stage], 2 * kStageBytes2);
           tma_load_2d_pair(sa, &map_a, &full[stage], kb * BK, m0);
-          tma_load_2d_pair(sa + kABytes, &map_b, &full[stage], kb * BK, n0);
+          if constexpr (TN == 384) {  // B box = 64 rows: MMA-1 rows (2 boxes), then MMA-2 rows
+            const int32_t nt = static_cast<int32_t>(nb * 384);
+            tma_load_2d_pair(sa + kABytes, &map_b, &full[stage], kb * BK, nt + static_cast<int32_t>(rank) * 128);
+            tma_load_2d_pair(sa + kABytes + 8192, &map_b, &full[stage], kb * BK,
+                             nt + static_cast<int32_t>(rank) * 128 + 64);
+            tma_load_2d_pair(sa + kABytes + 16384, &map_b, &full[stage], kb * BK,
+                             nt + 256 + static_cast<int32_t>(rank) * 64);
+          } else {
+            tma_load_2d_pair(sa + kABytes, &map_b, &full[stage], kb * BK, n0);
+          }
           if (++stage == kStages2) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
+      GTRACE_END(0);
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {  // ---------------- MMA issuer (leader CTA)
@@ -909,18 +1068,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
       for (int64_t u = cluster; u < units; u += n_clusters) {
         const int sp = static_cast<int>(u % splits);
         const int kb0 = sp * k_blocks / splits, kb1 = (sp + 1) * k_blocks / splits;
+        GTRACE(1, 0, u);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
+        GTRACE(1, 1, u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * TN);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
+          GTRACE(1, 2, u);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = smem_u32(stage_base + stage * kStageBytes2);
           const uint32_t sb = sa + kABytes;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
+          for (int k = 0; k < BK / 16; ++k) {
             umma_f16_pair(d_tmem, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32), C::kIdesc,
                           (kb != kb0 || k != 0) ? 1u : 0u);
+            if constexpr (TN == 384)
+              umma_f16_pair(d_tmem + 256, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + 16384 + k * 32),
+                            C::idesc(128), (kb != kb0 || k != 0) ? 1u : 0u);
+          }
           umma_commit_pair(&empty[stage]);
           if (++stage == kStages2) {
             stage = 0;
@@ -928,18 +1094,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
           }
         }
         umma_commit_pair(&tfull[acc]);
-        if (++acc == kAccStages) {
+        GTRACE(1, 3, u);
+        if (++acc == kAcc) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
+      GTRACE_END(1);
     }
   } else {  // ---------------- epilogue warps (both CTAs)
     const int ew = warp - 2;
     const int quarter = warp % 4;
     const int half = C::kEpiW == 8 ? ew / 4 : 0;  // column chunks half, half + step, ...
     constexpr int kStep = C::kEpiW == 8 ? 2 : 1;
-    uint8_t* stg[2] = {epi_base + (ew * 2) * kEpiBytes, epi_base + (ew * 2 + 1) * kEpiBytes};
+    uint8_t* stg[2] = {epi_base + (ew * C::kStg) * kEpiBytes, epi_base + (ew * C::kStg + C::kStg - 1) * kEpiBytes};
     int acc = 0;
     uint32_t acc_phase = 0;
     int buf = 0;
@@ -947,7 +1115,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
       const int64_t t = u / splits;
       int64_t mb, nb;
       tile_coords(t, m_blocks, n_blocks, mb, nb);
+      if (warp == 2 && lane == 0) GTRACE(2, 0, u);
       mbar_wait(&tfull[acc], acc_phase);
+      if (warp == 2 && lane == 0) GTRACE(2, 1, u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       int64_t row0 = mb * 2 * BM + rank * BM + quarter * 32;
       int64_t row_end = M;
@@ -959,7 +1129,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
       auto release = [&]() {  // accumulator fully read: hand it back to the MMA warp
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+        if (lane == 0) mbar_arrive_leader_relaxed(&tempty[acc]);
+        if (warp == 2 && lane == 0) GTRACE(2, 2, u);
       };
       if constexpr (GROUPED) {
         // whole 32-row slabs inside the expert segment by TMA; the straddling slab row by row
@@ -973,16 +1144,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
       } else if constexpr (SPLIT && TN == 256) {
         store_tile_splitk<EPI>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, static_cast<int>(rank) * 8 + ew, t,
                                static_cast<int>(u % splits), splits, ws, sem, release);
-      } else {
+      } else if constexpr (EPI == 2) {
         store_tile<EPI, TN>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, kStep, &rope);
         release();
+      } else {
+        auto mark = [&](int ev) {
+          if (warp == 2 && lane == 0) GTRACE(2, ev, u);
+        };
+        store_tile_st<EPI, TN>(tcol, stg[0], lane, nb, row0, M, EPI == 1 ? N / 2 : N, c_out, ldc, &rope, release,
+                               mark);
       }
-      if (++acc == kAccStages) {
+      if (warp == 2 && lane == 0) GTRACE(2, 3, u);
+      if (++acc == kAcc) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (warp == 2 && lane == 0) GTRACE_END(2);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();
@@ -1052,6 +1231,8 @@ void gemm_bf16_tc_init() {
                                   static_cast<int>(Tc2Cfg<192, false>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tc2Cfg<128, false>::kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<384, false>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<4, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1150,11 +1331,16 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
       static const int forced = [] {
         const char* e = std::getenv("OPF_GEMM_TN");
         const int v = e ? std::atoi(e) : 0;
-        return (v == 192 || v == 128) ? v : 256;
+        return (v == 192 || v == 128 || v == 384) ? v : 0;
       }();
-      tn = forced;
+      // 256x384 tiles when they fit one round of clusters and 256-wide ones
+      // would need two (a ~1.3-wave tail): e.g. 8192 x 768 -> 64 tiles, not 96
+      const int64_t t256 = mt * ((g.n + 255) / 256), t384 = mt * ((g.n + 383) / 384);
+      const bool one_wave_384 = g.n % 384 == 0 && t384 <= cmax && t256 > cmax && g.k >= 1024;
+      tn = forced ? forced : (one_wave_384 ? 384 : 256);
+      if (tn == 384 && g.n % 384 != 0) tn = 256;
     }
-    const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, static_cast<uint32_t>(tn / 2));
+    const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, static_cast<uint32_t>(tn == 384 ? 64 : tn / 2));
     const int64_t tiles = mt * ((g.n + tn - 1) / tn);
     int splits = tn == 256 && g.epi != 2 && g.epi != 4 ? gemm_splitk_splits(g.m, g.n, g.k, g.max_ctas) : 1;
     float4* ws = nullptr;
@@ -1174,28 +1360,31 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     const dim3 blocks(2u * static_cast<unsigned>(std::max(clusters, 1)));
     if (splits > 1 && g.epi == 1)
       launch_pdl(gemm_tc2_kernel<1, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
-                 g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
+                 g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (splits > 1)
       launch_pdl(gemm_tc2_kernel<0, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
-                 g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
+                 g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (g.epi == 4)
       launch_pdl(gemm_tc2_kernel<4, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb,
-                 mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
+                 mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (g.epi == 2)
       launch_pdl(gemm_tc2_kernel<2, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb,
-                 mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
+                 mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (g.epi == 1)
       launch_pdl(gemm_tc2_kernel<1, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
+                 g.n, g.k, splits, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (tn == 256)
       launch_pdl(gemm_tc2_kernel<0, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, splits, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
+                 g.n, g.k, splits, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
+    else if (tn == 384)
+      launch_pdl(gemm_tc2_kernel<0, 384>, blocks, dim3(Tc2Cfg<384, false>::kThreads), Tc2Cfg<384, false>::kSmemBytes, s, ma, mb, mc, g.m,
+                 g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (tn == 192)
       launch_pdl(gemm_tc2_kernel<0, 192>, blocks, dim3(Tc2Cfg<192, false>::kThreads), Tc2Cfg<192, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
+                 g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else
       launch_pdl(gemm_tc2_kernel<0, 128>, blocks, dim3(Tc2Cfg<128, false>::kThreads), Tc2Cfg<128, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, 1, ws, sem, rope, kNoGtab, kNoOut, int64_t{0}, kNoPush);
+                 g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     return;
   }
   const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN);
@@ -1314,3 +1503,13 @@ void k_pack_gate_up(const void* src, void* dst, int64_t K, int64_t I, cudaStream
 }
 
 }  // namespace opflow
+
+#ifdef OPF_GEMM_TRACE
+// tools/gemm_trace.py: read (and reset) the trace buffers of the last launch
+extern "C" int opf_debug_gemm_trace(unsigned long long* out, int* counts) {
+  if (cudaMemcpyFromSymbol(out, opflow::g_gemm_trace, sizeof(opflow::g_gemm_trace)) != cudaSuccess) return 1;
+  if (cudaMemcpyFromSymbol(counts, opflow::g_gemm_trace_n, sizeof(opflow::g_gemm_trace_n)) != cudaSuccess) return 1;
+  const int zero[3] = {0, 0, 0};
+  return cudaMemcpyToSymbol(opflow::g_gemm_trace_n, zero, sizeof(zero)) == cudaSuccess ? 0 : 1;
+}
+#endif
