@@ -872,6 +872,65 @@ __device__ __forceinline__ void store_tile_st(uint32_t tmem_col0, uint8_t* sbuf,
   }
 }
 
+// RoPE epilogue with plain stores (EPI 2, TN = 256 or 384: TN / 128 heads of
+// 128 per tile).  For head h of the tile, dims d < 64 and d + 64 rotate as
+// in store_tile_rope; the two 64-column halves go out one after the other
+// through the warp's one 4 KB staging buffer (the half not being staged is
+// recomputed from TMEM, which is cheaper than a second buffer's worth of
+// pipeline stages).  Released after the last head's last TMEM load.
+template <int TN, typename Release>
+__device__ __forceinline__ void store_tile_rope_st(uint32_t tmem_col0, uint8_t* sbuf, int lane, int64_t nb,
+                                                   int64_t row0, int64_t M, int64_t n_out,
+                                                   __nv_bfloat16* __restrict__ c, int64_t ldc, const RopeArgs& rope,
+                                                   Release&& release) {
+  constexpr int kHeads = TN / 128;
+  const float p = row0 + lane < M ? static_cast<float>(rope.pos[row0 + lane]) : 0.0f;
+#pragma unroll 1
+  for (int hh = 0; hh < kHeads; ++hh) {
+    const bool rot = (nb * TN) / 128 + hh < rope.rot_heads;
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+      __syncwarp();  // the previous half's read-back of sbuf is done
+#pragma unroll 1
+      for (int j = 0; j < 2; ++j) {
+        uint32_t a[32], b[32];
+        tmem_ld32(tmem_col0 + static_cast<uint32_t>(hh * 128 + j * 32), a);
+        tmem_ld32(tmem_col0 + static_cast<uint32_t>(hh * 128 + 64 + j * 32), b);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (hh == kHeads - 1 && half == 1 && j == 1) release();
+        float o[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float x = __uint_as_float(a[i]), y = __uint_as_float(b[i]);
+          if (rot) {
+            const float inv_freq = exp2f(-2.0f * static_cast<float>(j * 32 + i) / 128.0f * rope.log2_theta);
+            const float ang = p * inv_freq;
+            const float q = rintf(ang * 0.15915494309189535f);
+            const float r = fmaf(-q, 6.28318548202514648f, fmaf(-q, -1.7484556e-07f, ang));
+            float sn, cs;
+            __sincosf(r, &sn, &cs);
+            o[i] = half == 0 ? x * cs - y * sn : y * cs + x * sn;
+          } else {
+            o[i] = half == 0 ? x : y;
+          }
+        }
+        stage_half(sbuf, o, j, lane);
+      }
+      __syncwarp();
+      const int64_t col0 = nb * TN + hh * 128 + half * 64;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int row = i * 4 + lane / 8, jj = lane % 8;
+        const int64_t col = col0 + jj * 8;
+        if (row0 + row < M && col < n_out) {
+          const uint4 u = *reinterpret_cast<const uint4*>(sbuf + row * 128 + ((jj ^ (row & 7)) * 16));
+          *reinterpret_cast<uint4*>(c + (row0 + row) * ldc + col) = u;
+        }
+      }
+    }
+  }
+}
+
 // GROUPED (MoE experts, TN = 256, unsplit): gtab = [n_tiles, (row0, row_end,
 // expert) x n_tiles] with 256-row tiles; N is the per-expert width, expert e's
 // B rows start at e * N; rows of a tile past row_end belong to the next
@@ -1145,8 +1204,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
         store_tile_splitk<EPI>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, static_cast<int>(rank) * 8 + ew, t,
                                static_cast<int>(u % splits), splits, ws, sem, release);
       } else if constexpr (EPI == 2) {
-        store_tile<EPI, TN>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, kStep, &rope);
-        release();
+        store_tile_rope_st<TN>(tcol, stg[0], lane, nb, row0, M, N, c_out, ldc, rope, release);
       } else {
         auto mark = [&](int ev) {
           if (warp == 2 && lane == 0) GTRACE(2, ev, u);
@@ -1232,6 +1290,8 @@ void gemm_bf16_tc_init() {
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tc2Cfg<128, false>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Tc2Cfg<384, false>::kSmemBytes)));
+    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<2, 384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tc2Cfg<384, false>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
@@ -1327,7 +1387,7 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     // measured slower per FLOP on B200 (more L2 -> SMEM bytes per MAC), so the
     // rounds x width model alone picks them wrongly (profiles/r01_gemm_sweep*.json).
     int tn = 256;
-    if (g.epi == 0) {
+    if (g.epi == 0 || g.epi == 2) {
       static const int forced = [] {
         const char* e = std::getenv("OPF_GEMM_TN");
         const int v = e ? std::atoi(e) : 0;
@@ -1338,7 +1398,7 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
       const int64_t t256 = mt * ((g.n + 255) / 256), t384 = mt * ((g.n + 383) / 384);
       const bool one_wave_384 = g.n % 384 == 0 && t384 <= cmax && t256 > cmax && g.k >= 1024;
       tn = forced ? forced : (one_wave_384 ? 384 : 256);
-      if (tn == 384 && g.n % 384 != 0) tn = 256;
+      if ((tn == 384 && g.n % 384 != 0) || (g.epi == 2 && tn != 384)) tn = 256;
     }
     const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, static_cast<uint32_t>(tn == 384 ? 64 : tn / 2));
     const int64_t tiles = mt * ((g.n + tn - 1) / tn);
@@ -1366,6 +1426,9 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
                  g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (g.epi == 4)
       launch_pdl(gemm_tc2_kernel<4, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb,
+                 mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
+    else if (g.epi == 2 && tn == 384)
+      launch_pdl(gemm_tc2_kernel<2, 384>, blocks, dim3(Tc2Cfg<384, false>::kThreads), Tc2Cfg<384, false>::kSmemBytes, s, ma, mb,
                  mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (g.epi == 2)
       launch_pdl(gemm_tc2_kernel<2, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb,

@@ -375,13 +375,15 @@ def _rope_ref(x, pos, nq, nkv, theta=10000.0):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,nq,nkv", [(8192, 4, 1), (512, 32, 8), (100, 8, 2), (1024, 2, 1)])
-def test_gemm_rope_epilogue_fused(cuda, m, nq, nkv):
+@pytest.mark.parametrize("m,nq,nkv,K", [(8192, 4, 1, 512), (512, 32, 8, 512), (100, 8, 2, 512), (1024, 2, 1, 512),
+                                         (8192, 4, 1, 4096)])
+def test_gemm_rope_epilogue_fused(cuda, m, nq, nkv, K):
     """MatMul -> rope in one dispatch runs as ONE tcgen05 GEMM with the RoPE
     epilogue (q/k heads rotated on the fp32 accumulator, v heads copied);
-    matches torch fp32 rope(a @ w)."""
+    matches torch fp32 rope(a @ w).  8192 x 768 x 4096 is the TP=8 QKV shape:
+    256x384 tiles, three heads per tile."""
     import torch
-    K, N = 512, (nq + 2 * nkv) * 128
+    N = (nq + 2 * nkv) * 128
     g = torch.Generator(device="cuda").manual_seed(m + nq)
     a = (torch.rand(m, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
     w = ((torch.rand(K, N, device="cuda", generator=g) * 2 - 1) / K ** 0.5).to(torch.bfloat16)
