@@ -273,12 +273,7 @@ __global__ void decode_simt_kernel(const T* __restrict__ qkv, const T* __restric
 bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                      const int64_t* table, const int64_t* ctx, __nv_bfloat16* out, int64_t B, int nq,
                      int nkv, int hd, int page, int64_t max_pages, float scale, int max_ctas, int hnd,
-                     int64_t cache_pages, cudaStream_t s);
-
-bool decode_bf16_tma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
-                     const int64_t* table, const int64_t* ctx, __nv_bfloat16* out, int64_t B, int nq, int nkv,
-                     int hd, int page, int64_t max_pages, int64_t cache_pages, float scale, int max_ctas,
-                     cudaStream_t s);
+                     bool coresident, cudaStream_t s);
 
 // implemented in attention_tc.cu (tensor-core prefill); returns false when the
 // shape is not supported there.
@@ -374,15 +369,10 @@ opf_status op_attn_decode(const opf_op_ctx* c, const opf_view* in, int32_t n_in,
   auto s = static_cast<cudaStream_t>(stream);
   const int grp = nq / nkv;
   const int impl = static_cast<int>(ctx_param(*c, "impl", 0.0));  // 0 auto, 1 warp-SIMT, 2 generic
-  if (in[0].dtype == OPF_BF16 && impl == 0 && hnd == 0 && ctx_param(*c, "simt", 0.0) == 0.0 &&
-      decode_bf16_tma(vptr<__nv_bfloat16>(in[0]), vptr<__nv_bfloat16>(in[1]), vptr<__nv_bfloat16>(in[2]),
-                      vptr<int64_t>(in[3]), vptr<int64_t>(in[4]), vptr<__nv_bfloat16>(out[0]), rows, nq,
-                      nkv, hd, page, max_pages, in[1].shape[0], scale, c->max_ctas, s))
-    return launch_status("attn_decode_tma");
   if (in[0].dtype == OPF_BF16 && impl == 0 && ctx_param(*c, "simt", 0.0) == 0.0 &&
       decode_bf16_mma(vptr<__nv_bfloat16>(in[0]), vptr<__nv_bfloat16>(in[1]), vptr<__nv_bfloat16>(in[2]),
                       vptr<int64_t>(in[3]), vptr<int64_t>(in[4]), vptr<__nv_bfloat16>(out[0]), rows, nq,
-                      nkv, hd, page, max_pages, scale, c->max_ctas, hnd, in[1].shape[0], s))
+                      nkv, hd, page, max_pages, scale, c->max_ctas, hnd, (c->flags & OPF_CTX_CORESIDENT) != 0, s))
     return launch_status("attn_decode_mma");
   if (hnd) return op_error(Errc::ShapeMismatch, "attn_decode: HND pages need the tensor-core path (bf16, hd 128, group <= 8)");
   if (in[0].dtype == OPF_BF16 && hd == 128 && grp <= kMaxGroup && impl != 2 &&

@@ -209,6 +209,12 @@ def test_llama_decode_bf16(cuda, kv_layout):
         got, _ = run_graph(desc, 16, host, strat)
         for k in want:
             assert rel_err(got[k], want[k]) < 2e-2
+    # NanoFlow with co-resident lanes (lane SM budget -1): the small-footprint
+    # 2-CTA GEMM and the 8-warp decode attention share every SM
+    got, _ = run_graph(desc, 16, host, {"name": "split_overlap", "n_microbatches": 2, "lane_sm_budget": [-1, -1, 0]},
+                       [of.PartitionRule.by_func("attn_decode")])
+    for k in want:
+        assert rel_err(got[k], want[k]) < 2e-2
 
 
 @pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 512, 1024), (300, 520, 200), (1, 256, 64),
@@ -234,6 +240,15 @@ def test_gemm_tcgen05_vs_torch(cuda, m, n, k):
     want = a.float() @ w.float()
     err = ((c.float() - want).norm() / want.norm()).item()
     assert err < 1e-2, err
+    # the co-resident 2-CTA variant (lane SM budget -1: 2-stage ring, no split-K)
+    sess2 = of.Session(gr, of.partition(gr, []), {"lanes": 1, "lane_sm_budget": [-1]})
+    c3 = torch.empty_like(c)
+    for name, t in (("a", a), ("w", w), ("c", c3)):
+        sess2.bind(name, t)
+    sess2.run()
+    torch.cuda.synchronize()
+    err3 = ((c3.float() - want).norm() / want.norm()).item()
+    assert err3 < 1e-2, err3
     # the CUDA-core reference path (direct opf_launch on the [K,N] weight) agrees
     c2 = torch.empty_like(c)
     of.launch({"name": "mm", "kind": "MatMul", "inputs": [], "outputs": []}, [a, w], [c2], m)
