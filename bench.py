@@ -579,12 +579,7 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
     sess.bind("slots", keep["slots"])
     cands = {"sequential": {"name": "sequential"},
              "nanoflow_u2": {"name": "split_overlap", "n_microbatches": 2, "lane_mode": "ubatch"},
-             "nanoflow_class": {"name": "split_overlap", "n_microbatches": 2},
-             # co-resident lanes: both keep the whole grid with small-footprint
-             # kernels (one GEMM CTA + one attention CTA per SM)
-             "nanoflow_coresident": {"name": "split_overlap", "n_microbatches": 2, "lane_sm_budget": [-1, -1, 0]},
-             "nanoflow_u2_coresident": {"name": "split_overlap", "n_microbatches": 2, "lane_mode": "ubatch",
-                                        "lane_sm_budget": [-1, -1, 0]}}
+             "nanoflow_class": {"name": "split_overlap", "n_microbatches": 2}}
     # NanoFlow SM partitioning: the GEMM fillers (compute lane 0) on G SMs, the
     # persistent paged attention (memory lane 1) on the other 148 - G SMs,
     # nano-batch A's attention concurrent with nano-batch B's GEMMs.

@@ -65,17 +65,12 @@ typedef struct opf_op_ctx {
   const char* const* param_names;
   const double* param_values;
   int32_t max_ctas;        /* SM budget for this launch (0 = whole GPU) */
-  int32_t flags;           /* OPF_CTX_* bits */
+  int32_t _pad;
   void* comm;              /* opf_comm* when the session is tensor-parallel, else NULL */
   const void* aux;         /* op-private device data prepared at plan build (may be NULL) */
   void* workspace;         /* arena scratch, workspace_bytes long */
   size_t workspace_bytes;
 } opf_op_ctx;
-
-/* The launch shares its SMs with a concurrent lane (lane SM budget -1): the op
- * picks its small-footprint kernel variant (shared memory and registers sized
- * so one CTA of each lane fits an SM) and keeps the whole-GPU grid. */
-#define OPF_CTX_CORESIDENT 1
 
 /* Device kernel entry point: async on `stream` (a cudaStream_t), never
  * allocates, outputs are caller-owned views (the zero-copy redirection hook). */

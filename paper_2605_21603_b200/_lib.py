@@ -34,7 +34,7 @@ class opf_op_ctx(C.Structure):
     _fields_ = [("op_name", C.c_char_p), ("kind", C.c_int32), ("custom_name", C.c_char_p),
                 ("world_size", C.c_int64), ("seed", C.c_uint64), ("n_params", C.c_int32),
                 ("param_names", C.POINTER(C.c_char_p)), ("param_values", C.POINTER(C.c_double)),
-                ("max_ctas", C.c_int32), ("flags", C.c_int32), ("comm", C.c_void_p),
+                ("max_ctas", C.c_int32), ("_pad", C.c_int32), ("comm", C.c_void_p),
                 ("aux", C.c_void_p), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t)]
 
 

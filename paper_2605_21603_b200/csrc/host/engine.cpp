@@ -526,13 +526,11 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
       if (l.is_copy) return;
       if (cfg_.gemm_sm_budget > 0 && d.lane == 0) l.max_ctas = cfg_.gemm_sm_budget;
       if (d.lane < static_cast<int>(budgets.size()) && budgets[d.lane] > 0) l.max_ctas = budgets[d.lane];
-      if (d.lane < static_cast<int>(budgets.size()) && budgets[d.lane] < 0) l.flags |= OPF_CTX_CORESIDENT;
       opf_op_ctx c{};
       c.kind = static_cast<int32_t>(l.kind);
       c.world_size = l.attrs.world_size;
       c.comm = comm_;
       c.max_ctas = l.max_ctas;
-      c.flags = l.flags;
       std::vector<opf_view> iv, ov;
       for (const auto& v : l.in) iv.push_back(make_view(nullptr, v.elem_offset, v.dtype, v.shape, v.batched));
       for (const auto& v : l.out) ov.push_back(make_view(nullptr, v.elem_offset, v.dtype, v.shape, v.batched));
@@ -633,8 +631,7 @@ std::unique_ptr<CompiledPlan> Session::compile(const SchedContext& ctx, const st
             int mc = 0;
             if (cfg_.gemm_sm_budget > 0 && d.lane == 0) mc = cfg_.gemm_sm_budget;
             if (d.lane < static_cast<int>(budgets.size()) && budgets[d.lane] > 0) mc = budgets[d.lane];
-            const bool coloc = d.lane < static_cast<int>(budgets.size()) && budgets[d.lane] < 0;  // never splits K
-            addnorm = coloc || gemm_splitk_splits(nrows, w.shape[1], w.shape[0], mc) <= 1;
+            addnorm = gemm_splitk_splits(nrows, w.shape[1], w.shape[0], mc) <= 1;
           }
           for (int32_t u : {act.inputs.size() == 3 ? act.inputs[0] : -1, act.inputs.size() == 3 ? act.inputs[2] : -1})
             if (addnorm && u >= 0) {
@@ -830,7 +827,6 @@ void Session::launch_one(const PlannedLaunch& l, cudaStream_t s) {
   c.param_names = pn.data();
   c.param_values = pv.data();
   c.max_ctas = l.max_ctas;
-  c.flags = l.flags;
   c.comm = comm_;
   c.aux = l.prepacked >= 0 ? (l.prepack_mode == 1 ? prepacked_act_ : prepacked_)[l.prepacked] : l.aux;
   if (l.kind == OperatorKind::kAllToAll && l.fn.empty())

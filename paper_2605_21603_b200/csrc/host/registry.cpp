@@ -107,7 +107,6 @@ size_t kind_workspace(const opf_op_ctx& c, const opf_view* in, int n_in, const o
     if (epi == 2) return 0;  // RoPE epilogue runs unsplit
     if (epi == 4)            // residual-norm epilogue: per-row, per-column-tile sums of squares
       return (static_cast<size_t>(rows * (out[0].shape[1] / 256)) * sizeof(float) + 255) / 256 * 256;
-    if (c.flags & OPF_CTX_CORESIDENT) return 0;  // co-resident variants never split K
     const int64_t N = out[0].shape[1] * (epi == 1 ? 2 : 1);
     return gemm_splitk_workspace(rows, N, in[0].shape[1], c.max_ctas);
   }
@@ -148,7 +147,6 @@ opf_status launch_kind(const opf_op_ctx& c, const opf_view* in, int n_in, opf_vi
           g.lda = K;
           g.ldc = out[0].shape[1];
           g.max_ctas = c.max_ctas;
-          g.coloc = (c.flags & OPF_CTX_CORESIDENT) != 0;
           g.epi = epi;
           g.ws = c.workspace;
           g.ws_bytes = c.workspace_bytes;

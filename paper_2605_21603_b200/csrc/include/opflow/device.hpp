@@ -125,7 +125,6 @@ struct GemmArgs {
   void* c;         // [M,N] row-major bf16, row stride ldc elements
   int64_t m, n, k, lda, ldc;
   int max_ctas;    // 0 = all SMs
-  bool coloc;      // co-resident with a concurrent lane's kernel: small-footprint 2-CTA variant, whole grid, no split-K
   bool b_kn;       // simt path only: B given as [K,N] row-major instead of [N,K]
   int epi;         // 0 plain; 1 SiLU-mul (Bt packed by k_pack_gate_up, C is [M, N/2]);
                    // 2 rotate-half RoPE on 128-wide q/k heads (C = rope(A B^T))

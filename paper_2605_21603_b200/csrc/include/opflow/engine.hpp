@@ -130,8 +130,6 @@ class Scheduler {
   virtual std::string key() const = 0;  // plan-cache key component
   // Per-lane SM budgets (max SMs a lane's GEMM / attention launches occupy;
   // 0 = all).  NanoFlow-style SM partitioning between concurrent streams.
-  // -1 = co-resident: the lane keeps every SM but takes small-footprint kernel
-  // variants so that one CTA of each concurrent lane fits an SM.
   virtual std::vector<int> lane_budgets() const { return {}; }
 };
 
@@ -174,7 +172,6 @@ struct PlannedLaunch {
   int prepack_mode = 0;          // 0 transposed, 1 gate/up interleaved (SiLU-mul epilogue)
   bool is_copy = false;          // concat fallback copy
   int max_ctas = 0;
-  int flags = 0;                 // OPF_CTX_* (co-resident with a concurrent lane)
 };
 
 struct PlannedDispatch {

@@ -273,7 +273,7 @@ __global__ void decode_simt_kernel(const T* __restrict__ qkv, const T* __restric
 bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                      const int64_t* table, const int64_t* ctx, __nv_bfloat16* out, int64_t B, int nq,
                      int nkv, int hd, int page, int64_t max_pages, float scale, int max_ctas, int hnd,
-                     bool coresident, cudaStream_t s);
+                     cudaStream_t s);
 
 // implemented in attention_tc.cu (tensor-core prefill); returns false when the
 // shape is not supported there.
@@ -372,7 +372,7 @@ opf_status op_attn_decode(const opf_op_ctx* c, const opf_view* in, int32_t n_in,
   if (in[0].dtype == OPF_BF16 && impl == 0 && ctx_param(*c, "simt", 0.0) == 0.0 &&
       decode_bf16_mma(vptr<__nv_bfloat16>(in[0]), vptr<__nv_bfloat16>(in[1]), vptr<__nv_bfloat16>(in[2]),
                       vptr<int64_t>(in[3]), vptr<int64_t>(in[4]), vptr<__nv_bfloat16>(out[0]), rows, nq,
-                      nkv, hd, page, max_pages, scale, c->max_ctas, hnd, (c->flags & OPF_CTX_CORESIDENT) != 0, s))
+                      nkv, hd, page, max_pages, scale, c->max_ctas, hnd, s))
     return launch_status("attn_decode_mma");
   if (hnd) return op_error(Errc::ShapeMismatch, "attn_decode: HND pages need the tensor-core path (bf16, hd 128, group <= 8)");
   if (in[0].dtype == OPF_BF16 && hd == 128 && grp <= kMaxGroup && impl != 2 &&

@@ -13,21 +13,16 @@
 // fp32 on the fragments; the W warps' (m, l, O) and the current token merge in
 // shared memory.  Algorithmic bytes per (sequence, kv head) = 2 * ctx * 128 * 2.
 //
-// Two shapes ship:
-//   W = 12, D = 2 (192 KB rings, one CTA per SM): the whole-GPU kernel, 0.93 of
-//     the measured HBM read peak at 512 x 4K.
-//   W = 8,  D = 2 (128 KB, <= 128 registers): the co-resident variant
-//     (OPF_CTX_CORESIDENT) that leaves room on every SM for one CTA of the 2-CTA
-//     GEMM's co-resident variant on the other lane (NanoFlow without SM
-//     partitioning: both kernels keep the whole grid).
-// Measured losers (an M = 16 padded-group kernel, a shared TMA ring, a TMA-fed
-// per-warp ring, other W x D shapes) live in the git history and DESIGN §8.
+// Shipped shape: W = 12 warps, D = 2 pages per warp (192 KB of rings, 165
+// registers, one CTA per SM), 0.93 of the measured HBM read peak at 512 x 4K
+// (DESIGN §5).  Measured losers (an M = 16 padded-group kernel, a shared TMA
+// ring, TMA-fed per-warp rings, other W x D shapes, and the co-resident 4/8-warp
+// shapes of commit 7418aec) live in the git history and DESIGN §5.1 / §8.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <cfloat>
 #include <cstdlib>
-#include <string>
 
 #include "opflow/device.hpp"
 
@@ -274,23 +269,12 @@ bool launch_decode_t(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __
 bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                      const int64_t* table, const int64_t* ctx, __nv_bfloat16* out, int64_t B, int nq,
                      int nkv, int hd, int page, int64_t max_pages, float scale, int max_ctas, int hnd,
-                     bool coresident, cudaStream_t s) {
+                     cudaStream_t s) {
   if (hd != HD || page != PAGE || nq % nkv != 0 || nq / nkv > 8) return false;
   const int64_t items = B * nkv;
   int64_t grid = max_ctas > 0 ? std::min<int64_t>(max_ctas, num_sms()) : num_sms();
   grid = std::max<int64_t>(1, std::min(grid, items));
   const float sl2 = scale * 1.4426950408889634f;
-  if (coresident) {
-    static const int v = [] {
-      const char* e = std::getenv("OPF_COLOC_ATT");
-      if (e && std::string(e) == "4x4") return 1;
-      if (e && std::string(e) == "4x3") return 2;
-      return 0;
-    }();
-    if (v == 1) return launch_decode_t<4, 4, 3>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
-    if (v == 2) return launch_decode_t<4, 3, 3>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
-    return launch_decode_t<8, 2, 2>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
-  }
   return launch_decode_t<12, 2, 1>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
 }
 

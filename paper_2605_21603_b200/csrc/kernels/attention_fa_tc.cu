@@ -982,24 +982,14 @@ bool prefill_bf16_tcgen05(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t 
   }();
   static bool attr = cudaFuncSetAttribute(fa_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(kSmemTotal)) == cudaSuccess &&
-                     cudaFuncSetAttribute(fa_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(kSmemTotal)) == cudaSuccess &&
                      cudaFuncSetAttribute(fa_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(kPPSmem)) == cudaSuccess;
   if (!enc || !attr) return false;
   // Two heads of one GQA group per item (fa_pp_kernel: registers rebalanced
   // with setmaxnreg, whole S row per thread) for even groups — measured 111 vs
-  // 126 us at 8 x 1024 tokens, 32 / 8 heads (620 vs 547 TFLOP/s); OPF_FA=single
-  // forces the one-head kernel.
-  static const bool one_tile = [] {
-    const char* e = std::getenv("OPF_FA");
-    return e && std::string(e) == "single";
-  }();
-  const bool pp = !one_tile && (nq / nkv) % 2 == 0;
-  static const int parts = [] {  // OPF_FA_PARTS=2|4 softmax column parts per row
-    const char* e = std::getenv("OPF_FA_PARTS");
-    return e && std::atoi(e) == 4 ? 4 : 2;
-  }();
+  // 126 us at 8 x 1024 tokens, 32 / 8 heads (620 vs 547 TFLOP/s); odd groups
+  // take the one-head kernel with two softmax column parts per row.
+  const bool pp = (nq / nkv) % 2 == 0;
   const int64_t W = static_cast<int64_t>(nq + 2 * nkv) * HD;
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(rows)};
@@ -1016,9 +1006,6 @@ bool prefill_bf16_tcgen05(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t 
   grid = static_cast<int>(std::min<int64_t>(grid, items));
   if (pp)
     launch_pdl(fa_pp_kernel, dim3(grid), dim3(kPPThreads), kPPSmem, s, m, out, nq, nkv, S, n_seqs,
-               scale * 1.4426950408889634f);
-  else if (parts == 4)
-    launch_pdl(fa_tc_kernel<4>, dim3(grid), dim3(128 + 4 * 128), kSmemTotal, s, m, out, nq, nkv, S, n_seqs,
                scale * 1.4426950408889634f);
   else
     launch_pdl(fa_tc_kernel<2>, dim3(grid), dim3(128 + 2 * 128), kSmemTotal, s, m, out, nq, nkv, S, n_seqs,

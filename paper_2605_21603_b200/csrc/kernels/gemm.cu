@@ -701,7 +701,7 @@ __device__ __forceinline__ void store_tile_splitk(const CUtensorMap* map_c, uint
 // there); smem-slot and accumulator-ready commits multicast to both CTAs;
 // both CTAs' epilogue warps release the accumulator on the leader's barrier.
 //
-// Tile width TN in {256, 192, 128} (OPF_GEMM_TN; 256 by default).  Epilogue
+// Tile width TN in {256, 384} (384: one-wave shapes, below).  Epilogue
 // warps: 4 (one per TMEM lane quarter, 6-stage ring) for whole-K tiles; the
 // split-K variant uses 8 (warp w reads lane quarter w % 4 and the 64-column
 // chunks (w - 2) / 4, +2: 16 independent regions per tile for the partial
@@ -714,24 +714,15 @@ __device__ __forceinline__ void store_tile_splitk(const CUtensorMap* map_c, uint
 // MMAs, N = 256 (TMEM columns 0..255, B rows 0..127 of each CTA's half) and
 // N = 128 (columns 256..383, B rows 128..191); one accumulator stage (384 of
 // the 512 TMEM columns), plain-store epilogue only.
-//
-// COLOC (co-resident lane, OPF_CTX_CORESIDENT): the same kernel in a footprint
-// that leaves room on every SM for one CTA of the concurrent lane's kernel
-// (the paged decode attention's 128 KB variant): a 2-stage ring, one staging
-// buffer per epilogue warp (82 KB of shared memory) and <= 168 registers per
-// thread (__launch_bounds__ min 2 blocks).  The whole grid stays available, so
-// the GEMM fills the tensor pipe while the attention CTAs on the same SMs wait
-// on HBM.
-template <int TN, bool SPLIT, int COLOC = 0>
+template <int TN, bool SPLIT>
 struct Tc2Cfg {
   static constexpr int kEpiW = SPLIT ? 8 : 4;
   static constexpr int kThreads = 64 + kEpiW * 32;
-  static constexpr int kMinBlocks = COLOC ? 2 : 1;
   static constexpr int kAcc = TN == 384 ? 1 : 2;       // TMEM accumulator stages
-  static constexpr int kStg = (TN == 384 || COLOC) ? 1 : 2;  // 4 KB staging buffers per epilogue warp
+  static constexpr int kStg = TN == 384 ? 1 : 2;       // 4 KB staging buffers per epilogue warp
   static constexpr uint32_t kStageBytes = kABytes + (TN / 2) * BK * 2;
   static constexpr uint32_t kFixed = 1024 + kEpiW * kStg * kEpiBytes + 512;
-  static constexpr int kStages = COLOC ? COLOC : (((232448 - kFixed) / kStageBytes) > 6 ? 6 : (232448 - kFixed) / kStageBytes);
+  static constexpr int kStages = ((232448 - kFixed) / kStageBytes) > 6 ? 6 : (232448 - kFixed) / kStageBytes;
   static constexpr uint32_t kSmemBytes = kFixed + kStages * kStageBytes;
   static constexpr uint32_t idesc(int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
@@ -1021,15 +1012,14 @@ __device__ int g_gemm_trace_n[3];
   } while (0)
 #endif
 
-template <int EPI, int TN, bool SPLIT = false, bool GROUPED = false, int COLOC = 0>
-__global__ void __cluster_dims__(2, 1, 1)
-    __launch_bounds__(Tc2Cfg<TN, SPLIT, COLOC>::kThreads, Tc2Cfg<TN, SPLIT, COLOC>::kMinBlocks)
+template <int EPI, int TN, bool SPLIT = false, bool GROUPED = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K, int splits,
                     float4* __restrict__ ws, int* __restrict__ sem, RopeArgs rope,
                     const int32_t* __restrict__ gtab, __nv_bfloat16* __restrict__ c_out,
                     int64_t ldc, PushArgs push) {
-  using C = Tc2Cfg<TN, SPLIT, COLOC>;
+  using C = Tc2Cfg<TN, SPLIT>;
   constexpr int kStages2 = C::kStages;
   constexpr uint32_t kStageBytes2 = C::kStageBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1295,10 +1285,6 @@ void gemm_bf16_tc_init() {
                                   static_cast<int>(kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
-    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(Tc2Cfg<192, false>::kSmemBytes)));
-    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(Tc2Cfg<128, false>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tc2Cfg<384, false>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<2, 384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1311,21 +1297,6 @@ void gemm_bf16_tc_init() {
                                   static_cast<int>(Tc2Cfg<256, true>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tc2Cfg<256, true>::kSmemBytes)));
-    // co-resident variants: the whole shared-memory carveout, so that an SM
-    // running one of them keeps room for the concurrent lane's CTA
-    auto coloc = [](auto kern, int bytes) {
-      OPF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      OPF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    };
-    constexpr int b2 = Tc2Cfg<256, false, 2>::kSmemBytes, b3 = Tc2Cfg<256, false, 3>::kSmemBytes;
-    coloc(gemm_tc2_kernel<0, 256, false, false, 2>, b2);
-    coloc(gemm_tc2_kernel<1, 256, false, false, 2>, b2);
-    coloc(gemm_tc2_kernel<2, 256, false, false, 2>, b2);
-    coloc(gemm_tc2_kernel<4, 256, false, false, 2>, b2);
-    coloc(gemm_tc2_kernel<0, 256, false, false, 3>, b3);
-    coloc(gemm_tc2_kernel<1, 256, false, false, 3>, b3);
-    coloc(gemm_tc2_kernel<2, 256, false, false, 3>, b3);
-    coloc(gemm_tc2_kernel<4, 256, false, false, 3>, b3);
   });
 }
 
@@ -1349,11 +1320,6 @@ int gemm_splitk_splits(int64_t m, int64_t n, int64_t k, int max_ctas) {
     const char* e = std::getenv("OPF_GEMM_SPLITK");
     return e ? std::atoi(e) : -1;
   }();
-  static const int tn_forced = [] {
-    const char* e = std::getenv("OPF_GEMM_TN");
-    return e ? std::atoi(e) : 256;
-  }();
-  if (tn_forced == 192 || tn_forced == 128) return 1;
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   const int64_t clusters = std::max(grid / 2, 1);
@@ -1398,63 +1364,26 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     if (e && std::string(e) == "2sm") return 2;
     return 0;
   }();
-  const bool pair = mode == 2 || (mode == 0 && g.m > BM) || g.epi == 4 || g.coloc;  // EPI 4 lives in the 2-CTA kernel
+  const bool pair = mode == 2 || (mode == 0 && g.m > BM) || g.epi == 4;  // EPI 4 lives in the 2-CTA kernel
   const int64_t n_out = g.epi == 1 ? g.n / 2 : g.n;
   const CUtensorMap ma = make_map(g.a, g.k, g.m, g.lda, BK, BM);
   const CUtensorMap mc = make_map(g.c, n_out, g.m, g.ldc, 64, 32);
   int grid = num_sms();
   if (g.max_ctas > 0 && g.max_ctas < grid) grid = g.max_ctas;
-  if (pair && g.coloc) {  // co-resident lane: small-footprint variants, 256-wide tiles, no split-K
-    const int64_t mt = (g.m + 2 * BM - 1) / (2 * BM);
-    const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, 128);
-    const int64_t tiles = mt * ((g.n + 255) / 256);
-    const int clusters = static_cast<int>(std::min<int64_t>(tiles, std::max(grid / 2, 1)));
-    const dim3 blocks(2u * static_cast<unsigned>(std::max(clusters, 1)));
-    static const int stages = [] {
-      const char* e = std::getenv("OPF_COLOC_STAGES");
-      return e && std::atoi(e) == 3 ? 3 : 2;
-    }();
-    auto go = [&](auto kern, auto cfg) {
-      using CC = decltype(cfg);
-      launch_pdl(kern, blocks, dim3(CC::kThreads), CC::kSmemBytes, s, ma, mb, mc, g.m, g.n, g.k, 1,
-                 static_cast<float4*>(nullptr), static_cast<int*>(nullptr), rope, kNoGtab,
-                 static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
-    };
-    auto pick = [&](auto c2, auto c3, auto k2, auto k3) {
-      if (stages == 3) go(k3, c3); else go(k2, c2);
-    };
-    using C2 = Tc2Cfg<256, false, 2>;
-    using C3 = Tc2Cfg<256, false, 3>;
-    if (g.epi == 1)
-      pick(C2{}, C3{}, gemm_tc2_kernel<1, 256, false, false, 2>, gemm_tc2_kernel<1, 256, false, false, 3>);
-    else if (g.epi == 2)
-      pick(C2{}, C3{}, gemm_tc2_kernel<2, 256, false, false, 2>, gemm_tc2_kernel<2, 256, false, false, 3>);
-    else if (g.epi == 4)
-      pick(C2{}, C3{}, gemm_tc2_kernel<4, 256, false, false, 2>, gemm_tc2_kernel<4, 256, false, false, 3>);
-    else
-      pick(C2{}, C3{}, gemm_tc2_kernel<0, 256, false, false, 2>, gemm_tc2_kernel<0, 256, false, false, 3>);
-    return;
-  }
   if (pair) {
     const int64_t mt = (g.m + 2 * BM - 1) / (2 * BM);
     const int cmax = std::max(grid / 2, 1);
-    // Tile width: 256 unless OPF_GEMM_TN forces 192 / 128.  Narrower tiles
-    // quantise better onto 74 clusters (e.g. N = 768: 96 -> 128 tiles) but
-    // measured slower per FLOP on B200 (more L2 -> SMEM bytes per MAC), so the
-    // rounds x width model alone picks them wrongly (profiles/r01_gemm_sweep*.json).
+    // Tile width 256, or 384 for one-wave shapes.  (Narrower 192 / 128 tiles
+    // quantise better onto 74 clusters, e.g. N = 768: 96 -> 128 tiles, but
+    // measured slower per FLOP on B200 — more L2 -> SMEM bytes per MAC —
+    // profiles/r01_gemm_sweep*.json; they were removed in round 2.)
     int tn = 256;
     if (g.epi == 0 || g.epi == 2) {
-      static const int forced = [] {
-        const char* e = std::getenv("OPF_GEMM_TN");
-        const int v = e ? std::atoi(e) : 0;
-        return (v == 192 || v == 128 || v == 384) ? v : 0;
-      }();
       // 256x384 tiles when they fit one round of clusters and 256-wide ones
       // would need two (a ~1.3-wave tail): e.g. 8192 x 768 -> 64 tiles, not 96
       const int64_t t256 = mt * ((g.n + 255) / 256), t384 = mt * ((g.n + 383) / 384);
       const bool one_wave_384 = g.n % 384 == 0 && t384 <= cmax && t256 > cmax && g.k >= 1024;
-      tn = forced ? forced : (one_wave_384 ? 384 : 256);
-      if ((tn == 384 && g.n % 384 != 0) || (g.epi == 2 && tn != 384)) tn = 256;
+      tn = one_wave_384 ? 384 : 256;
     }
     const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, static_cast<uint32_t>(tn == 384 ? 64 : tn / 2));
     const int64_t tiles = mt * ((g.n + tn - 1) / tn);
@@ -1495,14 +1424,8 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     else if (tn == 256)
       launch_pdl(gemm_tc2_kernel<0, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
                  g.n, g.k, splits, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
-    else if (tn == 384)
-      launch_pdl(gemm_tc2_kernel<0, 384>, blocks, dim3(Tc2Cfg<384, false>::kThreads), Tc2Cfg<384, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
-    else if (tn == 192)
-      launch_pdl(gemm_tc2_kernel<0, 192>, blocks, dim3(Tc2Cfg<192, false>::kThreads), Tc2Cfg<192, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else
-      launch_pdl(gemm_tc2_kernel<0, 128>, blocks, dim3(Tc2Cfg<128, false>::kThreads), Tc2Cfg<128, false>::kSmemBytes, s, ma, mb, mc, g.m,
+      launch_pdl(gemm_tc2_kernel<0, 384>, blocks, dim3(Tc2Cfg<384, false>::kThreads), Tc2Cfg<384, false>::kSmemBytes, s, ma, mb, mc, g.m,
                  g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     return;
   }

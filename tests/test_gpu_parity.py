@@ -209,12 +209,6 @@ def test_llama_decode_bf16(cuda, kv_layout):
         got, _ = run_graph(desc, 16, host, strat)
         for k in want:
             assert rel_err(got[k], want[k]) < 2e-2
-    # NanoFlow with co-resident lanes (lane SM budget -1): the small-footprint
-    # 2-CTA GEMM and the 8-warp decode attention share every SM
-    got, _ = run_graph(desc, 16, host, {"name": "split_overlap", "n_microbatches": 2, "lane_sm_budget": [-1, -1, 0]},
-                       [of.PartitionRule.by_func("attn_decode")])
-    for k in want:
-        assert rel_err(got[k], want[k]) < 2e-2
 
 
 @pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 512, 1024), (300, 520, 200), (1, 256, 64),
@@ -240,15 +234,6 @@ def test_gemm_tcgen05_vs_torch(cuda, m, n, k):
     want = a.float() @ w.float()
     err = ((c.float() - want).norm() / want.norm()).item()
     assert err < 1e-2, err
-    # the co-resident 2-CTA variant (lane SM budget -1: 2-stage ring, no split-K)
-    sess2 = of.Session(gr, of.partition(gr, []), {"lanes": 1, "lane_sm_budget": [-1]})
-    c3 = torch.empty_like(c)
-    for name, t in (("a", a), ("w", w), ("c", c3)):
-        sess2.bind(name, t)
-    sess2.run()
-    torch.cuda.synchronize()
-    err3 = ((c3.float() - want).norm() / want.norm()).item()
-    assert err3 < 1e-2, err3
     # the CUDA-core reference path (direct opf_launch on the [K,N] weight) agrees
     c2 = torch.empty_like(c)
     of.launch({"name": "mm", "kind": "MatMul", "inputs": [], "outputs": []}, [a, w], [c2], m)
@@ -303,36 +288,6 @@ def test_prefill_attention_tensor_core(cuda, S, nq, nkv, seqs):
     torch.cuda.synchronize()
     assert rel_err(out.float().cpu().numpy(), want) < 1e-2
     assert rel_err(out2.float().cpu().numpy(), want) < 1e-2
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("tn", [192, 128])
-def test_gemm_tile_width_variants(tn):
-    """The 2-CTA kernel's narrower tile widths (OPF_GEMM_TN, read once per
-    process) stay correct: ragged N, short and long K."""
-    import subprocess
-    import sys
-    code = (
-        "import torch,json,sys; sys.path.insert(0, '.');"
-        "from paper_2605_21603_b200 import opflow as of\n"
-        "for (m,n,k) in [(8192,768,4096),(4096,712,256),(1000,3584,512)]:\n"
-        "  g=torch.Generator(device='cuda').manual_seed(m+n)\n"
-        "  a=(torch.rand(m,k,device='cuda',generator=g)*2-1).to(torch.bfloat16)\n"
-        "  w=((torch.rand(k,n,device='cuda',generator=g)*2-1)/k**0.5).to(torch.bfloat16)\n"
-        "  d=json.dumps({'tensors':[{'name':'a','shape':[m,k],'dtype':'bf16','role':'input'},"
-        "{'name':'w','shape':[k,n],'batch':'replicated','dtype':'bf16','role':'weight'},"
-        "{'name':'c','shape':[m,n],'dtype':'bf16','role':'output'}],'operators':[{'name':'mm','kind':'MatMul',"
-        "'inputs':['a','w'],'outputs':['c']}]})\n"
-        "  gr=of.build_graph(d); s=of.Session(gr, of.partition(gr, []), {'lanes':1})\n"
-        "  c=torch.empty(m,n,dtype=torch.bfloat16,device='cuda'); s.bind('a',a); s.bind('w',w); s.bind('c',c); s.run()\n"
-        "  torch.cuda.synchronize(); want=a.float()@w.float()\n"
-        "  e=((c.float()-want).norm()/want.norm()).item(); assert e<1e-2,(m,n,k,e)\n"
-        "print('ok')\n")
-    import os
-    env = dict(os.environ, OPF_GEMM_TN=str(tn))
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
-                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
 @pytest.mark.gpu

@@ -2,7 +2,11 @@
 paged decode attention of one nano-batch (256 x 4K context) and the GEMMs of
 the other (M = 256), each timed alone and both launched concurrently on two
 streams, for the whole-GPU kernels and the co-resident (lane SM budget -1)
-variants.  Usage: python tools/coresident_probe.py"""
+variants.  The co-resident variants (lane SM budget -1: 2/3-stage 2-CTA GEMM,
+4/8-warp attention, OPF_COLOC_ATT / OPF_COLOC_STAGES) exist only in the library
+of commit 7418aec: `git checkout 7418aec -- paper_2605_21603_b200/csrc` and
+rebuild to reproduce.  Measured: no configuration beats running
+the two whole-GPU kernels back to back.  Usage: python tools/coresident_probe.py"""
 import json
 import os
 import sys
