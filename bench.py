@@ -291,33 +291,66 @@ def with_auto(cands, world):
     return dict(cands, dynaflow_auto=auto_spec(cands))
 
 
-def gemm_roofline(of, torch, dev, shapes, reps=20):
-    """Time each projection GEMM alone (tcgen05 kernel, CUDA events on its
-    stream, inputs > L2 rotated); FLOP-weighted achieved TFLOP/s."""
+def graph_reps_ms(of, torch, dev, stream, tensors, op, shared, reps):
+    """Device time of ONE op, measured as `reps` copies of it back to back in
+    one CUDA graph (a one-lane sequential Session), CUDA events on `stream`
+    around the replay: no host gap between launches (a per-launch Session.run
+    costs tens of us of host time, more than a TP=8 skinny GEMM).  Every copy
+    has its own inputs and outputs except the names in `shared`, so the
+    inputs rotate through reps x (per-copy bytes) > L2 instead of re-hitting
+    a warm L2.  `tensors`: [(name, torch tensor, role)], `op`: the op dict."""
+    descs, ops, binds = [], [], []
+    for r in range(reps):
+        ren = {n: (n if n in shared else f"{n}_{r}") for n, _, _ in tensors}
+        for n, x, role in tensors:
+            if n in shared and r > 0:
+                continue
+            dt = {torch.bfloat16: "bf16", torch.int64: "i64", torch.float32: "f32"}[x.dtype]
+            t = {"name": ren[n], "shape": list(x.shape), "dtype": dt, "role": role}
+            if role == "weight":
+                t["batch"] = "replicated"
+            descs.append(t)
+            binds.append((ren[n], x if (n in shared or r == 0) else x.clone()))
+        o = dict(op, name=f"{op['name']}_{r}", inputs=[ren[i] for i in op["inputs"]],
+                 outputs=[ren[i] for i in op["outputs"]])
+        ops.append(o)
+    g = of.build_graph(json.dumps({"tensors": descs, "operators": ops}))
+    sess = of.Session(g, of.partition(g, []), {"lanes": 1, "device": dev.index})
+    keep = []
+    for n, x in binds:
+        keep.append(x)
+        sess.bind(n, x)
+    for _ in range(3):
+        sess.run(None, stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for _ in range(3):
+        e0.record(stream)
+        sess.run(None, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / reps)
+    del sess, keep
+    torch.cuda.empty_cache()
+    return sorted(times)[1]
+
+
+def gemm_roofline(of, torch, dev, shapes, reps=8):
+    """Each projection GEMM (tcgen05 kernel) timed on the device: `reps`
+    launches back to back in one CUDA graph, each with its own A / W / C
+    (rotated, > L2), CUDA events on the launching stream; FLOP-weighted
+    achieved TFLOP/s."""
     tot_flops, tot_ms, rows = 0.0, 0.0, []
     stream = torch.cuda.current_stream(dev)
     for name, (m, k, n) in shapes.items():
-        desc = json.dumps({"tensors": [
-            {"name": "a", "shape": [m, k], "dtype": "bf16", "role": "input"},
-            {"name": "w", "shape": [k, n], "batch": "replicated", "dtype": "bf16", "role": "weight"},
-            {"name": "c", "shape": [m, n], "dtype": "bf16", "role": "output"}],
-            "operators": [{"name": "mm", "kind": "MatMul", "inputs": ["a", "w"], "outputs": ["c"]}]})
-        g = of.build_graph(desc)
-        sess = of.Session(g, of.partition(g, []), {"lanes": 1, "device": dev.index})
         a = torch.randn(m, k, device=dev, dtype=torch.bfloat16)
         w = (torch.randn(k, n, device=dev, dtype=torch.bfloat16) / k ** 0.5).to(torch.bfloat16)
         c = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
-        sess.bind("a", a), sess.bind("w", w), sess.bind("c", c)
-        for _ in range(3):
-            sess.run(None, stream)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(reps):
-            sess.run(None, stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / reps
+        op = {"name": "mm", "kind": "MatMul", "inputs": ["a", "w"], "outputs": ["c"]}
+        ms = graph_reps_ms(of, torch, dev, stream, [("a", a, "input"), ("w", w, "weight"), ("c", c, "output")],
+                           op, shared=(), reps=reps)
+        del a, w, c
         fl = 2.0 * m * n * k
         tot_flops += fl
         tot_ms += ms
@@ -327,7 +360,6 @@ def gemm_roofline(of, torch, dev, shapes, reps=20):
         if tr:
             row["ncu_dram_bytes"] = tr["dram_bytes"]
         rows.append(row)
-        del sess
     achieved = tot_flops / tot_ms / 1e9
     return achieved, rows
 
@@ -632,34 +664,13 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
 QWEN3 = dict(hidden=2048, heads=32, kv_heads=4, head_dim=128, experts=128, topk=8, moe_inter=768)
 
 
-def time_op(of, torch, dev, stream, fn, ins, outs, params, rows, reps=20):
-    """One registered op through a one-op Session (prepack + workspace planned
-    by the engine), CUDA events on `stream` around back-to-back graph replays."""
-    tensors = []
-    for name, x, role in ins + outs:
-        dt = {torch.bfloat16: "bf16", torch.int64: "i64", torch.float32: "f32"}[x.dtype]
-        t = {"name": name, "shape": list(x.shape), "dtype": dt, "role": role}
-        if role == "weight":
-            t["batch"] = "replicated"
-        tensors.append(t)
-    desc = json.dumps({"tensors": tensors, "operators": [
-        {"name": "op", "kind": "Custom", "inputs": [i[0] for i in ins], "outputs": [o[0] for o in outs],
-         "attrs": {"custom_name": fn, "params": params}}]})
-    g = of.build_graph(desc)
-    sess = of.Session(g, of.partition(g, []), {"lanes": 1, "device": dev.index})
-    for name, x, _ in ins + outs:
-        sess.bind(name, x)
-    for _ in range(3):
-        sess.run(None, stream)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(reps):
-        sess.run(None, stream)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    del sess
-    return e0.elapsed_time(e1) / reps
+def time_op(of, torch, dev, stream, fn, ins, outs, params, rows, reps=8, shared=()):
+    """One registered op (prepack + workspace planned by the engine) timed on
+    the device: `reps` copies back to back in one CUDA graph, rotated inputs
+    (names in `shared` are bound once), CUDA events on `stream`."""
+    op = {"name": "op", "kind": "Custom", "inputs": [i[0] for i in ins], "outputs": [o[0] for o in outs],
+          "attrs": {"custom_name": fn, "params": params}}
+    return graph_reps_ms(of, torch, dev, stream, list(ins) + list(outs), op, shared=shared, reps=reps)
 
 
 def run_moe(of, torch, dev, args, rank, world, stream, comm=None, window_ok=True):

@@ -23,6 +23,7 @@
 
 #include <cfloat>
 #include <cstdlib>
+#include <string>
 
 #include "opflow/device.hpp"
 
@@ -42,6 +43,18 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 }
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+// KV bytes are read exactly once per step: mark their L2 lines evict-first so
+// the 8.6 GB/layer stream does not evict the operands a concurrent GEMM (the
+// other nano-batch's projections) re-reads across its N tiles.
+__device__ __forceinline__ void cp16_ef(uint32_t dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 __device__ __forceinline__ void ldsm4(uint32_t a, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -70,7 +83,7 @@ __device__ __forceinline__ uint32_t pk(float lo, float hi) {
 // per page, a 32-float accumulator.  P^T reaches the B-fragment layout through 8
 // shuffles; the softmax reduces over tokens (lane bits 2..4).  W warps with
 // D-deep private cp.async page rings (W x D x 8 KB of smem).
-template <int W, int D, int MinBlocks>
+template <int W, int D, int MinBlocks, bool EF>
 __global__ void __launch_bounds__(W * 32, MinBlocks)
     decode_t_kernel(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ kc,
                     const __nv_bfloat16* __restrict__ vc, const int64_t* __restrict__ table,
@@ -82,6 +95,7 @@ __global__ void __launch_bounds__(W * 32, MinBlocks)
   pdl_trigger();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int g = lane >> 2, t = lane & 3;
+  const uint64_t pol = EF ? evict_first_policy() : 0;
   for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int64_t b = item / nkv;
     const int kh = static_cast<int>(item % nkv);
@@ -107,8 +121,13 @@ __global__ void __launch_bounds__(W * 32, MinBlocks)
       for (int i = 0; i < 8; ++i) {
         const int idx = i * 32 + lane;
         const int r = idx >> 4, c = idx & 15;
-        cp16(kd + swz(r, c), kp + r * tok_stride + c * 8);
-        cp16(vd + swz(r, c), vp + r * tok_stride + c * 8);
+        if constexpr (EF) {
+          cp16_ef(kd + swz(r, c), kp + r * tok_stride + c * 8, pol);
+          cp16_ef(vd + swz(r, c), vp + r * tok_stride + c * 8, pol);
+        } else {
+          cp16(kd + swz(r, c), kp + r * tok_stride + c * 8);
+          cp16(vd + swz(r, c), vp + r * tok_stride + c * 8);
+        }
       }
     };
     // Q^T as the B operand: n = head g of the group (zero for g >= G), k = dims
@@ -249,19 +268,19 @@ __global__ void __launch_bounds__(W * 32, MinBlocks)
 
 }  // namespace
 
-template <int W, int D, int MinBlocks>
+template <int W, int D, int MinBlocks, bool EF>
 bool launch_decode_t(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                      const int64_t* table, const int64_t* ctx, __nv_bfloat16* out, int nq, int nkv,
                      int64_t max_pages, float scale_log2, int64_t items, int64_t grid, int hnd,
                      cudaStream_t s) {
   constexpr int kSmem = W * D * 2 * kPageBytes;
   static_assert(kSmem >= (W * 8 * (HD + 2) + 8) * 4, "merge buffers fit in the rings");
-  static bool attr = cudaFuncSetAttribute(decode_t_kernel<W, D, MinBlocks>,
+  static bool attr = cudaFuncSetAttribute(decode_t_kernel<W, D, MinBlocks, EF>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) == cudaSuccess &&
-                     cudaFuncSetAttribute(decode_t_kernel<W, D, MinBlocks>,
+                     cudaFuncSetAttribute(decode_t_kernel<W, D, MinBlocks, EF>,
                                           cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess;
   if (!attr) return false;
-  launch_pdl(decode_t_kernel<W, D, MinBlocks>, dim3(static_cast<unsigned>(grid)), dim3(W * 32), kSmem, s, qkv,
+  launch_pdl(decode_t_kernel<W, D, MinBlocks, EF>, dim3(static_cast<unsigned>(grid)), dim3(W * 32), kSmem, s, qkv,
              kc, vc, table, ctx, out, nq, nkv, max_pages, scale_log2, items, hnd);
   return true;
 }
@@ -275,7 +294,13 @@ bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __
   int64_t grid = max_ctas > 0 ? std::min<int64_t>(max_ctas, num_sms()) : num_sms();
   grid = std::max<int64_t>(1, std::min(grid, items));
   const float sl2 = scale * 1.4426950408889634f;
-  return launch_decode_t<12, 2, 1>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
+  static const bool ef = [] {
+    const char* e = std::getenv("OPF_DECODE_L2");  // "normal": plain cp.async (A/B switch)
+    return !(e && std::string(e) == "normal");
+  }();
+  if (ef)
+    return launch_decode_t<12, 2, 1, true>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
+  return launch_decode_t<12, 2, 1, false>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
 }
 
 }  // namespace opflow
