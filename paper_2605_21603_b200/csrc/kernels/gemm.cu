@@ -190,13 +190,18 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
 
 __device__ __forceinline__ void tile_coords(int64_t t, int64_t m_blocks, int64_t n_blocks,
                                             int64_t& mb, int64_t& nb) {
-  const int64_t per_group = static_cast<int64_t>(kGroupM) * n_blocks;
-  const int64_t g = t / per_group;
-  const int64_t first_m = g * kGroupM;
-  const int64_t gm = min(static_cast<int64_t>(kGroupM), m_blocks - first_m);
-  const int64_t r = t % per_group;
-  mb = first_m + r % gm;
-  nb = r / gm;
+  // 32-bit arithmetic: tile counts fit easily, and a 64-bit divide is a ~70
+  // instruction software routine on the single producer / MMA thread, paid per
+  // tile (measured ~600 cycles between two tiles' MMAs on K = 512 shapes)
+  const uint32_t tt = static_cast<uint32_t>(t), mbk = static_cast<uint32_t>(m_blocks);
+  const uint32_t per_group = static_cast<uint32_t>(kGroupM) * static_cast<uint32_t>(n_blocks);
+  const uint32_t g = tt / per_group;
+  const uint32_t first_m = g * kGroupM;
+  const uint32_t gm = min(static_cast<uint32_t>(kGroupM), mbk - first_m);
+  const uint32_t r = tt - g * per_group;
+  const uint32_t q = r / gm;
+  mb = first_m + (r - q * gm);
+  nb = q;
 }
 
 // Epilogue of one accumulator tile for one warp (32 rows): TMEM -> registers
@@ -1082,8 +1087,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t u = cluster; u < units; u += n_clusters) {
-        const int64_t t = u / splits;
-        const int sp = static_cast<int>(u % splits);
+        const int64_t t = splits == 1 ? u : static_cast<int64_t>(static_cast<uint32_t>(u) / static_cast<uint32_t>(splits));
+        const int sp = static_cast<int>(u - t * splits);
         int64_t mb, nb;
         tile_coords(t, m_blocks, n_blocks, mb, nb);
         int32_t m0 = static_cast<int32_t>(mb * 2 * BM + rank * BM);
@@ -1092,7 +1097,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
           m0 = gtab[1 + 3 * mb] + static_cast<int32_t>(rank * BM);
           n0 += static_cast<int32_t>(gtab[3 + 3 * mb] * N);
         }
-        const int kb0 = sp * k_blocks / splits, kb1 = (sp + 1) * k_blocks / splits;
+        const int kb0 = splits == 1 ? 0 : sp * k_blocks / splits;
+        const int kb1 = splits == 1 ? k_blocks : (sp + 1) * k_blocks / splits;
         GTRACE(0, 0, u);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -1125,8 +1131,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int64_t u = cluster; u < units; u += n_clusters) {
-        const int sp = static_cast<int>(u % splits);
-        const int kb0 = sp * k_blocks / splits, kb1 = (sp + 1) * k_blocks / splits;
+        const int sp = splits == 1 ? 0 : static_cast<int>(static_cast<uint32_t>(u) % static_cast<uint32_t>(splits));
+        const int kb0 = splits == 1 ? 0 : sp * k_blocks / splits;
+        const int kb1 = splits == 1 ? k_blocks : (sp + 1) * k_blocks / splits;
         GTRACE(1, 0, u);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         GTRACE(1, 1, u);
@@ -1171,7 +1178,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
     uint32_t acc_phase = 0;
     int buf = 0;
     for (int64_t u = cluster; u < units; u += n_clusters) {
-      const int64_t t = u / splits;
+      const int64_t t = splits == 1 ? u : static_cast<int64_t>(static_cast<uint32_t>(u) / static_cast<uint32_t>(splits));
       int64_t mb, nb;
       tile_coords(t, m_blocks, n_blocks, mb, nb);
       if (warp == 2 && lane == 0) GTRACE(2, 0, u);
@@ -1202,7 +1209,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
         store_tile_push<TN>(tcol, stg[0], lane, nb, row0, M, N, push, release);
       } else if constexpr (SPLIT && TN == 256) {
         store_tile_splitk<EPI>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, static_cast<int>(rank) * 8 + ew, t,
-                               static_cast<int>(u % splits), splits, ws, sem, release);
+                               static_cast<int>(u - t * splits), splits, ws, sem, release);
       } else if constexpr (EPI == 2) {
         store_tile_rope_st<TN>(tcol, stg[0], lane, nb, row0, M, N, c_out, ldc, rope, release);
       } else {

@@ -16,15 +16,18 @@
 //   moe_combine  yd, slot, w -> y [T,H] = sum_j w[t,j] * yd[slot[t,j]]  (j ascending)
 //
 // Routing is a stable counting sort over the T*k (token, j) slots: per-chunk
-// expert histograms, one scan CTA, then one warp per chunk ranks equal experts
-// with __match_any_sync so positions follow slot order — bit-identical to a
-// stable argsort (the oracle's restatement).  Ids outside [0,E) are dropped
+// expert histograms, then one CTA per chunk derives its bases from the whole
+// count matrix and ranks equal experts (per-warp counts + __match_any_sync) so
+// positions follow slot order — bit-identical to a stable argsort (the
+// oracle's restatement).  Ids outside [0,E) are dropped
 // (slot = -1, no contribution).  All index work is exact; the grouped GEMM's
 // tile table (row0, row_end, expert per 128-row tile) is rebuilt on the device
 // by each GEMM op from `ids`, so every launch is graph-capturable (no host sync).
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cfloat>
+#include <mutex>
 
 #include "opflow/device.hpp"
 #include "opflow/p2p.cuh"
@@ -33,7 +36,6 @@ namespace opflow {
 
 namespace {
 
-constexpr int kChunk = 256;  // slots per routing chunk (one hist CTA / one assign warp each)
 constexpr int kMaxE = 1024;
 
 __device__ __forceinline__ bool valid_id(int64_t e, int E) { return e >= 0 && e < E; }
@@ -110,16 +112,37 @@ __global__ void __launch_bounds__(256) topk_kernel(const T* __restrict__ logits,
 }
 
 // ---------------------------------------------------------------- routing
-// per-chunk expert histograms: cnt[c * E + e]
-__global__ void __launch_bounds__(256) route_hist_kernel(const int64_t* __restrict__ ids, int64_t n, int E,
-                                                         int32_t* __restrict__ cnt) {
+// Stable counting sort of the n = T*k slots by expert in THREE launches:
+//   route_hist_kernel   C CTAs, one chunk of `chunk` slots each -> cnt[c][e]
+//   route_assign_kernel C CTAs: every CTA loads the whole C x E count matrix
+//                       (<= 64 KB) into smem and derives its own bases
+//                       (expert offsets + the counts of earlier chunks) —
+//                       no separate scan launch — then ranks its slots round
+//                       by round (1024 per round: per-warp expert counts,
+//                       a scan over the 32 warps, __match_any_sync inside a warp)
+//   gather_tokens_kernel one warp per token: the row is read once and
+//                       written to its k expert-sorted rows
+// The grouped GEMMs only need the tile table: route_hist + route_tiles_kernel.
+// C <= 64 and C * E <= 16384 keep the count matrix in shared memory.
+constexpr int kRouteThreads = 1024;
+
+int64_t route_chunk(int64_t n, int E) {
+  const int64_t cmax = std::max<int64_t>(1, std::min<int64_t>(64, 16384 / E));
+  const int64_t per = (n + cmax - 1) / cmax;
+  return std::max<int64_t>(kRouteThreads, (per + kRouteThreads - 1) / kRouteThreads * kRouteThreads);
+}
+int64_t route_chunks(int64_t n, int E) { return n > 0 ? (n + route_chunk(n, E) - 1) / route_chunk(n, E) : 0; }
+
+__global__ void __launch_bounds__(kRouteThreads) route_hist_kernel(const int64_t* __restrict__ ids, int64_t n, int E,
+                                                                   int64_t chunk, int32_t* __restrict__ cnt) {
   pdl_wait();
-  __shared__ int32_t h[kMaxE];
+  extern __shared__ int32_t h[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) h[e] = 0;
   __syncthreads();
-  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kChunk;
-  for (int i = threadIdx.x; i < kChunk && s0 + i < n; i += blockDim.x) {
-    const int64_t e = ids[s0 + i];
+  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t s1 = s0 + chunk < n ? s0 + chunk : n;
+  for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
+    const int64_t e = ids[s];
     if (valid_id(e, E)) atomicAdd(&h[e], 1);
   }
   __syncthreads();
@@ -127,130 +150,168 @@ __global__ void __launch_bounds__(256) route_hist_kernel(const int64_t* __restri
   pdl_trigger();
 }
 
-// One CTA: base[c][e] = off[e] + sum_{c' < c} cnt[c'][e]  (in place over cnt),
-// and (optionally) the grouped-GEMM tile table.  Thread (part p, expert e)
-// owns a contiguous range of chunks of column e (P = 1024 / E parts): range
-// sums -> per-part prefixes -> a block-wide scan over experts (totals and
-// tile counts) -> the range rewritten as running bases.  Loads are batched 8
-// deep so the latency of the column walk is paid C / (8 P) times, not C.
-__global__ void __launch_bounds__(1024) route_scan_kernel(int32_t* __restrict__ cnt, int chunks, int E,
-                                                          int32_t* __restrict__ gtab, int tile_m,
-                                                          int32_t* __restrict__ tot_out, int32_t* __restrict__ off_out) {
-  pdl_wait();
-  __shared__ int32_t psum[1024], sc[kMaxE], st[kMaxE];
-  const int tid = threadIdx.x;
-  const int P = E >= 1024 ? 1 : 1024 / E;
-  const int e = tid % E, p = tid / E;
-  const bool act = tid < P * E;
-  const int c0 = act ? static_cast<int>(static_cast<int64_t>(p) * chunks / P) : 0;
-  const int c1 = act ? static_cast<int>(static_cast<int64_t>(p + 1) * chunks / P) : 0;
-  int32_t sum = 0;
-  for (int c = c0; c < c1; c += 8) {
-    int32_t v[8];
+// exclusive block scan of one value per thread (1024 threads); returns the
+// exclusive prefix, *total = the sum over the block
+__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* warp_tot, int32_t* total) {
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  int32_t x = v;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = c + i < c1 ? cnt[static_cast<int64_t>(c + i) * E + e] : 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) sum += v[i];
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
-  if (act) psum[tid] = sum;
+  if (lane == 31) warp_tot[w] = x;
   __syncthreads();
-  if (act && p == 0) {  // exclusive prefix over this expert's parts; totals
-    int32_t r = 0;
-    for (int q = 0; q < P; ++q) {
-      const int32_t t = psum[q * E + e];
-      psum[q * E + e] = r;
-      r += t;
+  if (w == 0) {
+    int32_t t = warp_tot[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
     }
-    sc[e] = r;
-    st[e] = (r + tile_m - 1) / tile_m;
+    warp_tot[lane] = t;  // inclusive over warps
   }
   __syncthreads();
-  for (int d = 1; d < E; d <<= 1) {  // inclusive scan over experts (rows, tiles)
-    int32_t a = 0, b = 0;
-    if (tid < E && tid >= d) {
-      a = sc[tid - d];
-      b = st[tid - d];
-    }
-    __syncthreads();
-    if (tid < E && tid >= d) {
-      sc[tid] += a;
-      st[tid] += b;
-    }
-    __syncthreads();
-  }
-  if (gtab && tid == 0) gtab[0] = st[E - 1];
-  if (act) {
-    const int32_t off = e ? sc[e - 1] : 0;
-    int32_t run = off + psum[tid];
-    for (int c = c0; c < c1; c += 8) {
-      int32_t v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = c + i < c1 ? cnt[static_cast<int64_t>(c + i) * E + e] : 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (c + i < c1) {
-          cnt[static_cast<int64_t>(c + i) * E + e] = run;
-          run += v[i];
-        }
-    }
-    if (p == 0) {
-      const int32_t tot = sc[e] - off;
-      if (tot_out) tot_out[e] = tot;
-      if (off_out) off_out[e] = off;
-      if (gtab) {
-        const int32_t end = off + tot;
-        int32_t* g = gtab + 1 + 3 * (e ? st[e - 1] : 0);
-        for (int32_t r = off, i = 0; r < end; r += tile_m, ++i) {
-          g[3 * i] = r;
-          g[3 * i + 1] = end;
-          g[3 * i + 2] = e;
-        }
-      }
-    }
-  }
-  pdl_trigger();
+  const int32_t r = x - v + (w ? warp_tot[w - 1] : 0);
+  if (total) *total = warp_tot[31];
+  __syncthreads();
+  return r;
 }
 
-// One warp per chunk: stable positions.  slot[s] = row of slot s in the
-// expert-sorted layout (or -1 for an invalid id).
-__global__ void __launch_bounds__(32) route_assign_kernel(const int64_t* __restrict__ ids, int64_t n, int E,
-                                                          const int32_t* __restrict__ base,
-                                                          int64_t* __restrict__ slot) {
-  __shared__ int32_t run[kMaxE];
-  const int lane = threadIdx.x;
-  for (int e = lane; e < E; e += 32) run[e] = base[static_cast<int64_t>(blockIdx.x) * E + e];
-  __syncwarp();
-  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kChunk;
-  for (int step = 0; step < kChunk / 32; ++step) {
-    const int64_t s = s0 + step * 32 + lane;
-    int key = E + lane;  // unique sentinel for lanes without a valid slot
-    if (s < n) {
+// shared memory of route_assign_kernel: counts [C][E] i32, run [E] i32,
+// per-warp counts [32][E] u16, 32 warp totals
+size_t route_assign_smem(int C, int E) {
+  return static_cast<size_t>(C) * E * 4 + static_cast<size_t>(E) * 4 + 32 * static_cast<size_t>(E) * 2 + 32 * 4;
+}
+
+__global__ void __launch_bounds__(kRouteThreads) route_assign_kernel(const int64_t* __restrict__ ids, int64_t n, int E,
+                                                                     int64_t chunk, int C,
+                                                                     const int32_t* __restrict__ cnt,
+                                                                     int64_t* __restrict__ slot,
+                                                                     int32_t* __restrict__ tot_out,
+                                                                     int32_t* __restrict__ off_out) {
+  pdl_wait();
+  extern __shared__ __align__(16) uint8_t rs[];
+  int32_t* cm = reinterpret_cast<int32_t*>(rs);
+  int32_t* run = cm + static_cast<int64_t>(C) * E;
+  uint16_t* wh = reinterpret_cast<uint16_t*>(run + E);
+  int32_t* wt = reinterpret_cast<int32_t*>(wh + 32 * E);
+  const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+  for (int i = tid; i < C * E; i += blockDim.x) cm[i] = cnt[i];
+  for (int i = tid; i < 32 * E; i += blockDim.x) wh[i] = 0;
+  __syncthreads();
+  // bases of this chunk (thread e owns expert e): off[e] = exclusive scan of
+  // the expert totals, plus the counts of the chunks before this one
+  int32_t tot = 0, pre = 0;
+  if (tid < E)
+    for (int c = 0; c < C; ++c) {
+      const int32_t v = cm[c * E + tid];
+      tot += v;
+      if (c < static_cast<int>(blockIdx.x)) pre += v;
+    }
+  const int32_t off = block_excl_scan(tid < E ? tot : 0, wt, nullptr);
+  if (tid < E) {
+    run[tid] = off + pre;
+    if (blockIdx.x == 0) {
+      if (tot_out) tot_out[tid] = tot;
+      if (off_out) off_out[tid] = off;
+    }
+  }
+  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t s1 = s0 + chunk < n ? s0 + chunk : n;
+  for (int64_t r0 = s0; r0 < s1; r0 += blockDim.x) {  // rounds of 1024 slots, in slot order
+    const int64_t s = r0 + tid;
+    int key = -1 - lane;  // unique per lane when the slot is absent or its id invalid
+    if (s < s1) {
       const int64_t e = ids[s];
       if (valid_id(e, E)) key = static_cast<int>(e);
     }
     const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const unsigned lt = (1u << lane) - 1u;
-    if (s < n) slot[s] = key < E ? static_cast<int64_t>(run[key] + __popc(peers & lt)) : -1;
-    __syncwarp();
-    if (key < E && (__ffs(peers) - 1) == lane) run[key] += __popc(peers);
-    __syncwarp();
+    const int below = __popc(peers & ((1u << lane) - 1u));  // same-expert slots earlier in my warp
+    if (key >= 0 && below == 0) wh[warp * E + key] = static_cast<uint16_t>(__popc(peers));
+    __syncthreads();
+    int32_t round_tot = 0;
+    if (tid < E) {  // per-warp counts -> exclusive offsets over the 32 warps
+#pragma unroll 8
+      for (int w = 0; w < 32; ++w) {
+        const int32_t v = wh[w * E + tid];
+        wh[w * E + tid] = static_cast<uint16_t>(round_tot);
+        round_tot += v;
+      }
+    }
+    __syncthreads();
+    if (key >= 0)
+      slot[s] = static_cast<int64_t>(run[key] + wh[warp * E + key] + below);
+    else if (s < s1)
+      slot[s] = -1;
+    __syncthreads();
+    if (tid < E) {
+      run[tid] += round_tot;
+      for (int w = 0; w < 32; ++w) wh[w * E + tid] = 0;
+    }
+    __syncthreads();
   }
+  pdl_trigger();
 }
 
-// xd[slot[s]] = x[s / k]   (one warp per slot, 16-byte vectors)
-__global__ void __launch_bounds__(256) gather_rows_kernel(const __nv_bfloat16* __restrict__ x,
-                                                          const int64_t* __restrict__ slot, int64_t n, int k,
-                                                          int64_t H, __nv_bfloat16* __restrict__ xd) {
+// shared memory of route_tiles_kernel: counts [C][E] i32 + 32 warp totals
+// Grouped-GEMM tile table from the chunk counts (one CTA): gtab[0] = tiles,
+// then (row0, row_end, expert) per tile_m-row tile, experts in order.
+__global__ void __launch_bounds__(kRouteThreads) route_tiles_kernel(const int32_t* __restrict__ cnt, int C, int E,
+                                                                    int tile_m, int32_t* __restrict__ gtab) {
+  pdl_wait();
+  __shared__ int32_t wt[32];
+  const int tid = threadIdx.x;
+  int32_t tot = 0;
+  if (tid < E)
+    for (int c = 0; c < C; ++c) tot += cnt[static_cast<int64_t>(c) * E + tid];
+  const int32_t tiles = tid < E ? (tot + tile_m - 1) / tile_m : 0;
+  const int32_t off = block_excl_scan(tid < E ? tot : 0, wt, nullptr);
+  int32_t n_tiles = 0;
+  const int32_t tbase = block_excl_scan(tiles, wt, &n_tiles);
+  if (tid == 0) gtab[0] = n_tiles;
+  if (tid < E) {
+    int32_t* g = gtab + 1 + 3 * tbase;
+    for (int32_t i = 0; i < tiles; ++i) {
+      g[3 * i] = off + i * tile_m;
+      g[3 * i + 1] = off + tot;
+      g[3 * i + 2] = tid;
+    }
+  }
+  pdl_trigger();
+}
+
+// xd[slot[t, j]] = x[t] for j < k: one warp per token, the row read once into
+// registers (8 x 16 B per lane per 4 KB) and written to its k expert-sorted rows
+__global__ void __launch_bounds__(256) gather_tokens_kernel(const __nv_bfloat16* __restrict__ x,
+                                                            const int64_t* __restrict__ slot, int64_t T, int k,
+                                                            int64_t H, __nv_bfloat16* __restrict__ xd) {
   pdl_wait();
   pdl_trigger();
-  const int64_t s = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
-  if (s >= n) return;
-  const int64_t d = slot[s];
-  if (d < 0) return;
-  const uint4* src = reinterpret_cast<const uint4*>(x + (s / k) * H);
-  uint4* dst = reinterpret_cast<uint4*>(xd + d * H);
-  for (int64_t i = lane; i < H / 8; i += 32) dst[i] = src[i];
+  if (t >= T) return;
+  const int64_t my_slot = lane < k ? slot[t * k + lane] : -1;
+  const uint4* src = reinterpret_cast<const uint4*>(x + t * H);
+  const int64_t nv = H / 8;
+  for (int64_t v0 = 0; v0 < nv; v0 += 8 * 32) {
+    uint4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t idx = v0 + i * 32 + lane;
+      if (idx < nv) v[i] = __ldcs(src + idx);
+    }
+    for (int j = 0; j < k; ++j) {
+      const int64_t d = __shfl_sync(0xffffffffu, my_slot, j);
+      if (d < 0) continue;
+      uint4* dst = reinterpret_cast<uint4*>(xd + d * H);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t idx = v0 + i * 32 + lane;
+        if (idx < nv) dst[idx] = v[i];
+      }
+    }
+  }
 }
 
 // y[t] = sum_j w[t,j] * yd[slot[t,j]]  (fp32, j ascending), one CTA per token
@@ -438,20 +499,33 @@ __global__ void tiles_from_counts_kernel(const int64_t* __restrict__ counts, int
 }
 
 // ---------------------------------------------------------------- host ops
-int64_t chunks_of(int64_t n) { return (n + kChunk - 1) / kChunk; }
 int64_t max_tiles(int64_t n, int E) { return n / moe_tile_m() + E + 1; }
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 int topk_param(const opf_op_ctx& c) { return static_cast<int>(ctx_param(c, "topk", 8)); }
 int experts_param(const opf_op_ctx& c) { return static_cast<int>(ctx_param(c, "experts", 128)); }
 
-// route: histogram + scan (+ tile table); returns the per-chunk bases in ws
-void route_plan(const int64_t* ids, int64_t n, int E, char* ws, int32_t* gtab, cudaStream_t s,
-                int32_t* tot = nullptr, int32_t* off = nullptr) {
-  auto* cnt = reinterpret_cast<int32_t*>(ws);
-  const int64_t C = chunks_of(n);
-  if (C > 0) launch_pdl(route_hist_kernel, dim3(static_cast<unsigned>(C)), dim3(256), 0, s, ids, n, E, cnt);
-  launch_pdl(route_scan_kernel, dim3(1), dim3(1024), 0, s, cnt, static_cast<int>(C), E, gtab, moe_tile_m(), tot, off);
+size_t cnt_bytes(int64_t n, int E) { return align256(static_cast<size_t>(route_chunks(n, E)) * E * 4); }
+
+// per-chunk expert histograms into ws (C x E i32)
+void route_hist(const int64_t* ids, int64_t n, int E, int32_t* cnt, cudaStream_t s) {
+  const int64_t C = route_chunks(n, E);
+  if (C > 0)
+    launch_pdl(route_hist_kernel, dim3(static_cast<unsigned>(C)), dim3(kRouteThreads), static_cast<size_t>(E) * 4, s,
+               ids, n, E, route_chunk(n, E), cnt);
+}
+// slot[s] = row of slot s in the expert-sorted layout (-1: invalid id); tot / off per expert (optional)
+void route_assign(const int64_t* ids, int64_t n, int E, const int32_t* cnt, int64_t* slot, cudaStream_t s,
+                  int32_t* tot = nullptr, int32_t* off = nullptr) {
+  const int C = static_cast<int>(route_chunks(n, E));
+  const size_t smem = route_assign_smem(C, E);
+  static std::once_flag once;
+  std::call_once(once, [] {
+    OPF_CUDA(cudaFuncSetAttribute(route_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(route_assign_smem(16, 1024))));
+  });
+  launch_pdl(route_assign_kernel, dim3(static_cast<unsigned>(std::max(C, 1))), dim3(kRouteThreads), smem, s, ids, n,
+             E, route_chunk(n, E), C, cnt, slot, tot, off);
 }
 
 opf_status op_moe_topk(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out, int32_t n_out,
@@ -484,12 +558,12 @@ opf_status op_moe_topk(const opf_op_ctx* c, const opf_view* in, int32_t n_in, op
 }
 
 size_t ws_dispatch(const opf_op_ctx& c, const opf_view*, int, const opf_view*, int, int64_t rows) {
-  return align256(static_cast<size_t>(chunks_of(rows * topk_param(c))) * experts_param(c) * 4) + 256;
+  return cnt_bytes(rows * topk_param(c), experts_param(c)) + 256;
 }
 size_t ws_grouped(const opf_op_ctx& c, const opf_view*, int, const opf_view*, int, int64_t rows) {
   const int64_t n = rows * topk_param(c);
-  return align256(static_cast<size_t>(chunks_of(n)) * experts_param(c) * 4) +
-         align256(static_cast<size_t>(1 + 3 * max_tiles(n, experts_param(c))) * 4) + 256;
+  return cnt_bytes(n, experts_param(c)) + align256(static_cast<size_t>(1 + 3 * max_tiles(n, experts_param(c))) * 4) +
+         256;
 }
 
 opf_status need_ws(const opf_op_ctx* c, size_t bytes, const char* who) {
@@ -513,12 +587,11 @@ opf_status op_moe_dispatch(const opf_op_ctx* c, const opf_view* in, int32_t n_in
   const int64_t n = rows * k;
   const int64_t* ids = vptr<int64_t>(in[1]);
   int64_t* slot = vptr<int64_t>(out[1]);
-  char* ws = static_cast<char*>(c->workspace);
-  route_plan(ids, n, E, ws, nullptr, s);
-  route_assign_kernel<<<static_cast<unsigned>(chunks_of(n)), 32, 0, s>>>(ids, n, E,
-                                                                          reinterpret_cast<int32_t*>(ws), slot);
-  launch_pdl(gather_rows_kernel, dim3(static_cast<unsigned>((n * 32 + 255) / 256)), dim3(256), 0, s,
-             static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[0])), static_cast<const int64_t*>(slot), n,
+  auto* cnt = static_cast<int32_t*>(c->workspace);
+  route_hist(ids, n, E, cnt, s);
+  route_assign(ids, n, E, cnt, slot, s);
+  launch_pdl(gather_tokens_kernel, dim3(static_cast<unsigned>((rows * 32 + 255) / 256)), dim3(256), 0, s,
+             static_cast<const __nv_bfloat16*>(vptr<__nv_bfloat16>(in[0])), static_cast<const int64_t*>(slot), rows,
              k, H, vptr<__nv_bfloat16>(out[0]));
   return launch_status("moe_dispatch");
 }
@@ -565,8 +638,11 @@ opf_status grouped(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_vi
   char* ws = static_cast<char*>(c->workspace);
   int32_t* gtab;
   if (ep == 1) {
-    gtab = reinterpret_cast<int32_t*>(ws + align256(static_cast<size_t>(chunks_of(n)) * E * 4));
-    route_plan(vptr<int64_t>(in[1]), n, E, ws, gtab, s);
+    auto* cnt = reinterpret_cast<int32_t*>(ws);
+    gtab = reinterpret_cast<int32_t*>(ws + cnt_bytes(n, E));
+    route_hist(vptr<int64_t>(in[1]), n, E, cnt, s);
+    launch_pdl(route_tiles_kernel, dim3(1), dim3(kRouteThreads), 0, s, static_cast<const int32_t*>(cnt),
+               static_cast<int>(route_chunks(n, E)), E, moe_tile_m(), gtab);
   } else {
     gtab = reinterpret_cast<int32_t*>(ws);
     launch_pdl(tiles_from_counts_kernel, dim3(1), dim3(32), 0, s, static_cast<const int64_t*>(vptr<int64_t>(in[1])),
@@ -617,8 +693,7 @@ opf_status ep_ctx(const opf_op_ctx* c, const char* who, EpCtx* x, std::initializ
 size_t ws_ep_dispatch(const opf_op_ctx& c, const opf_view*, int, const opf_view*, int, int64_t rows) {
   const int64_t n = rows * topk_param(c);
   const int E = experts_param(c);
-  return align256(static_cast<size_t>(chunks_of(n)) * E * 4) + align256(static_cast<size_t>(n) * 8) +
-         3 * align256(static_cast<size_t>(E) * 4) + 256;
+  return cnt_bytes(n, E) + align256(static_cast<size_t>(n) * 8) + 3 * align256(static_cast<size_t>(E) * 4) + 256;
 }
 
 opf_status op_moe_ep_dispatch(const opf_op_ctx* c, const opf_view* in, int32_t n_in, opf_view* out,
@@ -643,14 +718,14 @@ opf_status op_moe_ep_dispatch(const opf_op_ctx* c, const opf_view* in, int32_t n
   const int64_t n = rows * k;
   char* ws = static_cast<char*>(c->workspace);
   auto* cnt = reinterpret_cast<int32_t*>(ws);
-  auto* slot_local = reinterpret_cast<int64_t*>(ws + align256(static_cast<size_t>(chunks_of(n)) * E * 4));
+  auto* slot_local = reinterpret_cast<int64_t*>(ws + cnt_bytes(n, E));
   auto* tot = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(slot_local) + align256(static_cast<size_t>(n) * 8));
   auto* off = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(tot) + align256(static_cast<size_t>(E) * 4));
   auto* send_off = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(off) + align256(static_cast<size_t>(E) * 4));
   const int64_t* ids = vptr<int64_t>(in[1]);
   if (n > 0) {
-    route_plan(ids, n, E, ws, nullptr, s, tot, off);
-    route_assign_kernel<<<static_cast<unsigned>(chunks_of(n)), 32, 0, s>>>(ids, n, E, cnt, slot_local);
+    route_hist(ids, n, E, cnt, s);
+    route_assign(ids, n, E, cnt, slot_local, s, tot, off);
   } else {
     OPF_CUDA(cudaMemsetAsync(tot, 0, E * 4, s));
   }
