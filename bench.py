@@ -45,6 +45,9 @@ try:
 except Exception:  # noqa: BLE001
     TRAFFIC = {}
 
+# tcgen05 GEMM share of the prefill step's launch time (ncu launch list of the
+# replayed plan only, tools/replay_step.py: profiles/r02_launches_step_prefill4_summary.txt)
+GEMM_LAUNCH_SHARE = 0.929
 LLAMA = dict(hidden=4096, heads=32, kv_heads=8, head_dim=128, inter=14336)
 METRIC = "tokens/sec overlapped vs sequential schedule, Llama-3-8B layer TP=1/2/4/8"
 
@@ -382,6 +385,27 @@ def run_ours(args):
         comm_window_ok = enable_window_all(of, comm, 3 * args.tokens * LLAMA["hidden"] * 2, world)
     tp = world
     T, S, L = args.tokens, args.seq_len, args.layers
+    # ---- roofline of the dominant kernel (tcgen05 GEMM), per-rank shapes, timed
+    # alone BEFORE the timed legs: the same conditions as the burst peak it is
+    # divided by (MEASURED_PEAKS: cuBLAS best-of-10 on a cool GPU).  The in-step
+    # figure (power-capped, vs the sustained peak) is derived below from the
+    # step time and the GEMM share of the committed ncu launch list.
+    H, I = LLAMA["hidden"], LLAMA["inter"] // tp
+    nq, nkv, hd = LLAMA["heads"] // tp, LLAMA["kv_heads"] // tp, LLAMA["head_dim"]
+    shapes = {"qkv": (T, H, (nq + 2 * nkv) * hd), "o": (T, nq * hd, H), "gate_up": (T, H, 2 * I),
+              "down": (T, I, H)}
+    achieved, gemm_rows = gemm_roofline(of, torch, dev, shapes) if rank == 0 else (0.0, [])
+    traffic = None
+    if gemm_rows and all("ncu_dram_bytes" in r for r in gemm_rows):
+        traffic = round(sum(r["ncu_dram_bytes"] for r in gemm_rows) / len(gemm_rows))
+    tp8 = None
+    if rank == 0 and tp == 1:
+        # the north-star target config's per-rank shapes (TP=8), measured on this GPU
+        I8, nq8, nkv8 = LLAMA["inter"] // 8, LLAMA["heads"] // 8, LLAMA["kv_heads"] // 8
+        s8 = {"qkv": (T, H, (nq8 + 2 * nkv8) * hd), "o": (T, nq8 * hd, H), "gate_up": (T, H, 2 * I8),
+              "down": (T, I8, H)}
+        a8, r8 = gemm_roofline(of, torch, dev, s8)
+        tp8 = {"achieved": round(a8, 1), "frac": round(a8 / PEAKS["bf16_tflops"], 4), "per_gemm": r8}
     desc = of.llama_graph(layers=L, tokens=T, seq_len=S, tp=tp, dtype="bf16", **LLAMA)
     # TP: AllReduce / add_rmsnorm subgraphs for TokenWeave, and the row-parallel
     # o_proj / down MatMuls isolated so fuse_gemm can fold them into the collective
@@ -470,23 +494,6 @@ def run_ours(args):
     del sess_b
     e2e_val = tokens_job / (e2e_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (tcgen05 GEMM), per-rank shapes
-    H, I = LLAMA["hidden"], LLAMA["inter"] // tp
-    nq, nkv, hd = LLAMA["heads"] // tp, LLAMA["kv_heads"] // tp, LLAMA["head_dim"]
-    shapes = {"qkv": (T, H, (nq + 2 * nkv) * hd), "o": (T, nq * hd, H), "gate_up": (T, H, 2 * I),
-              "down": (T, I, H)}
-    achieved, gemm_rows = gemm_roofline(of, torch, dev, shapes) if rank == 0 else (0.0, [])
-    traffic = None
-    if gemm_rows and all("ncu_dram_bytes" in r for r in gemm_rows):
-        traffic = round(sum(r["ncu_dram_bytes"] for r in gemm_rows) / len(gemm_rows))
-    tp8 = None
-    if rank == 0 and tp == 1:
-        # the north-star target config's per-rank shapes (TP=8), measured on this GPU
-        I8, nq8, nkv8 = LLAMA["inter"] // 8, LLAMA["heads"] // 8, LLAMA["kv_heads"] // 8
-        s8 = {"qkv": (T, H, (nq8 + 2 * nkv8) * hd), "o": (T, nq8 * hd, H), "gate_up": (T, H, 2 * I8),
-              "down": (T, I8, H)}
-        a8, r8 = gemm_roofline(of, torch, dev, s8)
-        tp8 = {"achieved": round(a8, 1), "frac": round(a8 / PEAKS["bf16_tflops"], 4), "per_gemm": r8}
     flops_layer = sum(2.0 * m * k * n for (m, k, n) in shapes.values())
     line = None
     decode = None
@@ -531,7 +538,8 @@ def run_ours(args):
                          "achieved": round(achieved, 1),
                          "peak": PEAKS["bf16_tflops"], "unit": "TFLOP/s",
                          "frac": round(achieved / PEAKS["bf16_tflops"], 4),
-                         "peak_source": PEAK_SRC + " burst (kernel timed alone)",
+                         "peak_source": PEAK_SRC + " burst (kernel timed alone, before the timed legs: "
+                                        "8 launches back to back in one CUDA graph, rotated inputs > L2)",
                          "frac_of_sustained": round(achieved / PEAKS["bf16_tflops_sustained"], 4),
                          "traffic": traffic,
                          "traffic_note": "mean ncu dram read+write bytes per GEMM launch over the 4 "
@@ -540,7 +548,15 @@ def run_ours(args):
                          "per_gemm": gemm_rows, "tp8_shapes": tp8,
                          "algorithmic_flops_per_layer": flops_layer,
                          "gemm_share_of_step_at_roofline": round(
-                             flops_layer * L / (PEAKS["bf16_tflops"] * 1e12) * 1e3 / best_ms, 4)},
+                             flops_layer * L / (PEAKS["bf16_tflops"] * 1e12) * 1e3 / best_ms, 4),
+                         "in_step": {
+                             "achieved": round(flops_layer * L / (GEMM_LAUNCH_SHARE * best_ms / 1e3) / 1e12, 1),
+                             "peak": PEAKS["bf16_tflops_sustained"],
+                             "frac": round(flops_layer * L / (GEMM_LAUNCH_SHARE * best_ms / 1e3) / 1e12
+                                           / PEAKS["bf16_tflops_sustained"], 4),
+                             "how": f"GEMM FLOPs per step / (GEMM share {GEMM_LAUNCH_SHARE} of the ncu launch "
+                                    "list profiles/r02_launches_prefill4_summary.txt x ms_per_step), vs the "
+                                    "sustained (power-capped) peak"}},
             "cpu_baseline": cpu,
             "decode": decode,
             "moe": moe,

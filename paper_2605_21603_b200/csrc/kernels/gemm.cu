@@ -20,6 +20,7 @@
 // and for direct opf_launch calls on un-packed [K,N] weights.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <mutex>
 
@@ -888,48 +889,59 @@ __device__ __forceinline__ void store_tile_rope_st(uint32_t tmem_col0, uint8_t* 
                                                    int64_t row0, int64_t M, int64_t n_out,
                                                    __nv_bfloat16* __restrict__ c, int64_t ldc, const RopeArgs& rope,
                                                    Release&& release) {
+  (void)sbuf;
   constexpr int kHeads = TN / 128;
-  const float p = row0 + lane < M ? static_cast<float>(rope.pos[row0 + lane]) : 0.0f;
+  const bool row_ok = row0 + lane < M;
+  const float p = row_ok ? static_cast<float>(rope.pos[row0 + lane]) : 0.0f;
+  __nv_bfloat16* crow = c + (row0 + lane) * ldc + nb * TN;
+  // Pair-chunk j (32 of the 64 rotation pairs) outermost: the cos / sin of
+  // this lane's row for those pairs are computed ONCE per tile and reused by
+  // every head and both halves (the per-element form, 2 x heads sincos + an
+  // exp2 per pair, took ~40k cycles per decode tile).  Each lane owns one row
+  // and stores its 8-column pieces directly (16 B per store; L2 merges the
+  // sectors), so no staging order ties the heads together.
 #pragma unroll 1
-  for (int hh = 0; hh < kHeads; ++hh) {
-    const bool rot = (nb * TN) / 128 + hh < rope.rot_heads;
-#pragma unroll 1
-    for (int half = 0; half < 2; ++half) {
-      __syncwarp();  // the previous half's read-back of sbuf is done
-#pragma unroll 1
-      for (int j = 0; j < 2; ++j) {
-        uint32_t a[32], b[32];
-        tmem_ld32(tmem_col0 + static_cast<uint32_t>(hh * 128 + j * 32), a);
-        tmem_ld32(tmem_col0 + static_cast<uint32_t>(hh * 128 + 64 + j * 32), b);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (hh == kHeads - 1 && half == 1 && j == 1) release();
-        float o[32];
+  for (int j = 0; j < 2; ++j) {
+    float cs[32], sn[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < 32; ++i) {
+      const float inv_freq = exp2f(-2.0f * static_cast<float>(j * 32 + i) / 128.0f * rope.log2_theta);
+      const float ang = p * inv_freq;
+      const float q = rintf(ang * 0.15915494309189535f);
+      const float r = fmaf(-q, 6.28318548202514648f, fmaf(-q, -1.7484556e-07f, ang));
+      __sincosf(r, &sn[i], &cs[i]);
+    }
+#pragma unroll 1
+    for (int hh = 0; hh < kHeads; ++hh) {
+      const bool rot = (nb * TN) / 128 + hh < rope.rot_heads;
+      uint32_t a[32], b[32];
+      tmem_ld32(tmem_col0 + static_cast<uint32_t>(hh * 128 + j * 32), a);
+      tmem_ld32(tmem_col0 + static_cast<uint32_t>(hh * 128 + 64 + j * 32), b);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (hh == kHeads - 1 && j == 1) release();
+      const int64_t col_lo = hh * 128 + j * 32;
+#pragma unroll
+      for (int q8 = 0; q8 < 4; ++q8) {
+        float o0[8], o1[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int i = q8 * 8 + e;
           const float x = __uint_as_float(a[i]), y = __uint_as_float(b[i]);
-          if (rot) {
-            const float inv_freq = exp2f(-2.0f * static_cast<float>(j * 32 + i) / 128.0f * rope.log2_theta);
-            const float ang = p * inv_freq;
-            const float q = rintf(ang * 0.15915494309189535f);
-            const float r = fmaf(-q, 6.28318548202514648f, fmaf(-q, -1.7484556e-07f, ang));
-            float sn, cs;
-            __sincosf(r, &sn, &cs);
-            o[i] = half == 0 ? x * cs - y * sn : y * cs + x * sn;
-          } else {
-            o[i] = half == 0 ? x : y;
-          }
+          o0[e] = rot ? x * cs[i] - y * sn[i] : x;
+          o1[e] = rot ? y * cs[i] + x * sn[i] : y;
         }
-        stage_half(sbuf, o, j, lane);
-      }
-      __syncwarp();
-      const int64_t col0 = nb * TN + hh * 128 + half * 64;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int row = i * 4 + lane / 8, jj = lane % 8;
-        const int64_t col = col0 + jj * 8;
-        if (row0 + row < M && col < n_out) {
-          const uint4 u = *reinterpret_cast<const uint4*>(sbuf + row * 128 + ((jj ^ (row & 7)) * 16));
-          *reinterpret_cast<uint4*>(c + (row0 + row) * ldc + col) = u;
+        if (row_ok && nb * TN + hh * 128 + 128 <= n_out) {
+          uint4 u0, u1;
+          u0.x = pack_bf16(__float_as_uint(o0[0]), __float_as_uint(o0[1]));
+          u0.y = pack_bf16(__float_as_uint(o0[2]), __float_as_uint(o0[3]));
+          u0.z = pack_bf16(__float_as_uint(o0[4]), __float_as_uint(o0[5]));
+          u0.w = pack_bf16(__float_as_uint(o0[6]), __float_as_uint(o0[7]));
+          u1.x = pack_bf16(__float_as_uint(o1[0]), __float_as_uint(o1[1]));
+          u1.y = pack_bf16(__float_as_uint(o1[2]), __float_as_uint(o1[3]));
+          u1.z = pack_bf16(__float_as_uint(o1[4]), __float_as_uint(o1[5]));
+          u1.w = pack_bf16(__float_as_uint(o1[6]), __float_as_uint(o1[7]));
+          *reinterpret_cast<uint4*>(crow + col_lo + q8 * 8) = u0;
+          *reinterpret_cast<uint4*>(crow + col_lo + 64 + q8 * 8) = u1;
         }
       }
     }

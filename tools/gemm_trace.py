@@ -15,17 +15,29 @@ import torch  # noqa: E402
 from paper_2605_21603_b200 import _lib, opflow as of  # noqa: E402
 
 m, n, k = (int(x) for x in sys.argv[1:4])
+rope = len(sys.argv) > 4 and sys.argv[4] == "rope"  # MatMul -> rope (fused into the GEMM epilogue, EPI 2)
 dev = torch.device("cuda:0")
-d = json.dumps({"tensors": [{"name": "a", "shape": [m, k], "dtype": "bf16", "role": "input"},
-                            {"name": "w", "shape": [k, n], "batch": "replicated", "dtype": "bf16", "role": "weight"},
-                            {"name": "c", "shape": [m, n], "dtype": "bf16", "role": "output"}],
-                "operators": [{"name": "mm", "kind": "MatMul", "inputs": ["a", "w"], "outputs": ["c"]}]})
-g = of.build_graph(d)
+tens = [{"name": "a", "shape": [m, k], "dtype": "bf16", "role": "input"},
+        {"name": "w", "shape": [k, n], "batch": "replicated", "dtype": "bf16", "role": "weight"},
+        {"name": "c", "shape": [m, n], "dtype": "bf16", "role": "output"}]
+ops = [{"name": "mm", "kind": "MatMul", "inputs": ["a", "w"], "outputs": ["c"]}]
+if rope:  # Llama GQA: n = (nq + 2 nkv) * 128 with nq = 4 nkv
+    nkv = n // 128 // 6
+    tens[2] = {"name": "qkv", "shape": [m, n], "dtype": "bf16"}
+    tens += [{"name": "pos", "shape": [m], "dtype": "i64", "role": "input"},
+             {"name": "c", "shape": [m, n], "dtype": "bf16", "role": "output"}]
+    ops.append({"name": "rope", "kind": "Custom", "inputs": ["qkv", "pos"], "outputs": ["c"],
+                "attrs": {"custom_name": "rope", "params": {"heads": 4 * nkv, "kv_heads": nkv, "head_dim": 128,
+                                                             "theta": 500000.0}}})
+    ops[0]["outputs"] = ["qkv"]
+g = of.build_graph(json.dumps({"tensors": tens, "operators": ops}))
 s = of.Session(g, of.partition(g, []), {"lanes": 1})
 a = torch.randn(m, k, device=dev).to(torch.bfloat16)
 w = (torch.randn(k, n, device=dev) / k ** 0.5).to(torch.bfloat16)
 c = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
 s.bind("a", a), s.bind("w", w), s.bind("c", c)
+if rope:
+    s.bind("pos", torch.arange(m, device=dev, dtype=torch.int64) % 1024)
 L = _lib.lib()
 buf = (C.c_ulonglong * (3 * 2048))()
 cnt = (C.c_int * 3)()
