@@ -677,8 +677,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
   pdl_trigger();
-  int pp_k = 0, pp_s[2] = {0, 0}, pp_pv[2] = {0, 0}, pp_sm = 0;  // trace indices (FA_TRACE builds)
-  (void)pp_k, (void)pp_s, (void)pp_pv, (void)pp_sm;
+  int pp_k = 0, pp_s[2] = {0, 0}, pp_pv[2] = {0, 0}, pp_sm = 0, pp_ep = 0;  // trace indices (FA_TRACE builds)
+  (void)pp_k, (void)pp_s, (void)pp_pv, (void)pp_sm, (void)pp_ep;
 
   // Item order of this CTA: passes of gridDim.x items, longest first, walked
   // boustrophedon (even passes CTA c takes item c, odd passes item G-1-c), so
@@ -712,6 +712,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         const int row0 = seq * S;
         bar_wait(q_empty, qph ^ 1);
         qph ^= 1;
+        FA_T(1, static_cast<int>(kk));
         bar_expect(q_full, 2 * kTile);
         for (int t = 0; t < 2; ++t) {
           tma2d(su32(sm + kPPQ + t * kTile), &mqkv, q_full, (h0 + t) * HD, row0 + qt * BQ);
@@ -794,6 +795,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         const int n = qt + 1;
         bar_wait(q_full, qph);
         qph ^= 1;
+        FA_T(10, static_cast<int>(kk));
         bar_wait(&k_full[kst], kph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         issue_s(0);
@@ -877,6 +879,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) bar_arrive(&o_free[t]);
+      if (lane == 0 && warp == 4) FA_T(11, pp_ep++);
     };
     for (int64_t kk = 0, it = snake_item(0); it < n_items; it = snake_item(++kk)) {
       int qt, hp, seq;

@@ -16,7 +16,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     import bench
     from paper_2605_21603_b200 import opflow as of
     bench.ROUNDS, bench.SOAK_S = 3, 1.0
-    p = argparse.Namespace(layers=int(os.environ["AB_LAYERS"]), decode_batch=512, decode_ctx=4096, steps=5,
+    p = argparse.Namespace(layers=int(os.environ["AB_LAYERS"]), decode_batch=int(os.environ.get("AB_BATCH", 512)),
+                           decode_ctx=int(os.environ.get("AB_CTX", 4096)), steps=5,
                            warmup=3, rounds=3, soak=1.0,
                            sm_sweep=[int(x) for x in os.environ.get("AB_SMS", "").split()] or [])
     dev = torch.device("cuda:0")

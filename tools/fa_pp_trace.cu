@@ -53,5 +53,8 @@ int main(int argc, char** argv) {
     for (int e : ev) printf(" %10lld", t[e][j] - t0);
     printf("\n");
   }
+  // item boundaries: Q load issued (producer), Q landed at the MMA warp, head-0 epilogue done
+  printf("%4s %10s %10s %10s\n", "item", "Q issued", "Q at MMA", "epi0 done");
+  for (int j = 0; j < 8; ++j) printf("%4d %10lld %10lld %10lld\n", j, t[1][j] - t0, t[10][j] - t0, t[11][j] - t0);
   return 0;
 }
