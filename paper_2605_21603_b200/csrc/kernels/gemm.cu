@@ -184,6 +184,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 
+// SiLU(g) * u with the fast reciprocal (MUFU.RCP + FMUL; <= 2 ulp): the IEEE
+// division is a ~15-instruction FCHK / Newton sequence per element, issued by
+// the epilogue warps beside the producer and MMA warps of the same SM.
+// g -> -inf: exp(-g) = inf and __fdividef returns 0, the SiLU limit.
+__device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
+
 __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
   return *reinterpret_cast<const uint32_t*>(&v);
@@ -248,8 +254,8 @@ __device__ __forceinline__ void store_tile(const CUtensorMap* map_c, uint32_t tm
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const float g0 = __uint_as_float(v0[i]), g1 = __uint_as_float(v1[i]);
-        v0[i] = __float_as_uint(g0 / (1.0f + __expf(-g0)) * __uint_as_float(u0[i]));
-        v1[i] = __float_as_uint(g1 / (1.0f + __expf(-g1)) * __uint_as_float(u1[i]));
+        v0[i] = __float_as_uint(silu_mul(g0, __uint_as_float(u0[i])));
+        v1[i] = __float_as_uint(silu_mul(g1, __uint_as_float(u1[i])));
       }
     } else {
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -324,8 +330,8 @@ __device__ __forceinline__ void store_tile_direct(uint32_t tmem_col0, __nv_bfloa
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const float g0 = __uint_as_float(v0[i]), g1 = __uint_as_float(v1[i]);
-        v0[i] = __float_as_uint(g0 / (1.0f + __expf(-g0)) * __uint_as_float(u0[i]));
-        v1[i] = __float_as_uint(g1 / (1.0f + __expf(-g1)) * __uint_as_float(u1[i]));
+        v0[i] = __float_as_uint(silu_mul(g0, __uint_as_float(u0[i])));
+        v1[i] = __float_as_uint(silu_mul(g1, __uint_as_float(u1[i])));
       }
     } else {
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -678,7 +684,7 @@ __device__ __forceinline__ void store_tile_splitk(const CUtensorMap* map_c, uint
       splitk_sum_piece(g, regions, split_stride, S, h, lane);
       splitk_sum_piece(u, regions, split_stride, S, 2 + h, lane);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) g[i] = g[i] / (1.0f + __expf(-g[i])) * u[i];
+      for (int i = 0; i < 32; ++i) g[i] = silu_mul(g[i], u[i]);
       stage_half(sbuf, g, h, lane);
     }
     stage_commit(map_c, sbuf, buf, lane, nb * 128 + half * 64, row0, M);
@@ -821,8 +827,8 @@ __device__ __forceinline__ void store_tile_st(uint32_t tmem_col0, uint8_t* sbuf,
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const float g0 = __uint_as_float(v0[i]), g1 = __uint_as_float(v1[i]);
-        v0[i] = __float_as_uint(g0 / (1.0f + __expf(-g0)) * __uint_as_float(u0[i]));
-        v1[i] = __float_as_uint(g1 / (1.0f + __expf(-g1)) * __uint_as_float(u1[i]));
+        v0[i] = __float_as_uint(silu_mul(g0, __uint_as_float(u0[i])));
+        v1[i] = __float_as_uint(silu_mul(g1, __uint_as_float(u1[i])));
       }
     } else {
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
