@@ -68,8 +68,13 @@ __device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
                : "memory");
 }
+// Every arrive in this file hands TMEM (S, P or O) to the other side and
+// follows tcgen05.wait + tcgen05.fence::before_thread_sync, which order the
+// tensor-memory accesses; no generic-memory data rides on these barriers, so
+// the arrive is relaxed (no drain of the thread's in-flight global stores;
+// measured neutral here, unlike the GEMM epilogue's hand-back).
 __device__ __forceinline__ void bar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
 __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
@@ -861,19 +866,23 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const float inv = d.l > 0.0f ? 1.0f / d.l : 0.0f;
       __nv_bfloat16* op = out + (d.row0 + r) * (static_cast<int64_t>(nq) * HD) + static_cast<int64_t>(d.head) * HD;
+      // 32-byte stores (one sector per lane per instruction): half the
+      // scattered store wavefronts of 16-byte pieces — this warp's 32 rows are
+      // 8 KB apart, and the epilogue's store traffic shares the L1 / shared
+      // memory pipeline the MMAs read their operands through
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float o[32];
         tld32(orow + c * 32, o);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          uint4 u;
-          u.x = bf2(o[v * 8 + 0] * inv, o[v * 8 + 1] * inv);
-          u.y = bf2(o[v * 8 + 2] * inv, o[v * 8 + 3] * inv);
-          u.z = bf2(o[v * 8 + 4] * inv, o[v * 8 + 5] * inv);
-          u.w = bf2(o[v * 8 + 6] * inv, o[v * 8 + 7] * inv);
-          *reinterpret_cast<uint4*>(op + c * 32 + v * 8) = u;
+        for (int v = 0; v < 2; ++v) {
+          uint32_t w[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) w[e] = bf2(o[v * 16 + 2 * e] * inv, o[v * 16 + 2 * e + 1] * inv);
+          asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(op + c * 32 + v * 16),
+                       "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                       : "memory");
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
