@@ -1019,7 +1019,22 @@ bool prefill_bf16_tcgen05(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t 
   // with setmaxnreg, whole S row per thread) for even groups — measured 111 vs
   // 126 us at 8 x 1024 tokens, 32 / 8 heads (620 vs 547 TFLOP/s); odd groups
   // take the one-head kernel with two softmax column parts per row.
-  const bool pp = (nq / nkv) % 2 == 0;
+  static const int fa_mode = [] {  // OPF_FA=one|pair forces a kernel (A/B runs)
+    const char* e = std::getenv("OPF_FA");
+    if (e && std::string(e) == "one") return 1;
+    if (e && std::string(e) == "pair") return 2;
+    return 0;
+  }();
+  bool pp = (nq / nkv) % 2 == 0;
+  if (fa_mode == 1) pp = false;
+  // Fewer head-pair items than SMs (e.g. the TP=8 per-rank shape, 4 q heads:
+  // 128 items of up to 8 key tiles on 148 SMs) leaves SMs idle behind the
+  // longest item; one head per item doubles the items.  Measured per rank at
+  // 8 x 1024 tokens (tools/attn_tp8.py): TP=8 25.5 -> 21.9 us; TP=4 (256 pair
+  // items) stays on the pair kernel (29.3 vs 37.1 us).
+  const int64_t pair_items = static_cast<int64_t>(S / BQ) * (nq / 2) * (rows / S);
+  const int sm_grid = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
+  if (fa_mode == 0 && pp && pair_items < sm_grid) pp = false;
   const int64_t W = static_cast<int64_t>(nq + 2 * nkv) * HD;
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(rows)};
