@@ -367,6 +367,56 @@ def gemm_roofline(of, torch, dev, shapes, reps=8):
     return achieved, rows
 
 
+def attention_tp8(of, torch, dev):
+    """The two attention kernels at the TP=8 per-rank shapes (4 q / 1 kv heads):
+    causal prefill over 8 x 1024 tokens and paged decode over 512 x 4K, timed
+    alone (20 / 10 back-to-back launches, CUDA events)."""
+    hd, page, nq, nkv = LLAMA["head_dim"], 16, LLAMA["heads"] // 8, LLAMA["kv_heads"] // 8
+
+    def timed(fn, n):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n
+
+    S, seqs = 1024, 8
+    t = (torch.rand(S * seqs, (nq + 2 * nkv) * hd, device=dev) * 2 - 1).to(torch.bfloat16)
+    o = torch.empty(S * seqs, nq * hd, dtype=torch.bfloat16, device=dev)
+    op = {"name": "a", "kind": "Custom", "inputs": [], "outputs": [],
+          "attrs": {"custom_name": "attn_prefill", "params": {"heads": nq, "kv_heads": nkv, "head_dim": hd,
+                                                               "seq_len": S}}}
+    ms = timed(lambda: of.launch(op, [t], [o], S * seqs), 20)
+    fl = 4 * (S * (S + 1) / 2) * hd * nq * seqs
+    res = {"prefill": {"shape": f"{seqs}x{S} tokens, {nq} q / {nkv} kv heads, causal", "us": round(ms * 1e3, 1),
+                       "tflops": round(fl / ms / 1e9, 1), "frac": round(fl / ms / 1e9 / PEAKS["bf16_tflops"], 4)}}
+    B, ctx = 512, 4096
+    pages = B * ctx // page
+    g = torch.Generator(device=dev).manual_seed(3)
+    kc = torch.rand(pages, nkv, page, hd, device=dev, generator=g).to(torch.bfloat16)
+    vc = torch.rand(pages, nkv, page, hd, device=dev, generator=g).to(torch.bfloat16)
+    table = torch.randperm(pages, device=dev, generator=g).view(B, -1)
+    pos = torch.full((B,), ctx - 1, dtype=torch.int64, device=dev)
+    qkv = torch.randn(B, (nq + 2 * nkv) * hd, device=dev).to(torch.bfloat16)
+    o2 = torch.empty(B, nq * hd, device=dev, dtype=torch.bfloat16)
+    dop = {"name": "d", "kind": "Custom", "inputs": [], "outputs": [],
+           "attrs": {"custom_name": "attn_decode", "params": {"heads": nq, "kv_heads": nkv, "head_dim": hd,
+                                                              "page_size": page, "kv_layout": 1}}}
+    ms = timed(lambda: of.launch(dop, [qkv, kc, vc, table, pos], [o2], B), 10)
+    kvb = 2.0 * B * ctx * nkv * hd * 2
+    res["decode"] = {"shape": f"{B} seqs x {ctx} context, {nq} q / {nkv} kv heads, paged HND",
+                     "us": round(ms * 1e3, 1), "gbs": round(kvb / ms / 1e6, 1),
+                     "frac_of_read_peak": round(kvb / ms / 1e6 / 7443.2, 4)}
+    del kc, vc, t
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -405,7 +455,8 @@ def run_ours(args):
         s8 = {"qkv": (T, H, (nq8 + 2 * nkv8) * hd), "o": (T, nq8 * hd, H), "gate_up": (T, H, 2 * I8),
               "down": (T, I8, H)}
         a8, r8 = gemm_roofline(of, torch, dev, s8)
-        tp8 = {"achieved": round(a8, 1), "frac": round(a8 / PEAKS["bf16_tflops"], 4), "per_gemm": r8}
+        tp8 = {"achieved": round(a8, 1), "frac": round(a8 / PEAKS["bf16_tflops"], 4), "per_gemm": r8,
+               "attention": attention_tp8(of, torch, dev)}
     desc = of.llama_graph(layers=L, tokens=T, seq_len=S, tp=tp, dtype="bf16", **LLAMA)
     # TP: AllReduce / add_rmsnorm subgraphs for TokenWeave, and the row-parallel
     # o_proj / down MatMuls isolated so fuse_gemm can fold them into the collective

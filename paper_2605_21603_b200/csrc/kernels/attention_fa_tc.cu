@@ -860,6 +860,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       float l;
     } prev{0, 0, 0.0f};
     bool pending = false;
+    const bool out32 = (reinterpret_cast<uintptr_t>(out) & 31) == 0;  // rows are 256 B multiples
     auto epilogue = [&](const Done& d) {
       bar_wait(&o_full[t], oph);
       oph ^= 1;
@@ -880,9 +881,14 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           uint32_t w[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) w[e] = bf2(o[v * 16 + 2 * e] * inv, o[v * 16 + 2 * e + 1] * inv);
-          asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(op + c * 32 + v * 16),
-                       "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
-                       : "memory");
+          if (out32) {
+            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(op + c * 32 + v * 16),
+                         "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                         : "memory");
+          } else {  // output base only 16-byte aligned (a caller-owned view)
+            reinterpret_cast<uint4*>(op + c * 32 + v * 16)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            reinterpret_cast<uint4*>(op + c * 32 + v * 16)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
