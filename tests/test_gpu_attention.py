@@ -38,13 +38,15 @@ def test_decode_variants(cuda, nq, nkv, impl):
         assert rel_err(got[b], want[b]) < 1e-2, (b, ctx[b], rel_err(got[b], want[b]))
 
 
-def _prefill(t, nq, nkv, S, rows, **extra):
+def _prefill(t, nq, nkv, S, rows, max_ctas=0, offset=0, **extra):
     import torch
     op = {"name": "a", "kind": "Custom", "inputs": [], "outputs": [],
           "attrs": {"custom_name": "attn_prefill",
                     "params": dict({"heads": nq, "kv_heads": nkv, "head_dim": 128, "seq_len": S}, **extra)}}
-    out = torch.empty(rows, nq * 128, dtype=torch.bfloat16, device="cuda")
-    of.launch(op, [t], [out], rows)
+    # offset > 0: the output is a view `offset` elements into a larger buffer
+    buf = torch.empty(rows * nq * 128 + offset, dtype=torch.bfloat16, device="cuda")
+    out = buf[offset:].view(rows, nq * 128)
+    of.launch(op, [t], [out], rows, max_ctas=max_ctas)
     torch.cuda.synchronize()
     return out.float().cpu().numpy()
 
@@ -72,6 +74,13 @@ def test_prefill_tcgen05_vs_oracle(cuda, S, nq, nkv, seqs, ramp):
     assert np.isfinite(got).all()
     assert rel_err(got, want) < 1e-2
     assert rel_err(fa2, want) < 1e-2
+    # a 7-CTA budget: more head-pair items than CTAs, so even GQA groups take
+    # the two-head kernel (few items per SM pick one head per item), every CTA
+    # walking several items; and a 16-byte (not 32-byte) aligned output view
+    for got2 in (_prefill(t, nq, nkv, S, rows, max_ctas=7), _prefill(t, nq, nkv, S, rows, max_ctas=7, offset=8)):
+        assert rel_err(got2, want) < 1e-2
+        row_err2 = np.abs(got2 - want).max(axis=1) / (np.abs(want).max(axis=1) + 1e-6)
+        assert row_err2.max() < 5e-2, int(row_err2.argmax())
     # per-row check too (a wrong tile hides in a normwise error)
     row_err = np.abs(got - want).max(axis=1) / (np.abs(want).max(axis=1) + 1e-6)
     assert row_err.max() < 5e-2, int(row_err.argmax())
