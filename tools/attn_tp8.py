@@ -10,6 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_2605_21603_b200 import opflow as of  # noqa: E402
+import bench  # noqa: E402
 
 dev = torch.device("cuda:0")
 hd, page = 128, 16
@@ -41,7 +42,7 @@ for tp in [int(x) for x in os.environ.get("TPS", "1 8").split()]:
     ms = timed(lambda: of.launch(op, [t], [out], rows))
     fl = 4 * (S * (S + 1) / 2) * hd * nq * seqs
     res[f"prefill_tp{tp}"] = {"us": round(ms * 1e3, 1), "tflops": round(fl / ms / 1e9, 1)}
-    B, ctx = 512, 4096
+    B, ctx = int(os.environ.get("DEC_B", 512)), 4096
     pages = B * ctx // page
     g = torch.Generator(device=dev).manual_seed(3)
     kc = torch.rand(pages, nkv, page, hd, device=dev, generator=g).to(torch.bfloat16)
@@ -53,7 +54,11 @@ for tp in [int(x) for x in os.environ.get("TPS", "1 8").split()]:
     dop = {"name": "d", "kind": "Custom", "inputs": [], "outputs": [],
            "attrs": {"custom_name": "attn_decode",
                      "params": {"heads": nq, "kv_heads": nkv, "head_dim": hd, "page_size": page, "kv_layout": 1}}}
-    ms = timed(lambda: of.launch(dop, [qkv, kc, vc, table, pos], [o2], B), 10)
+    dop.update(inputs=["qkv", "k_cache", "v_cache", "block_table", "positions"], outputs=["out"])
+    ms = bench.graph_reps_ms(of, torch, dev, torch.cuda.current_stream(dev),
+                             [("qkv", qkv, "input"), ("k_cache", kc, "weight"), ("v_cache", vc, "weight"),
+                              ("block_table", table, "input"), ("positions", pos, "input"), ("out", o2, "output")],
+                             dop, shared=("k_cache", "v_cache", "block_table", "positions"), reps=4)
     kvb = 2.0 * B * ctx * nkv * hd * 2
     res[f"decode_tp{tp}"] = {"us": round(ms * 1e3, 1), "gbs": round(kvb / ms / 1e6, 1)}
     del kc, vc
