@@ -294,7 +294,7 @@ def with_auto(cands, world):
     return dict(cands, dynaflow_auto=auto_spec(cands))
 
 
-def graph_reps_ms(of, torch, dev, stream, tensors, op, shared, reps):
+def graph_reps_ms(of, torch, dev, stream, tensors, op, shared, reps, best_of=0):
     """Device time of ONE op, measured as `reps` copies of it back to back in
     one CUDA graph (a one-lane sequential Session), CUDA events on `stream`
     around the replay: no host gap between launches (a per-launch Session.run
@@ -328,7 +328,7 @@ def graph_reps_ms(of, torch, dev, stream, tensors, op, shared, reps):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     times = []
-    for _ in range(3):
+    for _ in range(best_of or 3):
         e0.record(stream)
         sess.run(None, stream)
         e1.record(stream)
@@ -336,7 +336,9 @@ def graph_reps_ms(of, torch, dev, stream, tensors, op, shared, reps):
         times.append(e0.elapsed_time(e1) / reps)
     del sess, keep
     torch.cuda.empty_cache()
-    return sorted(times)[1]
+    # best_of: the fastest replay, the statistic of the burst peak it is divided
+    # by (MEASURED_PEAKS: cuBLAS best-of-10); otherwise the median of 3
+    return min(times) if best_of else sorted(times)[1]
 
 
 def gemm_roofline(of, torch, dev, shapes, reps=8):
@@ -352,7 +354,7 @@ def gemm_roofline(of, torch, dev, shapes, reps=8):
         c = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
         op = {"name": "mm", "kind": "MatMul", "inputs": ["a", "w"], "outputs": ["c"]}
         ms = graph_reps_ms(of, torch, dev, stream, [("a", a, "input"), ("w", w, "weight"), ("c", c, "output")],
-                           op, shared=(), reps=reps)
+                           op, shared=(), reps=reps, best_of=10)
         del a, w, c
         fl = 2.0 * m * n * k
         tot_flops += fl
@@ -595,7 +597,8 @@ def run_ours(args):
                          "peak": PEAKS["bf16_tflops"], "unit": "TFLOP/s",
                          "frac": round(achieved / PEAKS["bf16_tflops"], 4),
                          "peak_source": PEAK_SRC + " burst (kernel timed alone, before the timed legs: "
-                                        "8 launches back to back in one CUDA graph, rotated inputs > L2)",
+                                        "8 launches back to back in one CUDA graph, rotated inputs > L2; best of 10 "
+                                        "replays, like the cuBLAS best-of-10 peak)",
                          "frac_of_sustained": round(achieved / PEAKS["bf16_tflops_sustained"], 4),
                          "traffic": traffic,
                          "traffic_note": "mean ncu dram read+write bytes per GEMM launch over the 4 "
