@@ -234,6 +234,7 @@ def time_steps(torch, fn, steps, warmup, stream, world):
 
 
 ROUNDS, SOAK_S = 3, 2.0
+COOLDOWN_S = 2.0  # idle time before each roofline GEMM (burst conditions)
 
 
 def time_candidates(torch, sess, cands, steps, warmup, stream, world, rounds=None, soak_s=None):
@@ -349,6 +350,10 @@ def gemm_roofline(of, torch, dev, shapes, reps=8):
     tot_flops, tot_ms, rows = 0.0, 0.0, []
     stream = torch.cuda.current_stream(dev)
     for name, (m, k, n) in shapes.items():
+        # a few idle seconds first: the previous shape's dense load leaves the
+        # GPU power-capped (clocks down ~25%), which the cool burst peak is not
+        torch.cuda.synchronize()
+        time.sleep(COOLDOWN_S)
         a = torch.randn(m, k, device=dev, dtype=torch.bfloat16)
         w = (torch.randn(k, n, device=dev, dtype=torch.bfloat16) / k ** 0.5).to(torch.bfloat16)
         c = torch.empty(m, n, device=dev, dtype=torch.bfloat16)

@@ -973,27 +973,43 @@ std::string Session::choose(const std::string& spec, cudaStream_t stream) {
           "auto strategy needs a non-empty 'candidates' list (or a 'table')");
   require(!dry_, Errc::EngineStopped, "auto strategy selection needs a device session");
   const int reps = v.get("reps") ? static_cast<int>(v.get("reps")->as_i64()) : 5;
+  // candidates timed in interleaved rounds, median per candidate: a B200 under
+  // its power cap drifts by several % within a second, so timing each
+  // candidate once, back to back, let the drift pick the winner
+  const int rounds = v.get("rounds") ? std::max(1, static_cast<int>(v.get("rounds")->as_i64())) : 3;
   const auto dump = dump_json;
   cudaEvent_t e0, e1;
   OPF_CUDA(cudaEventCreate(&e0));
   OPF_CUDA(cudaEventCreate(&e1));
+  std::vector<std::string> specs;
+  std::vector<std::unique_ptr<Scheduler>> strats;
+  for (const json::Value& c : cands->arr()) {
+    specs.push_back(dump(c));
+    strats.push_back(make_strategy(specs.back()));
+    run(*strats.back(), "builtin:" + specs.back(), stream);  // build + capture + warm-up
+  }
+  std::vector<std::vector<double>> per(specs.size());
+  for (int r = 0; r < rounds; ++r)
+    for (size_t i = 0; i < specs.size(); ++i) {
+      OPF_CUDA(cudaEventRecord(e0, stream));
+      for (int k = 0; k < reps; ++k) run(*strats[i], "builtin:" + specs[i], stream);
+      OPF_CUDA(cudaEventRecord(e1, stream));
+      OPF_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.0f;
+      OPF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      per[i].push_back(ms / reps);
+    }
   std::vector<double> times;
   std::string best;
   double best_ms = 1e300;
-  for (const json::Value& c : cands->arr()) {
-    const std::string cs = dump(c);
-    auto strat = make_strategy(cs);
-    run(*strat, "builtin:" + cs, stream);  // build + capture + warm-up
-    OPF_CUDA(cudaEventRecord(e0, stream));
-    for (int i = 0; i < reps; ++i) run(*strat, "builtin:" + cs, stream);
-    OPF_CUDA(cudaEventRecord(e1, stream));
-    OPF_CUDA(cudaEventSynchronize(e1));
-    float ms = 0.0f;
-    OPF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    times.push_back(ms / reps);
-    if (ms / reps < best_ms) {
-      best_ms = ms / reps;
-      best = cs;
+  for (size_t i = 0; i < specs.size(); ++i) {
+    std::vector<double> t = per[i];
+    std::sort(t.begin(), t.end());
+    const double med = t[t.size() / 2];
+    times.push_back(med);
+    if (med < best_ms) {
+      best_ms = med;
+      best = specs[i];
     }
   }
   cudaEventDestroy(e0);
