@@ -747,10 +747,13 @@ QWEN3 = dict(hidden=2048, heads=32, kv_heads=4, head_dim=128, experts=128, topk=
 def time_op(of, torch, dev, stream, fn, ins, outs, params, rows, reps=8, shared=()):
     """One registered op (prepack + workspace planned by the engine) timed on
     the device: `reps` copies back to back in one CUDA graph, rotated inputs
-    (names in `shared` are bound once), CUDA events on `stream`."""
+    (names in `shared` are bound once), CUDA events on `stream`; like the GEMM
+    rooflines, after a short idle and as the best of 10 replays (burst)."""
     op = {"name": "op", "kind": "Custom", "inputs": [i[0] for i in ins], "outputs": [o[0] for o in outs],
           "attrs": {"custom_name": fn, "params": params}}
-    return graph_reps_ms(of, torch, dev, stream, list(ins) + list(outs), op, shared=shared, reps=reps)
+    torch.cuda.synchronize()
+    time.sleep(COOLDOWN_S)
+    return graph_reps_ms(of, torch, dev, stream, list(ins) + list(outs), op, shared=shared, reps=reps, best_of=10)
 
 
 def run_moe(of, torch, dev, args, rank, world, stream, comm=None, window_ok=True):
