@@ -213,7 +213,8 @@ def test_llama_decode_bf16(cuda, kv_layout):
 
 @pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 512, 1024), (300, 520, 200), (1, 256, 64),
                                    (2048, 6144, 4096), (8192, 4096, 512), (77, 3000, 1032),
-                                   (8192, 768, 4096), (8192, 3584, 512), (8192, 712, 256), (1000, 712, 256)])
+                                   (8192, 768, 4096), (8192, 3584, 512), (8192, 712, 256), (1000, 712, 256),
+                                   (8000, 4096, 448), (12000, 2000, 192)])
 def test_gemm_tcgen05_vs_torch(cuda, m, n, k):
     import torch
     g = torch.Generator(device="cuda").manual_seed(m * 7 + n)
