@@ -248,7 +248,11 @@ __global__ void __launch_bounds__(128 + NP * 128, 1)
   uint64_t* v_empty = bars + 18; // [2]  PV_j retired (V slot free)
   uint64_t* s_full = bars + 8;   // [2]
   uint64_t* s_free = bars + 10;  // [2]
-  uint64_t* p_full = bars + 12;  // single P buffer
+  // one barrier per P buffer: a fast softmax warp may store P_{j+1} before a
+  // slow one stores P_j (S_{j+1} is already computed and P_{j+1} needs no PV
+  // to retire when j + 1 < 2); with one barrier for both buffers its early
+  // arrival completed P_j's phase and PV_j read a stale P quarter
+  uint64_t* p_full = bars + 12;  // [2]
   uint64_t* o_done = bars + 14;  // one phase per PV
   uint64_t* o_free = bars + 15;  // epilogue finished reading O
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
@@ -277,7 +281,8 @@ __global__ void __launch_bounds__(128 + NP * 128, 1)
       bar_init(&s_full[i], 1);
       bar_init(&s_free[i], kSoftW);
     }
-    bar_init(p_full, kSoftW);
+    bar_init(&p_full[0], kSoftW);
+    bar_init(&p_full[1], kSoftW);
     bar_init(o_done, 1);
     bar_init(o_free, kSoftW);
     *pv_count = 0;
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(128 + NP * 128, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
       int stage = 0;
-      uint32_t ph = 0, qph = 0, ofree_ph = 0, pfull_ph = 0;
+      uint32_t ph = 0, qph = 0, ofree_ph = 0, pfull_ph = 0;  // pfull_ph: per-P-buffer bits
       uint32_t sfree_ph = 0, sbuf_used = 0;  // per-S-buffer bits
       bool first_item = true;
       const uint32_t S_id = idesc(false), PV_id = idesc(true);
@@ -376,8 +381,8 @@ __global__ void __launch_bounds__(128 + NP * 128, 1)
         int pv_stage = stage;
         uint32_t pv_ph = ph;
         auto issue_pv = [&](int j) {
-          bar_wait(p_full, pfull_ph);
-          pfull_ph ^= 1;
+          bar_wait(&p_full[j & 1], (pfull_ph >> (j & 1)) & 1u);
+          pfull_ph ^= 1u << (j & 1);
           bar_wait(&v_full[pv_stage], pv_ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t vb = su32(sm + kSmemV + pv_stage * kTile);
@@ -563,7 +568,7 @@ __global__ void __launch_bounds__(128 + NP * 128, 1)
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) bar_arrive(p_full);
+        if (lane == 0) bar_arrive(&p_full[j & 1]);
         if (lane == 0 && warp == 4) FA_T(6, tile_sm);
         ++tile_sm;
       }
