@@ -166,3 +166,23 @@ def test_decode_hnd_layout_matches_nhd(cuda, nq, nkv):
     assert np.array_equal(outs[0], outs[1])  # same math, same order: bit-identical
     for b in range(B):
         assert rel_err(outs[1][b], want[b]) < 1e-2
+
+
+@pytest.mark.parametrize("S,nq,nkv,seqs", [(384, 6, 2, 5), (1024, 8, 2, 2), (512, 12, 4, 3)])
+def test_prefill_budget_sweep_rows(cuda, S, nq, nkv, seqs):
+    """Both tcgen05 prefill kernels (odd group -> one head per item, even ->
+    head pairs, small budgets -> several items per CTA) over a sweep of CTA
+    budgets, every output row against the oracle: a softmax warp running a tile
+    ahead of its neighbours once completed the wrong P buffer's phase (whole
+    32-row quarters wrong), visible under changed timing (tools/attn_stress.py)."""
+    import torch
+    rng = np.random.default_rng(S + nq)
+    rows = S * seqs
+    qkv = rng.uniform(-1, 1, (rows, (nq + 2 * nkv) * 128)).astype(np.float32)
+    t = torch.from_numpy(qkv).cuda().to(torch.bfloat16)
+    want = oracle.attn_prefill(t.float().cpu().numpy(), nq, nkv, 128, S)
+    for cap in (1, 2, 3, 5, 7, 16, 0):
+        for _ in range(3):
+            got = _prefill(t, nq, nkv, S, rows, max_ctas=cap)
+            row_err = np.abs(got - want).max(axis=1) / (np.abs(want).max(axis=1) + 1e-6)
+            assert row_err.max() < 5e-2, (cap, int(row_err.argmax()), float(row_err.max()))
