@@ -114,16 +114,16 @@ __global__ void __launch_bounds__(256) topk_kernel(const T* __restrict__ logits,
 // ---------------------------------------------------------------- routing
 // Stable counting sort of the n = T*k slots by expert in THREE launches:
 //   route_hist_kernel   C CTAs, one chunk of `chunk` slots each -> cnt[c][e]
-//   route_assign_kernel C CTAs: every CTA loads the whole C x E count matrix
-//                       (<= 64 KB) into smem and derives its own bases
-//                       (expert offsets + the counts of earlier chunks) —
-//                       no separate scan launch — then ranks its slots round
+//   route_assign_kernel C CTAs: every CTA reduces the whole C x E count
+//                       matrix (all 1024 threads, strided over chunks) to
+//                       its own bases (expert offsets + the counts of earlier
+//                       chunks) — no separate scan launch — then ranks its slots round
 //                       by round (1024 per round: per-warp expert counts,
 //                       a scan over the 32 warps, __match_any_sync inside a warp)
 //   gather_tokens_kernel one warp per token: the row is read once and
 //                       written to its k expert-sorted rows
 // The grouped GEMMs only need the tile table: route_hist + route_tiles_kernel.
-// C <= 64 and C * E <= 16384 keep the count matrix in shared memory.
+// C <= 64 chunks (C * E <= 16384 counts).
 constexpr int kRouteThreads = 1024;
 
 int64_t route_chunk(int64_t n, int E) {
@@ -178,10 +178,12 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* warp_tot,
   return r;
 }
 
-// shared memory of route_assign_kernel: counts [C][E] i32, run [E] i32,
-// per-warp counts [32][E] u16, 32 warp totals
+// shared memory of route_assign_kernel: partial sums [2][kRouteThreads] i32,
+// run [E] i32, per-warp counts [32][E] u16, 32 warp totals
 size_t route_assign_smem(int C, int E) {
-  return static_cast<size_t>(C) * E * 4 + static_cast<size_t>(E) * 4 + 32 * static_cast<size_t>(E) * 2 + 32 * 4;
+  (void)C;
+  return 2 * static_cast<size_t>(kRouteThreads) * 4 + static_cast<size_t>(E) * 4 + 32 * static_cast<size_t>(E) * 2 +
+         32 * 4;
 }
 
 __global__ void __launch_bounds__(kRouteThreads) route_assign_kernel(const int64_t* __restrict__ ids, int64_t n, int E,
@@ -192,22 +194,33 @@ __global__ void __launch_bounds__(kRouteThreads) route_assign_kernel(const int64
                                                                      int32_t* __restrict__ off_out) {
   pdl_wait();
   extern __shared__ __align__(16) uint8_t rs[];
-  int32_t* cm = reinterpret_cast<int32_t*>(rs);
-  int32_t* run = cm + static_cast<int64_t>(C) * E;
+  int32_t* ps = reinterpret_cast<int32_t*>(rs);  // [2][kRouteThreads] partial (total, before-me) sums
+  int32_t* run = ps + 2 * kRouteThreads;
   uint16_t* wh = reinterpret_cast<uint16_t*>(run + E);
   int32_t* wt = reinterpret_cast<int32_t*>(wh + 32 * E);
   const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
-  for (int i = tid; i < C * E; i += blockDim.x) cm[i] = cnt[i];
   for (int i = tid; i < 32 * E; i += blockDim.x) wh[i] = 0;
-  __syncthreads();
   // bases of this chunk (thread e owns expert e): off[e] = exclusive scan of
-  // the expert totals, plus the counts of the chunks before this one
+  // the expert totals, plus the counts of the chunks before this one.  Every
+  // thread sums a strided share of one expert's chunk counts straight from
+  // global memory (C / parts loads each), reduced through shared memory.
+  const int parts = kRouteThreads / E;  // E <= kRouteThreads
+  if (tid < parts * E) {
+    int32_t a = 0, b = 0;
+    for (int c = tid / E; c < C; c += parts) {
+      const int32_t v = cnt[static_cast<int64_t>(c) * E + tid % E];
+      a += v;
+      if (c < static_cast<int>(blockIdx.x)) b += v;
+    }
+    ps[tid] = a;
+    ps[kRouteThreads + tid] = b;
+  }
+  __syncthreads();
   int32_t tot = 0, pre = 0;
   if (tid < E)
-    for (int c = 0; c < C; ++c) {
-      const int32_t v = cm[c * E + tid];
-      tot += v;
-      if (c < static_cast<int>(blockIdx.x)) pre += v;
+    for (int p2 = 0; p2 < parts; ++p2) {
+      tot += ps[p2 * E + tid];
+      pre += ps[kRouteThreads + p2 * E + tid];
     }
   const int32_t off = block_excl_scan(tid < E ? tot : 0, wt, nullptr);
   if (tid < E) {
@@ -261,10 +274,20 @@ __global__ void __launch_bounds__(kRouteThreads) route_tiles_kernel(const int32_
                                                                     int tile_m, int32_t* __restrict__ gtab) {
   pdl_wait();
   __shared__ int32_t wt[32];
+  __shared__ int32_t part_sum[kRouteThreads];
   const int tid = threadIdx.x;
+  // every thread sums a strided share of the chunk counts of one expert
+  // (C / parts independent loads each instead of C dependent ones on E threads)
+  const int parts = kRouteThreads / E;  // E <= kRouteThreads
+  if (tid < parts * E) {
+    int32_t acc = 0;
+    for (int c = tid / E; c < C; c += parts) acc += cnt[static_cast<int64_t>(c) * E + tid % E];
+    part_sum[tid] = acc;
+  }
+  __syncthreads();
   int32_t tot = 0;
   if (tid < E)
-    for (int c = 0; c < C; ++c) tot += cnt[static_cast<int64_t>(c) * E + tid];
+    for (int p2 = 0; p2 < parts; ++p2) tot += part_sum[p2 * E + tid];
   const int32_t tiles = tid < E ? (tot + tile_m - 1) / tile_m : 0;
   const int32_t off = block_excl_scan(tid < E ? tot : 0, wt, nullptr);
   int32_t n_tiles = 0;
