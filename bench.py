@@ -501,6 +501,10 @@ def run_ours(args):
     seq_ms, best_ms = results["sequential"], results[best]
     tokens_job = T * 1  # TP: every rank processes the same T tokens of one replica
     value = tokens_job / (best_ms / 1e3)
+    # launch count / plan of the schedule `value` reports (the last timed run
+    # may have been another candidate or `auto`'s pick)
+    sess.run(cands[best], stream)
+    torch.cuda.synchronize()
     stats = sess.stats()
     launches = stats["last"]["launches"]
 
