@@ -68,13 +68,8 @@ __device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
                : "memory");
 }
-// Every arrive in this file hands TMEM (S, P or O) to the other side and
-// follows tcgen05.wait + tcgen05.fence::before_thread_sync, which order the
-// tensor-memory accesses; no generic-memory data rides on these barriers, so
-// the arrive is relaxed (no drain of the thread's in-flight global stores;
-// measured neutral here, unlike the GEMM epilogue's hand-back).
 __device__ __forceinline__ void bar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
 __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
