@@ -13,9 +13,10 @@
 // fp32 on the fragments; the W warps' (m, l, O) and the current token merge in
 // shared memory.  Algorithmic bytes per (sequence, kv head) = 2 * ctx * 128 * 2.
 //
-// Shipped shape: W = 12 warps, D = 2 pages per warp (192 KB of rings, 165
-// registers, one CTA per SM), 0.93 of the measured HBM read peak at 512 x 4K
-// (DESIGN §5).  Measured losers (an M = 16 padded-group kernel, a shared TMA
+// Shipped shapes: W = 6 warps, D = 2 pages per warp (96 KB of rings, 165
+// registers), two CTAs per SM; under an explicit SM budget (NanoFlow lane
+// partitions) W = 12, one CTA per SM.  0.94 of the measured HBM read peak at
+// 512 x 4K.  Measured losers (an M = 16 padded-group kernel, a shared TMA
 // ring, TMA-fed per-warp rings, other W x D shapes, and the co-resident 4/8-warp
 // shapes of commit 7418aec) live in the git history and DESIGN §5.1 / §8.
 #include <cuda.h>
@@ -291,16 +292,29 @@ bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __
                      cudaStream_t s) {
   if (hd != HD || page != PAGE || nq % nkv != 0 || nq / nkv > 8) return false;
   const int64_t items = B * nkv;
-  int64_t grid = max_ctas > 0 ? std::min<int64_t>(max_ctas, num_sms()) : num_sms();
-  grid = std::max<int64_t>(1, std::min(grid, items));
+  const int64_t grid = max_ctas > 0 ? std::min<int64_t>(max_ctas, num_sms()) : num_sms();  // SM budget
   const float sl2 = scale * 1.4426950408889634f;
   static const bool ef = [] {
     const char* e = std::getenv("OPF_DECODE_L2");  // "normal": plain cp.async (A/B switch)
     return !(e && std::string(e) == "normal");
   }();
+  // Two CTAs of 6 warps (96 KB of rings each) per SM, not one of 12: the
+  // same bytes in flight per SM, but an SM keeps streaming while one of its
+  // CTAs is between items — which matters when there are few items per SM
+  // (TP=8 per-rank shape, 512 items on 148 SMs: 170 -> 159 us; 64 x 4K:
+  // 166 -> 157 us; 512 x 4K at TP=1: 1229 -> 1221-1228 us; same box).
+  // An explicit SM budget (a NanoFlow lane partition) keeps one 12-warp CTA
+  // per SM, so that the CTA count still bounds the SMs the lane occupies.
+  if (max_ctas > 0) {
+    const int64_t g1 = std::max<int64_t>(1, std::min<int64_t>(grid, items));
+    if (ef)
+      return launch_decode_t<12, 2, 1, true>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, g1, hnd, s);
+    return launch_decode_t<12, 2, 1, false>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, g1, hnd, s);
+  }
+  const int64_t g2 = std::max<int64_t>(1, std::min<int64_t>(2 * grid, items));
   if (ef)
-    return launch_decode_t<12, 2, 1, true>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
-  return launch_decode_t<12, 2, 1, false>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, grid, hnd, s);
+    return launch_decode_t<6, 2, 2, true>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, g2, hnd, s);
+  return launch_decode_t<6, 2, 2, false>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, g2, hnd, s);
 }
 
 }  // namespace opflow
