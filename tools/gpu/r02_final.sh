@@ -13,7 +13,7 @@ timeout 600 $NCU --metrics gpu__time_duration.sum -c 3000 --csv --log-file $O/la
 timeout 600 $NCU --metrics gpu__time_duration.sum -c 600 --csv --log-file $O/launches_decode4.csv \
   python tools/step_breakdown.py decode 4 > $O/launches_decode4.log 2>&1; echo "launches2 rc=$?"
 cap() {  # name, which, kernel regex, count
-  timeout 400 $NCU --set full --import-source on -k "regex:$3" -c $4 -o /tmp/$1 python tools/profile_kernels.py $2 > $O/ncu/$1.log 2>&1
+  timeout 400 $NCU --set full --import-source on -f -k "regex:$3" -c $4 -o /tmp/$1 python tools/profile_kernels.py $2 > $O/ncu/$1.log 2>&1
   echo "$1 rc=$?"
   python profiles/ncu_summary.py /tmp/$1.ncu-rep > $O/ncu/$1.summary.txt 2>&1
   ncu -i /tmp/$1.ncu-rep --page details --csv > $O/ncu/$1.details.csv 2>/dev/null
