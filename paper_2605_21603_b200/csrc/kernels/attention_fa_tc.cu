@@ -576,19 +576,27 @@ __global__ void __launch_bounds__(128 + NP * 128, 1)
       const float inv = l_all > 0.0f ? 1.0f / l_all : 0.0f;
       __nv_bfloat16* orow = out + (static_cast<int64_t>(seq) * S + qt * BQ + r) * (static_cast<int64_t>(nq) * HD) +
                             static_cast<int64_t>(h) * HD + pt * CP;
+      // 256-bit stores when the output base allows (as in the two-head kernel:
+      // half the scattered store wavefronts of 128-bit pieces)
+      const bool out32 = (reinterpret_cast<uintptr_t>(out) & 31) == 0;
 #pragma unroll
       for (int c = 0; c < CP / 32; ++c) {
         float o[32];
         tld32(o_base + c * 32, o);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          uint4 u;
-          u.x = bf2(o[v * 8 + 0] * inv, o[v * 8 + 1] * inv);
-          u.y = bf2(o[v * 8 + 2] * inv, o[v * 8 + 3] * inv);
-          u.z = bf2(o[v * 8 + 4] * inv, o[v * 8 + 5] * inv);
-          u.w = bf2(o[v * 8 + 6] * inv, o[v * 8 + 7] * inv);
-          *reinterpret_cast<uint4*>(orow + c * 32 + v * 8) = u;
+        for (int v = 0; v < 2; ++v) {
+          uint32_t w[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) w[e] = bf2(o[v * 16 + 2 * e] * inv, o[v * 16 + 2 * e + 1] * inv);
+          if (out32) {
+            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(orow + c * 32 + v * 16),
+                         "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                         : "memory");
+          } else {
+            reinterpret_cast<uint4*>(orow + c * 32 + v * 16)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            reinterpret_cast<uint4*>(orow + c * 32 + v * 16)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
