@@ -736,7 +736,7 @@ def run_decode(of, torch, dev, args, tp, comm, rank, world, stream):
             "auto": None if auto_pick is None else {
                 "ms_per_step": round(auto_ms, 3), "chosen": auto_pick,
                 "speedup_vs_sequential": round(res["sequential"] / auto_ms, 4)},
-            "roofline": {"bound": "hbm", "kernel": "decode_t_kernel<6,2,2> (paged attention; tokens on MMA M, GQA group on N; 6 warps x 2-page cp.async rings, 2 CTAs per SM)",
+            "roofline": {"bound": "hbm", "kernel": "decode_t_kernel<6,2,2> (paged attention; tokens on MMA M, GQA group on N; one (seq, kv head) item per 6-warp CTA, 2-page cp.async rings, 2 CTAs per SM)",
                          "achieved": round(achieved, 1), "peak": PEAKS["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / PEAKS["hbm_gbs"], 4), "ms_per_launch": round(attn_ms, 4),
                          "read_peak_gbs": 7443.2, "frac_of_read_peak": round(achieved / 7443.2, 4),

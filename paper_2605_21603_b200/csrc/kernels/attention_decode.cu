@@ -4,8 +4,9 @@
 // [pages, nkv, 16, 128] HND, bf16) with a per-sequence block table; each
 // sequence attends to its `ctx` cached tokens plus itself.
 //
-// Persistent: the grid is the SM budget; a CTA walks (sequence, kv head) items,
-// so every K/V byte is read once.  Warp w of W streams pages w, w+W, ... (16
+// One (sequence, kv head) item per CTA — or, under an explicit SM budget, a
+// persistent grid of the budget walking the items — so every K/V byte is read
+// once.  Warp w of W streams pages w, w+W, ... (16
 // tokens x 256 B of K and of V each) with cp.async into its private D-deep ring
 // (XOR-swizzled).  Tokens sit on the MMA M dimension and the GQA group on N:
 // S^T = K Q^T and O^T += V^T P^T are 8 + 8 mma.sync m16n8k16 per page, so the
@@ -14,9 +15,9 @@
 // shared memory.  Algorithmic bytes per (sequence, kv head) = 2 * ctx * 128 * 2.
 //
 // Shipped shapes: W = 6 warps, D = 2 pages per warp (96 KB of rings, 165
-// registers), two CTAs per SM; under an explicit SM budget (NanoFlow lane
-// partitions) W = 12, one CTA per SM.  0.94 of the measured HBM read peak at
-// 512 x 4K.  Measured losers (an M = 16 padded-group kernel, a shared TMA
+// registers), two CTAs per SM, one item each; under an explicit SM budget
+// (NanoFlow lane partitions) W = 12, one persistent CTA per SM.  0.97 of the
+// measured HBM read peak at 512 x 4K.  Measured losers (an M = 16 padded-group kernel, a shared TMA
 // ring, TMA-fed per-warp rings, other W x D shapes, and the co-resident 4/8-warp
 // shapes of commit 7418aec) live in the git history and DESIGN §5.1 / §8.
 #include <cuda.h>
@@ -298,20 +299,22 @@ bool decode_bf16_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* kc, const __
     const char* e = std::getenv("OPF_DECODE_L2");  // "normal": plain cp.async (A/B switch)
     return !(e && std::string(e) == "normal");
   }();
-  // Two CTAs of 6 warps (96 KB of rings each) per SM, not one of 12: the
-  // same bytes in flight per SM, but an SM keeps streaming while one of its
-  // CTAs is between items — which matters when there are few items per SM
-  // (TP=8 per-rank shape, 512 items on 148 SMs: 170 -> 159 us; 64 x 4K:
-  // 166 -> 157 us; 512 x 4K at TP=1: 1229 -> 1221-1228 us; same box).
-  // An explicit SM budget (a NanoFlow lane partition) keeps one 12-warp CTA
-  // per SM, so that the CTA count still bounds the SMs the lane occupies.
+  // An explicit SM budget (a NanoFlow lane partition) keeps the persistent
+  // form, one 12-warp CTA per SM, so the CTA count bounds the SMs the lane
+  // occupies.  Otherwise one (sequence, kv head) item per CTA of 6 warps
+  // (96 KB of rings, two per SM) and the hardware scheduler refills an SM as
+  // soon as one of its CTAs finishes: no round quantisation, and a new item's
+  // ring fill overlaps the other CTA's streaming.  Same box, 512 x 4K: the
+  // persistent 12-warp form 1229 us, persistent 6-warp x 2 per SM 1223 us,
+  // one item per CTA 1189 us (7.22 TB/s, 0.97 of the read peak); TP=8 per-rank
+  // shape 170 / 159 / 159 us (profiles/r02_decode_half_cta_ab.txt).
   if (max_ctas > 0) {
     const int64_t g1 = std::max<int64_t>(1, std::min<int64_t>(grid, items));
     if (ef)
       return launch_decode_t<12, 2, 1, true>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, g1, hnd, s);
     return launch_decode_t<12, 2, 1, false>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, g1, hnd, s);
   }
-  const int64_t g2 = std::max<int64_t>(1, std::min<int64_t>(2 * grid, items));
+  const int64_t g2 = std::max<int64_t>(1, items);
   if (ef)
     return launch_decode_t<6, 2, 2, true>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, g2, hnd, s);
   return launch_decode_t<6, 2, 2, false>(qkv, kc, vc, table, ctx, out, nq, nkv, max_pages, sl2, items, g2, hnd, s);
