@@ -68,6 +68,12 @@ __device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
                : "memory");
 }
+// 16-byte global store that does not allocate in L1 (the output epilogues)
+__device__ __forceinline__ void st_na_v4(void* p, const uint32_t* w) {
+  asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+               "r"(w[3])
+               : "memory");
+}
 __device__ __forceinline__ void bar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
@@ -576,8 +582,8 @@ __global__ void __launch_bounds__(128 + NP * 128, 1)
       const float inv = l_all > 0.0f ? 1.0f / l_all : 0.0f;
       __nv_bfloat16* orow = out + (static_cast<int64_t>(seq) * S + qt * BQ + r) * (static_cast<int64_t>(nq) * HD) +
                             static_cast<int64_t>(h) * HD + pt * CP;
-      // 256-bit stores when the output base allows (as in the two-head kernel:
-      // half the scattered store wavefronts of 128-bit pieces)
+      // 256-bit stores that do not allocate in L1 when the output base allows
+      // (as in the two-head kernel)
       const bool out32 = (reinterpret_cast<uintptr_t>(out) & 31) == 0;
 #pragma unroll
       for (int c = 0; c < CP / 32; ++c) {
@@ -590,12 +596,12 @@ __global__ void __launch_bounds__(128 + NP * 128, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e) w[e] = bf2(o[v * 16 + 2 * e] * inv, o[v * 16 + 2 * e + 1] * inv);
           if (out32) {
-            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(orow + c * 32 + v * 16),
+            asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(orow + c * 32 + v * 16),
                          "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
                          : "memory");
           } else {
-            reinterpret_cast<uint4*>(orow + c * 32 + v * 16)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            reinterpret_cast<uint4*>(orow + c * 32 + v * 16)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            st_na_v4(orow + c * 32 + v * 16, w);
+            st_na_v4(orow + c * 32 + v * 16 + 8, w + 4);
           }
         }
       }
@@ -875,10 +881,12 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const float inv = d.l > 0.0f ? 1.0f / d.l : 0.0f;
       __nv_bfloat16* op = out + (d.row0 + r) * (static_cast<int64_t>(nq) * HD) + static_cast<int64_t>(d.head) * HD;
-      // 32-byte stores (one sector per lane per instruction): half the
-      // scattered store wavefronts of 16-byte pieces — this warp's 32 rows are
-      // 8 KB apart, and the epilogue's store traffic shares the L1 / shared
-      // memory pipeline the MMAs read their operands through
+      // Output rows go out with 32-byte stores that do not allocate in L1.
+      // This warp's 32 rows are 8 KB apart, so every store instruction
+      // scatters over 32 lines, and that traffic shares the L1 / shared
+      // memory array the MMAs read Q, K and V from: allocating the lines in
+      // L1 cost 6%, and 16-byte pieces (twice the sectors) another 3%
+      // (profiles/r02_attention_st256_ab.txt).
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float o[32];
@@ -890,12 +898,12 @@ __global__ void __launch_bounds__(kPPThreads, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e) w[e] = bf2(o[v * 16 + 2 * e] * inv, o[v * 16 + 2 * e + 1] * inv);
           if (out32) {
-            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(op + c * 32 + v * 16),
+            asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(op + c * 32 + v * 16),
                          "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
                          : "memory");
           } else {  // output base only 16-byte aligned (a caller-owned view)
-            reinterpret_cast<uint4*>(op + c * 32 + v * 16)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            reinterpret_cast<uint4*>(op + c * 32 + v * 16)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            st_na_v4(op + c * 32 + v * 16, w);
+            st_na_v4(op + c * 32 + v * 16 + 8, w + 4);
           }
         }
       }
