@@ -799,7 +799,8 @@ __device__ __forceinline__ void mbar_arrive_leader_relaxed(uint64_t* bar) {
 template <int EPI, int TN, typename Release, typename Mark>
 __device__ __forceinline__ void store_tile_st(uint32_t tmem_col0, uint8_t* sbuf, int lane, int64_t nb, int64_t row0,
                                               int64_t M, int64_t n_out, __nv_bfloat16* __restrict__ c, int64_t ldc,
-                                              const RopeArgs* rope, Release&& release, Mark&& mark) {
+                                              const RopeArgs* rope, Release&& release, Mark&& mark,
+                                              bool direct = false) {
   constexpr int kChunks = EPI == 1 ? 2 : TN / 64;
   float ss = 0.0f;  // EPI 4: this lane's row, this tile's columns
   const bool row_ok = row0 + lane < M;
@@ -852,6 +853,32 @@ __device__ __forceinline__ void store_tile_st(uint32_t tmem_col0, uint8_t* sbuf,
             dst[2 * e + 1] = __float_as_uint(b);
           }
         }
+      }
+    }
+    // direct (32-byte aligned rows only): each lane stores its own row's 64
+    // columns (32 B per store, not allocated in L1) instead of staging them through shared memory for
+    // 4-row coalesced stores.  The staging's shared-memory traffic (128 KB per
+    // 256x256 tile) matters on short-K tiles (8-28 k-blocks: the TP=8 O and
+    // down projections, -4% / -1.7%); on K >= 4096 the coalesced form is as
+    // fast or faster (profiles/r02_gemm_epi_direct_na_ab.txt).
+    if (direct) {
+      const int64_t col0d = (EPI == 1 ? nb * (TN / 2) : nb * TN) + chunk * 64;
+      if (col0d + 64 <= n_out) {
+        if (row_ok) {
+          __nv_bfloat16* dst = c + (row0 + lane) * ldc + col0d;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t* src = j < 2 ? &v0[16 * j] : &v1[16 * (j - 2)];
+            uint32_t w[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) w[e] = pack_bf16(src[2 * e], src[2 * e + 1]);
+            asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 16 * j),
+                         "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                         : "memory");
+          }
+        }
+        mark(5);
+        continue;
       }
     }
     __syncwarp();  // the previous chunk's read-back of sbuf is done
@@ -1235,7 +1262,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
           if (warp == 2 && lane == 0) GTRACE(2, ev, u);
         };
         store_tile_st<EPI, TN>(tcol, stg[0], lane, nb, row0, M, EPI == 1 ? N / 2 : N, c_out, ldc, &rope, release,
-                               mark);
+                               mark,
+                               K <= 2048 && ldc % 16 == 0 && (reinterpret_cast<uintptr_t>(c_out) & 31) == 0);
       }
       if (warp == 2 && lane == 0) GTRACE(2, 3, u);
       if (++acc == kAcc) {
