@@ -581,11 +581,13 @@ def run_ours(args):
         toy = run_toy(of, torch, dev, stream, args)
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(args, T, S, tp)
+        # "strong": the job is one replica of T tokens whatever N is (TP=N
+        # shards each layer; the MoE leg spreads the same T tokens over EP=N)
         line = {
             "metric": METRIC,
             "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(best_ms, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded uniform inputs, random-init weights)",
             "config": bench_config(args, tp),
             "strategy": best,
@@ -980,7 +982,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC,
         "value": cb["value"], "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(per_step * 1e3, 1), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded uniform inputs, random-init weights)",
         "config": bench_config(args, tp),
         "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,

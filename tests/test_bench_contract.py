@@ -38,6 +38,8 @@ def test_reference_arm_line():
     assert line["impl"] == "reference"
     import bench
     assert line["metric"] == bench.METRIC and line["unit"] == "tokens/s" and line["higher_is_better"] is True
+    # one replica of 8192 tokens whatever N is (TP=N shards the layer): total work fixed
+    assert line["scaling"] == "strong"
     assert line["config"]["workload"].startswith("llama3-8b-shaped prefill, 32 layers, 8192 tokens")
     cb = line["cpu_baseline"]
     assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] > 0 and cb["cpu_model"]
