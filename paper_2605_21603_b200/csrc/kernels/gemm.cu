@@ -981,10 +981,6 @@ __device__ __forceinline__ void store_tile_rope_st(uint32_t tmem_col0, uint8_t* 
   }
 }
 
-// GROUPED (MoE experts, TN = 256, unsplit): gtab = [n_tiles, (row0, row_end,
-// expert) x n_tiles] with 256-row tiles; N is the per-expert width, expert e's
-// B rows start at e * N; rows of a tile past row_end belong to the next
-// expert's tile (computed, never stored).
 // Push epilogue (EPI 3): the 32-row slab of this warp goes straight into the
 // owner rank's window (row r -> owner r / blk, this rank's slot there), 64
 // columns at a time through the swizzled staging buffer so every store
@@ -1062,12 +1058,11 @@ __device__ int g_gemm_trace_n[3];
   } while (0)
 #endif
 
-template <int EPI, int TN, bool SPLIT = false, bool GROUPED = false>
+template <int EPI, int TN, bool SPLIT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_c, int64_t M, int64_t N, int64_t K, int splits,
-                    float4* __restrict__ ws, int* __restrict__ sem, RopeArgs rope,
-                    const int32_t* __restrict__ gtab, __nv_bfloat16* __restrict__ c_out,
+                    float4* __restrict__ ws, int* __restrict__ sem, RopeArgs rope, __nv_bfloat16* __restrict__ c_out,
                     int64_t ldc, PushArgs push) {
   using C = Tc2Cfg<TN, SPLIT>;
   constexpr int kStages2 = C::kStages;
@@ -1090,7 +1085,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
   int gt_n = 0;
 #endif
   const bool leader = rank == 0;
-  int64_t m_blocks = (M + 2 * BM - 1) / (2 * BM);
+  const int64_t m_blocks = (M + 2 * BM - 1) / (2 * BM);
   const int64_t n_blocks = (N + TN - 1) / TN;
   const int k_blocks = static_cast<int>((K + BK - 1) / BK);
   const int64_t cluster = blockIdx.x / 2, n_clusters = gridDim.x / 2;
@@ -1121,7 +1116,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();     // inputs of the previous kernel on this stream are visible from here
   pdl_trigger();  // persistent grid: let the next kernel stage its prologue on freed SMs
-  if constexpr (GROUPED) m_blocks = *reinterpret_cast<const volatile int32_t*>(gtab);  // routing kernel output
   if constexpr (EPI == 3)  // one new push call: the reduce kernel that follows waits for this epoch's publishes
     if (blockIdx.x == 0 && threadIdx.x == 0) *push.epoch += 1;
   const int64_t tiles = m_blocks * n_blocks;
@@ -1136,12 +1130,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
         const int sp = static_cast<int>(u - t * splits);
         int64_t mb, nb;
         tile_coords(t, m_blocks, n_blocks, mb, nb);
-        int32_t m0 = static_cast<int32_t>(mb * 2 * BM + rank * BM);
-        int32_t n0 = static_cast<int32_t>(nb * TN + rank * (TN / 2));
-        if constexpr (GROUPED) {
-          m0 = gtab[1 + 3 * mb] + static_cast<int32_t>(rank * BM);
-          n0 += static_cast<int32_t>(gtab[3 + 3 * mb] * N);
-        }
+        const int32_t m0 = static_cast<int32_t>(mb * 2 * BM + rank * BM);
+        const int32_t n0 = static_cast<int32_t>(nb * TN + rank * (TN / 2));
         const int kb0 = splits == 1 ? 0 : sp * k_blocks / splits;
         const int kb1 = splits == 1 ? k_blocks : (sp + 1) * k_blocks / splits;
         GTRACE(0, 0, u);
@@ -1230,12 +1220,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
       mbar_wait(&tfull[acc], acc_phase);
       if (warp == 2 && lane == 0) GTRACE(2, 1, u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      int64_t row0 = mb * 2 * BM + rank * BM + quarter * 32;
-      int64_t row_end = M;
-      if constexpr (GROUPED) {
-        row0 = gtab[1 + 3 * mb] + rank * BM + quarter * 32;
-        row_end = gtab[2 + 3 * mb];
-      }
+      const int64_t row0 = mb * 2 * BM + rank * BM + quarter * 32;
       const uint32_t tcol = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * TN);
       auto release = [&]() {  // accumulator fully read: hand it back to the MMA warp
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1243,14 +1228,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Cfg<TN, SPLIT>::k
         if (lane == 0) mbar_arrive_leader_relaxed(&tempty[acc]);
         if (warp == 2 && lane == 0) GTRACE(2, 2, u);
       };
-      if constexpr (GROUPED) {
-        // whole 32-row slabs inside the expert segment by TMA; the straddling slab row by row
-        if (row0 + 32 <= row_end)
-          store_tile<EPI, TN>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, kStep, &rope);
-        else
-          store_tile_direct<EPI>(tcol, c_out, ldc, row0 + lane, row_end, nb);
-        release();
-      } else if constexpr (EPI == 3) {
+      if constexpr (EPI == 3) {
         store_tile_push<TN>(tcol, stg[0], lane, nb, row0, M, N, push, release);
       } else if constexpr (SPLIT && TN == 256) {
         store_tile_splitk<EPI>(&map_c, tcol, stg, buf, lane, nb, row0, M, half, static_cast<int>(rank) * 8 + ew, t,
@@ -1328,10 +1306,6 @@ void gemm_bf16_tc_init() {
                                   static_cast<int>(kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
-    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<0, 256, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
-    OPF_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<1, 256, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(Tc2Cfg<256, false>::kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemBytes)));
     OPF_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1393,7 +1367,6 @@ size_t gemm_splitk_workspace(int64_t m, int64_t n, int64_t k, int max_ctas) {
          static_cast<size_t>(tiles * 16) * sizeof(int);
 }
 
-constexpr const int32_t* kNoGtab = nullptr;
 constexpr __nv_bfloat16* kNoOut = nullptr;
 constexpr PushArgs kNoPush{};
 
@@ -1458,28 +1431,28 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t s) {
     const dim3 blocks(2u * static_cast<unsigned>(std::max(clusters, 1)));
     if (splits > 1 && g.epi == 1)
       launch_pdl(gemm_tc2_kernel<1, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
-                 g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
+                 g.m, g.n, g.k, splits, ws, sem, rope, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (splits > 1)
       launch_pdl(gemm_tc2_kernel<0, 256, true>, blocks, dim3(Tc2Cfg<256, true>::kThreads), Tc2Cfg<256, true>::kSmemBytes, s, ma, mb, mc,
-                 g.m, g.n, g.k, splits, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
+                 g.m, g.n, g.k, splits, ws, sem, rope, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (g.epi == 4)
       launch_pdl(gemm_tc2_kernel<4, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb,
-                 mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
+                 mc, g.m, g.n, g.k, 1, ws, sem, rope, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (g.epi == 2 && tn == 384)
       launch_pdl(gemm_tc2_kernel<2, 384>, blocks, dim3(Tc2Cfg<384, false>::kThreads), Tc2Cfg<384, false>::kSmemBytes, s, ma, mb,
-                 mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
+                 mc, g.m, g.n, g.k, 1, ws, sem, rope, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (g.epi == 2)
       launch_pdl(gemm_tc2_kernel<2, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb,
-                 mc, g.m, g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
+                 mc, g.m, g.n, g.k, 1, ws, sem, rope, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (g.epi == 1)
       launch_pdl(gemm_tc2_kernel<1, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, splits, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
+                 g.n, g.k, splits, ws, sem, rope, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else if (tn == 256)
       launch_pdl(gemm_tc2_kernel<0, 256>, blocks, dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, splits, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
+                 g.n, g.k, splits, ws, sem, rope, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     else
       launch_pdl(gemm_tc2_kernel<0, 384>, blocks, dim3(Tc2Cfg<384, false>::kThreads), Tc2Cfg<384, false>::kSmemBytes, s, ma, mb, mc, g.m,
-                 g.n, g.k, 1, ws, sem, rope, kNoGtab, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
+                 g.n, g.k, 1, ws, sem, rope, static_cast<__nv_bfloat16*>(g.c), g.ldc, kNoPush);
     return;
   }
   const CUtensorMap mb = make_map(g.bt, g.k, g.n, g.k, BK, BN);
@@ -1516,21 +1489,14 @@ void gemm_bf16_push(const GemmArgs& g, const PushArgs& p, cudaStream_t s) {
   const int clusters = static_cast<int>(std::min<int64_t>(tiles, std::max(grid / 2, 1)));
   launch_pdl(gemm_tc2_kernel<3, 256>, dim3(2u * static_cast<unsigned>(std::max(clusters, 1))),
              dim3(Tc2Cfg<256, false>::kThreads), Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, ma, g.m, g.n, g.k, 1,
-             static_cast<float4*>(nullptr), static_cast<int*>(nullptr), RopeArgs{}, kNoGtab, kNoOut, int64_t{0}, p);
+             static_cast<float4*>(nullptr), static_cast<int*>(nullptr), RopeArgs{}, kNoOut, int64_t{0}, p);
 }
 
 // Grouped (per-expert) GEMM: rows of `a` are expert-sorted segments, gtab the
 // device tile table built by the routing kernel, bt = [E * group_n, K] packed
 // expert weights.  max_mtiles bounds the tile count (grid sizing happens on the
 // host; the actual count is read on the device, so the launch is capturable).
-int moe_tile_m() {
-  static const int t = [] {  // OPF_MOE_TILE=256 selects the 2-CTA grouped kernel (measured no faster:
-                             // tile waste at ~512 rows/expert offsets the pair efficiency)
-    const char* e = std::getenv("OPF_MOE_TILE");
-    return e && std::atoi(e) == 256 ? 256 : 128;
-  }();
-  return t;
-}
+int moe_tile_m() { return BM; }  // 128-row expert tiles: the 1-SM grouped kernel
 
 void gemm_bf16_grouped(const GemmArgs& g, const int32_t* gtab, int64_t max_mtiles, int64_t group_n,
                        int64_t n_groups, cudaStream_t s) {
@@ -1543,21 +1509,6 @@ void gemm_bf16_grouped(const GemmArgs& g, const int32_t* gtab, int64_t max_mtile
   int grid = num_sms();
   if (g.max_ctas > 0 && g.max_ctas < grid) grid = g.max_ctas;
   const int64_t tiles = max_mtiles * (group_n / BN);
-  if (moe_tile_m() == 256) {
-    // 2-CTA pairs on 256-row expert tiles (tile table built with tile_m = 256)
-    const CUtensorMap mb = make_map(g.bt, g.k, group_n * n_groups, g.k, BK, BN / 2);
-    const int clusters = static_cast<int>(std::max<int64_t>(std::min<int64_t>(tiles, std::max(grid / 2, 1)), 1));
-    const dim3 blocks(2u * static_cast<unsigned>(clusters));
-    if (g.epi == 1)
-      launch_pdl(gemm_tc2_kernel<1, 256, false, true>, blocks, dim3(Tc2Cfg<256, false>::kThreads),
-                 Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m, group_n, g.k, 1, static_cast<float4*>(nullptr),
-                 static_cast<int*>(nullptr), RopeArgs{}, gtab, c, g.ldc, kNoPush);
-    else
-      launch_pdl(gemm_tc2_kernel<0, 256, false, true>, blocks, dim3(Tc2Cfg<256, false>::kThreads),
-                 Tc2Cfg<256, false>::kSmemBytes, s, ma, mb, mc, g.m, group_n, g.k, 1, static_cast<float4*>(nullptr),
-                 static_cast<int*>(nullptr), RopeArgs{}, gtab, c, g.ldc, kNoPush);
-    return;
-  }
   const CUtensorMap mb = make_map(g.bt, g.k, group_n * n_groups, g.k, BK, BN);
   if (tiles < grid) grid = static_cast<int>(std::max<int64_t>(tiles, 1));
   if (g.epi == 1)
