@@ -23,7 +23,8 @@ __device__ __forceinline__ int64_t wrap_add(int64_t a, int64_t b) {
 }
 
 // out[r][j] = sum_k a[r][k] * w[k][j], k ascending, one rounding per mul and add.
-// 64x64 output tile per CTA, 16-deep k slabs staged in shared memory, 4x4 per thread.
+// 64x64 output tile per CTA, 16-deep k slabs staged in shared memory, 4x4 per
+// thread.  Launched for int64 (wrapping); fp32 takes matmul_exact_f32_kernel.
 template <typename T>
 __global__ void __launch_bounds__(256) matmul_exact_kernel(const T* __restrict__ a,
                                                            const T* __restrict__ w, T* __restrict__ out,
@@ -74,6 +75,117 @@ __global__ void __launch_bounds__(256) matmul_exact_kernel(const T* __restrict__
       const int64_t r = m0 + ty * 4 + i, c = n0 + tx * 4 + j;
       if (r < rows && c < N) out[r * N + c] = acc[i][j];
     }
+}
+
+// fp32 form of the same contraction, register-tiled: BM x BN output tile per
+// CTA of 256 threads (128x128: 8x8 outputs per thread; 64x64: 4x4, for grids
+// that would not fill the SMs), 8-deep k slabs double-buffered in shared
+// memory (A transposed so a thread reads its rows as float4), each thread's
+// rows / columns in 4-wide groups 64 apart (conflict-free 128-bit shared
+// loads).  Each output still accumulates k = 0..K-1 in order with one
+// __fmul_rn and one __fadd_rn per term, so it is bit-identical to
+// matmul_exact_kernel (and to kernels_scalar.cpp:40-66); the next slab's global
+// loads are in flight while the current one is consumed.
+constexpr int kXK = 8;
+template <int BM, int BN>
+__global__ void __launch_bounds__(256) matmul_exact_f32_kernel(const float* __restrict__ a,
+                                                               const float* __restrict__ w,
+                                                               float* __restrict__ out, int64_t rows,
+                                                               int64_t K, int64_t N, bool vec) {
+  constexpr int TM = BM / 16, TN = BN / 16;   // outputs per thread: TM rows x TN columns
+  constexpr int VA = BM * kXK / 256, VW = BN * kXK / 256;  // slab elements each thread loads
+  __shared__ __align__(16) float As[2][kXK][BM];
+  __shared__ __align__(16) float Ws[2][kXK][BN];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM, n0 = static_cast<int64_t>(blockIdx.x) * BN;
+  // loader roles: A — row lr, k columns lc..lc+VA-1; W — k row wr, columns wc..wc+VW-1
+  const int lr = tid / (kXK / VA), lc = (tid % (kXK / VA)) * VA;
+  const int wr = tid / (BN / VW), wc = (tid % (BN / VW)) * VW;
+  float ra[VA], rw[VW];
+  auto fetch = [&](int64_t k0) {
+    const int64_t gr = m0 + lr, gk = k0 + lc;
+    if (vec && gr < rows && gk + VA <= K) {
+      if constexpr (VA == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(a + gr * K + gk);
+        ra[0] = v.x, ra[1] = v.y, ra[2] = v.z, ra[3] = v.w;
+      } else {
+        const float2 v = *reinterpret_cast<const float2*>(a + gr * K + gk);
+        ra[0] = v.x, ra[1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VA; ++i) ra[i] = (gr < rows && gk + i < K) ? a[gr * K + gk + i] : 0.0f;
+    }
+    const int64_t gwr = k0 + wr, gwc = n0 + wc;
+    if (vec && gwr < K && gwc + VW <= N) {
+      if constexpr (VW == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(w + gwr * N + gwc);
+        rw[0] = v.x, rw[1] = v.y, rw[2] = v.z, rw[3] = v.w;
+      } else {
+        const float2 v = *reinterpret_cast<const float2*>(w + gwr * N + gwc);
+        rw[0] = v.x, rw[1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VW; ++i) rw[i] = (gwr < K && gwc + i < N) ? w[gwr * N + gwc + i] : 0.0f;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < VA; ++i) As[buf][lc + i][lr] = ra[i];
+#pragma unroll
+    for (int i = 0; i < VW; ++i) Ws[buf][wr][wc + i] = rw[i];
+  };
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
+  const int64_t n_slabs = (K + kXK - 1) / kXK;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  for (int64_t s = 0; s < n_slabs; ++s) {
+    const int buf = static_cast<int>(s & 1);
+    if (s + 1 < n_slabs) fetch((s + 1) * kXK);
+    const int kend = static_cast<int>(K - s * kXK < kXK ? K - s * kXK : kXK);
+    for (int kk = 0; kk < kend; ++kk) {
+      float av[TM], wv[TN];
+#pragma unroll
+      for (int g = 0; g < TM / 4; ++g) {
+        const float4 v = *reinterpret_cast<const float4*>(&As[buf][kk][g * 64 + ty * 4]);
+        av[4 * g] = v.x, av[4 * g + 1] = v.y, av[4 * g + 2] = v.z, av[4 * g + 3] = v.w;
+      }
+#pragma unroll
+      for (int g = 0; g < TN / 4; ++g) {
+        const float4 v = *reinterpret_cast<const float4*>(&Ws[buf][kk][g * 64 + tx * 4]);
+        wv[4 * g] = v.x, wv[4 * g + 1] = v.y, wv[4 * g + 2] = v.z, wv[4 * g + 3] = v.w;
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], wv[j]));
+    }
+    if (s + 1 < n_slabs) stash(buf ^ 1);  // the other buffer was last read before the previous barrier
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t r = m0 + (i / 4) * 64 + ty * 4 + i % 4;
+    if (r >= rows) continue;
+#pragma unroll
+    for (int h = 0; h < TN / 4; ++h) {
+      const int64_t c = n0 + h * 64 + tx * 4;
+      if (vec && c + 4 <= N) {
+        *reinterpret_cast<float4*>(out + r * N + c) =
+            make_float4(acc[i][h * 4], acc[i][h * 4 + 1], acc[i][h * 4 + 2], acc[i][h * 4 + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (c + j < N) out[r * N + c + j] = acc[i][h * 4 + j];
+      }
+    }
+  }
 }
 
 template <typename T>
@@ -267,13 +379,23 @@ int num_sms() {
 
 void k_matmul_exact(Dtype dt, const void* a, const void* w, void* out, int64_t rows, int64_t k,
                     int64_t n, cudaStream_t s) {
+  if (dt == Dtype::kF32) {
+    const bool vec = k % 4 == 0 && n % 4 == 0 &&
+                     (reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(out)) % 16 == 0;
+    const int64_t big = ((n + 127) / 128) * ((rows + 127) / 128);
+    if (big >= num_sms()) {  // 128x128 tiles fill the SMs: 8x8 outputs per thread
+      dim3 g(static_cast<unsigned>((n + 127) / 128), static_cast<unsigned>((rows + 127) / 128));
+      matmul_exact_f32_kernel<128, 128><<<g, 256, 0, s>>>(static_cast<const float*>(a), static_cast<const float*>(w),
+                                                          static_cast<float*>(out), rows, k, n, vec);
+    } else {
+      dim3 g(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((rows + 63) / 64));
+      matmul_exact_f32_kernel<64, 64><<<g, 256, 0, s>>>(static_cast<const float*>(a), static_cast<const float*>(w),
+                                                        static_cast<float*>(out), rows, k, n, vec);
+    }
+    return;
+  }
   dim3 grid(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((rows + 63) / 64));
-  if (dt == Dtype::kF32)
-    matmul_exact_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(a),
-                                                    static_cast<const float*>(w),
-                                                    static_cast<float*>(out), rows, k, n);
-  else
-    matmul_exact_kernel<int64_t><<<grid, 256, 0, s>>>(static_cast<const int64_t*>(a),
+  matmul_exact_kernel<int64_t><<<grid, 256, 0, s>>>(static_cast<const int64_t*>(a),
                                                       static_cast<const int64_t*>(w),
                                                       static_cast<int64_t*>(out), rows, k, n);
 }
