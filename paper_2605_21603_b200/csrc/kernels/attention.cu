@@ -87,6 +87,85 @@ __global__ void prefill_simt_kernel(const T* __restrict__ qkv, T* __restrict__ o
   }
 }
 
+// ------------------------------------------------- prefill (fp32, short sequences)
+// One CTA per (sequence, q head, row slice): the sequence's K and V rows of
+// the head's kv head staged once in shared memory (K rows padded to hd + 1
+// floats so lanes reading different keys hit different banks).  Each warp
+// takes query rows; per row the lanes split the keys (scores for keys
+// lane, lane + 32, ... <= row), one warp max / sum gives the softmax, the
+// probabilities go through a per-warp shared buffer and the lanes split
+// head_dim for P V.  Exact two-pass softmax per row (the SIMT kernel above
+// is online); both are within the fp32 tolerance of the fp64 oracle.  Used
+// when S <= 256, hd <= 128 and K / V fit in shared memory (the C1 toy:
+// S = 128, hd = 64).
+constexpr int kSmallWarps = 8;
+template <int MAXT>
+__global__ void __launch_bounds__(kSmallWarps * 32) prefill_small_f32_kernel(
+    const float* __restrict__ qkv, float* __restrict__ out, int nq, int nkv, int hd, int S, float scale,
+    int slices) {
+  extern __shared__ float sm[];
+  const int hdp = hd + 1;
+  float* ks = sm;                                  // [S][hd + 1]
+  float* vs = ks + static_cast<int64_t>(S) * hdp;  // [S][hd]
+  float* qs = vs + static_cast<int64_t>(S) * hd;   // [warps][hd]
+  float* ps = qs + kSmallWarps * hd;               // [warps][S]
+  const int seq = blockIdx.x / nq, h = blockIdx.x % nq, slice = blockIdx.y;
+  const int kh = h / (nq / nkv);
+  const int64_t W = static_cast<int64_t>(nq + 2 * nkv) * hd;
+  const float* base = qkv + static_cast<int64_t>(seq) * S * W;
+  // rows this CTA handles: slice, slice + slices, ...; keys needed: 0..last row
+  const int last = slice + ((S - 1 - slice) / slices) * slices;
+  for (int i = threadIdx.x; i < (last + 1) * hd; i += blockDim.x) {
+    const int j = i / hd, d = i % hd;
+    ks[j * hdp + d] = base[j * W + static_cast<int64_t>(nq + kh) * hd + d];
+    vs[j * hd + d] = base[j * W + static_cast<int64_t>(nq + nkv + kh) * hd + d];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float* q = qs + warp * hd;
+  float* p = ps + warp * S;
+  for (int r = slice + warp * slices; r < S; r += kSmallWarps * slices) {
+    for (int d = lane; d < hd; d += 32) q[d] = base[r * W + static_cast<int64_t>(h) * hd + d] * scale;
+    __syncwarp();
+    float sc[MAXT];
+    float m = -FLT_MAX;
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) {
+      const int j = lane + 32 * t;
+      float dot = -FLT_MAX;
+      if (j <= r) {
+        dot = 0.0f;
+        const float* kr = ks + j * hdp;
+        for (int d = 0; d < hd; ++d) dot += q[d] * kr[d];
+      }
+      sc[t] = dot;
+      m = fmaxf(m, dot);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float l = 0.0f;
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) {
+      const int j = lane + 32 * t;
+      if (j <= r) {
+        const float e = expf(sc[t] - m);
+        l += e;
+        p[j] = e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    __syncwarp();
+    const float inv = 1.0f / l;
+    for (int d = lane; d < hd; d += 32) {
+      float acc = 0.0f;
+      for (int j = 0; j <= r; ++j) acc += p[j] * vs[j * hd + d];
+      out[(static_cast<int64_t>(seq) * S + r) * nq * hd + static_cast<int64_t>(h) * hd + d] = acc * inv;
+    }
+    __syncwarp();  // q / p of this row are read before the next row overwrites them
+  }
+}
+
 // ---------------------------------------------------------------- decode (paged)
 constexpr int kDecWarps = 4;
 constexpr int kMaxGroup = 8;   // q heads per kv head
@@ -286,6 +365,33 @@ bool prefill_bf16_tcgen05(const __nv_bfloat16* qkv, __nv_bfloat16* out, int64_t 
 opf_status attn_prefill_simt(const opf_view& in, opf_view& out, int64_t rows, int nq, int nkv,
                              int hd, int S, cudaStream_t s) {
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
+  const size_t small_smem =
+      (static_cast<size_t>(S) * (2 * hd + 1) + static_cast<size_t>(kSmallWarps) * (hd + S)) * sizeof(float);
+  if (in.dtype == OPF_F32 && S <= 256 && hd <= 128 && small_smem <= 200 * 1024) {
+    // enough CTAs for the SMs: split each (sequence, head)'s rows into slices
+    const int64_t units = (rows / S) * nq;
+    int slices = 1;
+    while (slices < 16 && units * slices < 2 * num_sms() && S / (slices * 2) >= kSmallWarps) slices *= 2;
+    const dim3 grid(static_cast<unsigned>(units), static_cast<unsigned>(slices));
+    static const bool attr_ok = [] {  // every instantiation (they share one function-pointer type)
+      bool ok = true;
+      for (auto k : {prefill_small_f32_kernel<2>, prefill_small_f32_kernel<4>, prefill_small_f32_kernel<8>})
+        ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) == cudaSuccess;
+      return ok;
+    }();
+    if (!attr_ok) return op_error(Errc::SchedulerError, "attn_prefill_small_f32: shared-memory attribute");
+    auto launch = [&](auto kern) {
+      kern<<<grid, kSmallWarps * 32, small_smem, s>>>(vptr<float>(in), vptr<float>(out), nq, nkv, hd, S, scale,
+                                                      slices);
+    };
+    if (S <= 64)
+      launch(prefill_small_f32_kernel<2>);
+    else if (S <= 128)
+      launch(prefill_small_f32_kernel<4>);
+    else
+      launch(prefill_small_f32_kernel<8>);
+    return launch_status("attn_prefill_small_f32");
+  }
   const int64_t warps = rows * nq;
   const int threads = 128;
   const unsigned grid = static_cast<unsigned>((warps * 32 + threads - 1) / threads);

@@ -186,3 +186,42 @@ def test_prefill_budget_sweep_rows(cuda, S, nq, nkv, seqs):
             got = _prefill(t, nq, nkv, S, rows, max_ctas=cap)
             row_err = np.abs(got - want).max(axis=1) / (np.abs(want).max(axis=1) + 1e-6)
             assert row_err.max() < 5e-2, (cap, int(row_err.argmax()), float(row_err.max()))
+
+
+@pytest.mark.parametrize("S,nq,nkv,hd,seqs", [
+    (128, 8, 8, 64, 8),    # C1 toy shape (BASELINE configs[0]); 8 row slices per (sequence, head)
+    (128, 8, 2, 64, 3),    # GQA group 4
+    (64, 4, 1, 128, 5),    # S <= 64 form, hd 128
+    (256, 2, 2, 32, 2),    # S = 256 form, few units (16 slices)
+    (37, 3, 1, 48, 4),     # S and hd not multiples of 32 (partial lanes / key columns)
+    (1, 2, 1, 64, 6),      # one-token sequences
+    (512, 2, 1, 64, 2),    # beyond the shared-memory form: the online SIMT kernel
+])
+def test_prefill_fp32_vs_oracle(cuda, S, nq, nkv, hd, seqs):
+    """fp32 prefill (the C1 toy's path): the shared-memory short-sequence
+    kernel for S <= 256 and the online SIMT kernel beyond, vs the fp64 oracle
+    within the fp32 tolerance (rel <= 1e-4, BASELINE north_star); also a
+    nano-batch row slice (a whole number of sequences) of the same input."""
+    import torch
+    rng = np.random.default_rng(S * 13 + nq * 3 + hd)
+    rows = S * seqs
+    qkv = rng.uniform(-1, 1, (rows, (nq + 2 * nkv) * hd)).astype(np.float32)
+    want = oracle.attn_prefill(qkv.astype(np.float64), nq, nkv, hd, S)
+    op = {"name": "a", "kind": "Custom", "inputs": [], "outputs": [],
+          "attrs": {"custom_name": "attn_prefill",
+                    "params": {"heads": nq, "kv_heads": nkv, "head_dim": hd, "seq_len": S}}}
+    t = torch.from_numpy(qkv).cuda()
+    out = torch.full((rows, nq * hd), float("nan"), dtype=torch.float32, device="cuda")
+    of.launch(op, [t], [out], rows)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert np.isfinite(got).all()
+    assert rel_err(got, want) < 1e-4, rel_err(got, want)
+    row_err = np.abs(got - want).max(axis=1) / (np.abs(want).max(axis=1) + 1e-6)
+    assert row_err.max() < 1e-3, int(row_err.argmax())
+    if seqs > 1:  # rows of the later sequences only (an offset view, as a nano-batch)
+        lo = S * (seqs // 2)
+        out2 = torch.full((rows - lo, nq * hd), float("nan"), dtype=torch.float32, device="cuda")
+        of.launch(op, [t[lo:]], [out2], rows - lo)
+        torch.cuda.synchronize()
+        assert rel_err(out2.cpu().numpy(), want[lo:]) < 1e-4
