@@ -117,3 +117,23 @@ if which in ("all", "moe"):
         s.run()
 torch.cuda.synchronize()
 print("done", which)
+if which == "toy":  # BASELINE configs[0]: the fp32 toy decoder (exact stand-in MatMuls, short-sequence prefill)
+    from pathlib import Path
+    from paper_2605_21603_b200.workloads import llama_inputs
+    root = Path(__file__).resolve().parent.parent
+    desc = (root / "oracle" / "fixtures" / "toy_decoder_c1.json").read_text()
+    host = llama_inputs(desc, 1024, seed=2026)
+    g = of.build_graph(desc)
+    s = of.Session(g, of.partition(g, []), {"lanes": 1})
+    keep = {}
+    for t in g.description["tensors"]:
+        if t["role"] in ("input", "weight"):
+            keep[t["name"]] = torch.from_numpy(host[t["name"]]).to(dev)
+        elif t["role"] == "output":
+            keep[t["name"]] = torch.empty(t["shape"], dtype=torch.float32, device=dev)
+        else:
+            continue
+        s.bind(t["name"], keep[t["name"]])
+    for _ in range(2):
+        s.run()
+    torch.cuda.synchronize()
