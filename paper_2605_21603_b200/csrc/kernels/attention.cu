@@ -103,29 +103,42 @@ template <int MAXT>
 __global__ void __launch_bounds__(kSmallWarps * 32) prefill_small_f32_kernel(
     const float* __restrict__ qkv, float* __restrict__ out, int nq, int nkv, int hd, int S, float scale,
     int slices) {
-  extern __shared__ float sm[];
-  const int hdp = hd + 1;
-  float* ks = sm;                                  // [S][hd + 1]
-  float* vs = ks + static_cast<int64_t>(S) * hdp;  // [S][hd]
-  float* qs = vs + static_cast<int64_t>(S) * hd;   // [warps][hd]
-  float* ps = qs + kSmallWarps * hd;               // [warps][S]
+  extern __shared__ __align__(16) float sm[];
+  const int hdp = hd + 4;  // K row stride: 16-byte aligned, and 8 lanes' float4 reads of 8 rows hit 8 bank quads
+  const int S4 = (S + 3) & ~3;
+  float* ks = sm;                                  // [S][hd + 4]
+  float* vs = ks + static_cast<int64_t>(S) * hdp;  // [S rounded up to 4][hd], rows past `last` zero
+  float* qs = vs + static_cast<int64_t>(S4) * hd;  // [warps][hd]
+  float* ps = qs + kSmallWarps * hd;               // [warps][S rounded up to 4]
   const int seq = blockIdx.x / nq, h = blockIdx.x % nq, slice = blockIdx.y;
   const int kh = h / (nq / nkv);
   const int64_t W = static_cast<int64_t>(nq + 2 * nkv) * hd;
   const float* base = qkv + static_cast<int64_t>(seq) * S * W;
   // rows this CTA handles: slice, slice + slices, ...; keys needed: 0..last row
   const int last = slice + ((S - 1 - slice) / slices) * slices;
-  for (int i = threadIdx.x; i < (last + 1) * hd; i += blockDim.x) {
-    const int j = i / hd, d = i % hd;
-    ks[j * hdp + d] = base[j * W + static_cast<int64_t>(nq + kh) * hd + d];
-    vs[j * hd + d] = base[j * W + static_cast<int64_t>(nq + nkv + kh) * hd + d];
+  const int hd4 = hd / 4;
+  for (int i = threadIdx.x; i < S4 * hd4; i += blockDim.x) {
+    const int j = i / hd4, d = (i % hd4) * 4;
+    if (j <= last) {
+      const float* row = base + j * W;
+      *reinterpret_cast<float4*>(ks + j * hdp + d) =
+          *reinterpret_cast<const float4*>(row + static_cast<int64_t>(nq + kh) * hd + d);
+      *reinterpret_cast<float4*>(vs + j * hd + d) =
+          *reinterpret_cast<const float4*>(row + static_cast<int64_t>(nq + nkv + kh) * hd + d);
+    } else {  // P V reads whole float4s of p: the rows it touches past the last key must be finite (zero)
+      *reinterpret_cast<float4*>(vs + j * hd + d) = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    }
   }
   __syncthreads();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   float* q = qs + warp * hd;
-  float* p = ps + warp * S;
+  float* p = ps + warp * S4;
   for (int r = slice + warp * slices; r < S; r += kSmallWarps * slices) {
-    for (int d = lane; d < hd; d += 32) q[d] = base[r * W + static_cast<int64_t>(h) * hd + d] * scale;
+    for (int d = lane * 4; d < hd; d += 128) {
+      float4 v = *reinterpret_cast<const float4*>(base + r * W + static_cast<int64_t>(h) * hd + d);
+      v.x *= scale, v.y *= scale, v.z *= scale, v.w *= scale;
+      *reinterpret_cast<float4*>(q + d) = v;
+    }
     __syncwarp();
     float sc[MAXT];
     float m = -FLT_MAX;
@@ -136,7 +149,11 @@ __global__ void __launch_bounds__(kSmallWarps * 32) prefill_small_f32_kernel(
       if (j <= r) {
         dot = 0.0f;
         const float* kr = ks + j * hdp;
-        for (int d = 0; d < hd; ++d) dot += q[d] * kr[d];
+        for (int d = 0; d < hd; d += 4) {
+          const float4 q4 = *reinterpret_cast<const float4*>(q + d);  // broadcast
+          const float4 k4 = *reinterpret_cast<const float4*>(kr + d);
+          dot += q4.x * k4.x + q4.y * k4.y + q4.z * k4.z + q4.w * k4.w;
+        }
       }
       sc[t] = dot;
       m = fmaxf(m, dot);
@@ -147,8 +164,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32) prefill_small_f32_kernel(
 #pragma unroll
     for (int t = 0; t < MAXT; ++t) {
       const int j = lane + 32 * t;
-      if (j <= r) {
-        const float e = expf(sc[t] - m);
+      if (j < S4) {  // keys past the row (and the pad to 4) get probability 0
+        const float e = j <= r ? expf(sc[t] - m) : 0.0f;
         l += e;
         p[j] = e;
       }
@@ -157,9 +174,16 @@ __global__ void __launch_bounds__(kSmallWarps * 32) prefill_small_f32_kernel(
     for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
     __syncwarp();
     const float inv = 1.0f / l;
+    const int jn = (r + 4) & ~3;  // keys 0..r, rounded up to whole float4s of p (zeros past r)
     for (int d = lane; d < hd; d += 32) {
       float acc = 0.0f;
-      for (int j = 0; j <= r; ++j) acc += p[j] * vs[j * hd + d];
+      for (int j = 0; j < jn; j += 4) {
+        const float4 p4 = *reinterpret_cast<const float4*>(p + j);  // broadcast
+        acc += p4.x * vs[j * hd + d];
+        acc += p4.y * vs[(j + 1) * hd + d];
+        acc += p4.z * vs[(j + 2) * hd + d];
+        acc += p4.w * vs[(j + 3) * hd + d];
+      }
       out[(static_cast<int64_t>(seq) * S + r) * nq * hd + static_cast<int64_t>(h) * hd + d] = acc * inv;
     }
     __syncwarp();  // q / p of this row are read before the next row overwrites them
@@ -366,8 +390,10 @@ opf_status attn_prefill_simt(const opf_view& in, opf_view& out, int64_t rows, in
                              int hd, int S, cudaStream_t s) {
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
   const size_t small_smem =
-      (static_cast<size_t>(S) * (2 * hd + 1) + static_cast<size_t>(kSmallWarps) * (hd + S)) * sizeof(float);
-  if (in.dtype == OPF_F32 && S <= 256 && hd <= 128 && small_smem <= 200 * 1024) {
+      (static_cast<size_t>(S) * (hd + 4) + static_cast<size_t>((S + 3) & ~3) * hd +
+       static_cast<size_t>(kSmallWarps) * (hd + ((S + 3) & ~3))) * sizeof(float);
+  if (in.dtype == OPF_F32 && S <= 256 && hd <= 128 && hd % 4 == 0 && small_smem <= 200 * 1024 &&
+      (reinterpret_cast<uintptr_t>(vptr<float>(in)) | reinterpret_cast<uintptr_t>(vptr<float>(out))) % 16 == 0) {
     // enough CTAs for the SMs: split each (sequence, head)'s rows into slices
     const int64_t units = (rows / S) * nq;
     int slices = 1;
